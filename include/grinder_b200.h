@@ -1,0 +1,233 @@
+/*
+ * grinder_b200.h — C ABI of the B200-native partition-wise GNN training step.
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json's
+ * north_star: GriNNder's partition-wise full-graph training step
+ * (reference package `grinder`, /root/reference/pkg/src/grinder).  The
+ * reference has no FFI — its boundary is the Python API in training.py,
+ * plan.py and partition.py — so every entry point below names the Python
+ * function it replaces.  The Python package `paper_2605_11517_b200`
+ * binds these with ctypes and keeps the reference's
+ * function names, argument meaning and ValueError behaviour.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, int32/int64 sizes and leading
+ *     dimensions, and the CUDA stream passed as `void*` (a cudaStream_t).
+ *   - Return value: 0 = ok, < 0 = argument error, > 0 = cudaError_t.
+ *     grd_last_error() returns a thread-local message for the last failure.
+ *   - Ownership: the caller allocates every buffer (device buffers come from
+ *     torch's caching allocator); the library never frees caller memory.
+ *     Opaque handles (grd_plan_*) own host memory until *_destroy.
+ *   - Device calls are asynchronous on the given stream and re-entrant; the
+ *     caller synchronises.  All reductions use fixed orders: no float
+ *     atomics, so every result is bitwise reproducible run to run.
+ *   - Dense row-major fp32 matrices carry a leading dimension (ld, elements);
+ *     activation buffers are padded to ld = round_up(width, 4) with zero
+ *     padding columns so rows are 16-byte aligned for 128-bit accesses.
+ */
+#ifndef GRINDER_B200_H
+#define GRINDER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRD_ABI_VERSION 1
+
+int grd_abi_version(void);
+const char* grd_last_error(void);
+/* Number of SMs of the current device (for grid sizing by the host side). */
+int grd_device_sm_count(int32_t* sm_count);
+
+/* ------------------------------------------------------------------------
+ * Host-side preprocessing (runs on CPU cores; no GPU needed).
+ * --------------------------------------------------------------------- */
+
+/* Symmetric Kronecker/RMAT graph, bit-exact with
+ * graph.py:158-209 generate_kronecker(scale, avg_degree, seed).
+ * `pcg_state` = {state_hi, state_lo, inc_hi, inc_lo} of
+ * numpy.random.PCG64(seed) (the stream numpy would draw from) and `cum` the
+ * f64 cumulative initiator np.cumsum((0.57,0.19,0.19,0.05)).  Writes CSR
+ * src_ptr[2^scale + 1] and dst_idx[<= dst_capacity]; *num_edges_out gets |E|. */
+int grd_kronecker_generate(int32_t scale, int64_t avg_degree,
+                           const uint64_t* pcg_state, const double* cum,
+                           int64_t* src_ptr, int32_t* dst_idx,
+                           int64_t dst_capacity, int64_t* num_edges_out,
+                           int32_t num_threads);
+
+/* Switching-aware partitioner, bit-exact with partition.py:254-321
+ * switching_aware_partition (its numba kernels _analyze_kernel :140-200 and
+ * _relocate_kernel :203-251).  `labels` holds random_partition()'s labels on
+ * entry (partition.py:103-111, drawn by numpy on the host) and the final
+ * labels on exit.  objective_trace needs max_iters slots, max_size_trace
+ * max_iters + 1. */
+typedef struct grd_partitioner_params {
+    double alpha_balance;
+    double beta;
+    double epsilon;
+    int32_t patience;
+    int32_t group_depth;
+    int32_t max_iters;
+    int32_t reserved;
+} grd_partitioner_params;
+
+int grd_sa_partition(int64_t num_vertices, const int64_t* src_ptr,
+                     const int32_t* dst_idx, int32_t num_partitions,
+                     const grd_partitioner_params* params, int32_t* labels,
+                     double* objective_trace, int64_t* max_size_trace,
+                     double* initial_objective, int32_t* iterations,
+                     int32_t* converged, int32_t num_threads);
+
+/* Partition plan, bit-exact with plan.py:75-136 build_partition_plan.
+ * Layout (concatenated over partitions in ascending id):
+ *   part_ptr[P+1]        offsets of each partition's targets in perm
+ *   perm[V]              targets of partition 0 ascending, then 1, ...
+ *   in_ptr[V+1]          edge offsets per perm row (== concatenated tgt_ptr)
+ *   in_src[E]            global source vertex of each edge
+ *   in_src_pos[E]        its gather-map position (== src_pos)
+ *   gather_ptr[P+1]      offsets of each partition's gather map
+ *   gather_map[sum G]    gather maps, each sorted by (owner, vertex id)
+ *   self_pos[V]          gather position of each target (perm order)
+ *   in_degree[V]         global in-degree per vertex
+ * Edges of one target are ordered by ascending gather position. */
+typedef struct grd_plan grd_plan;
+int grd_plan_create(int64_t num_vertices, const int64_t* src_ptr,
+                    const int32_t* dst_idx, const int32_t* labels,
+                    int32_t num_partitions, int32_t num_threads,
+                    grd_plan** plan_out);
+int grd_plan_sizes(const grd_plan* plan, int64_t* num_edges,
+                   int64_t* gather_total);
+int grd_plan_export(const grd_plan* plan, int64_t* part_ptr, int32_t* perm,
+                    int64_t* in_ptr, int32_t* in_src, int32_t* in_src_pos,
+                    int64_t* gather_ptr, int32_t* gather_map,
+                    int32_t* self_pos, int32_t* in_degree);
+void grd_plan_destroy(grd_plan* plan);
+
+/* ------------------------------------------------------------------------
+ * Device kernels (sm_100a).  All take `stream` = cudaStream_t.
+ * --------------------------------------------------------------------- */
+
+/* K1 — row gather: dst[i,:] = src[idx[i],:]  (training.py:301,330
+ * `acts[layer][topo.gather_map]`). */
+int grd_gather_rows(const float* src, int64_t ld_src, const int32_t* idx,
+                    int64_t n_rows, int32_t width, float* dst, int64_t ld_dst,
+                    void* stream);
+
+/* K9 — row scatter-add: dst[idx[i],:] += src[i,:] (training.py:166-175
+ * scatter_accumulate; idx is duplicate-free). */
+int grd_scatter_add_rows(const float* src, int64_t ld_src,
+                         const int32_t* idx, int64_t n_rows, int32_t width,
+                         float* dst, int64_t ld_dst, void* stream);
+
+/* K2/K8 — CSR sum-aggregation (SpMM pull), one warp per row:
+ *   s   = sum_{e in [row_ptr[r], row_ptr[r+1])} src_scale[idx[e]] * Y[idx[e],:]
+ *       + src_scale[self] * Y[self,:]            (self = self_idx[r] or out row)
+ *   out[out_row,:] = act( post(s) )
+ * post: divide by (row degree + 1) (mean, training.py:61-65) and/or multiply
+ * by post_scale[out_row] (symmetric norm).  Rows whose degree exceeds
+ * heavy_threshold are split into fixed segments (heavy_* arrays) whose
+ * partials are combined in segment order by the last finishing warp, so the
+ * result is deterministic.  Forward aggregation (training.py:48-58), its
+ * backward recompute (:113-114) and the transposed aggregation (:130-143,
+ * pulled over a CSC/CSR of the opposite direction) all map onto this. */
+typedef struct grd_agg_args {
+    int64_t n_rows;
+    const int64_t* row_ptr;
+    const int32_t* idx;
+    const int32_t* out_idx;    /* nullable: output row of row r (else r)  */
+    const int32_t* self_idx;   /* nullable: self row (else out row); <0 none */
+    const float* y;
+    int64_t ldy;
+    const float* src_scale;    /* nullable: per-Y-row multiplier           */
+    const float* post_scale;   /* nullable: per-output-row multiplier      */
+    int32_t post_div_deg;      /* divide by (degree + 1)                   */
+    int32_t relu;
+    float* out;
+    int64_t ldo;
+    int32_t width;
+    int32_t heavy_threshold;   /* <= 0: no splitting                       */
+    int64_t n_heavy;
+    const int32_t* heavy_rows;     /* [n_heavy] row indices                */
+    const int64_t* heavy_seg_ptr;  /* [n_heavy+1] segment offsets          */
+    const int32_t* seg_heavy;      /* [n_segs] owning heavy index          */
+    int64_t n_segs;
+    int32_t seg_len;               /* edges per segment                    */
+    int32_t reserved;
+    float* seg_partial;            /* [n_segs * round_up(width,4)] scratch */
+    int32_t* heavy_counter;        /* [n_heavy] zero on entry, zero on exit */
+    const float* mask_ref;         /* nullable: out = mask_ref[out_row,:] > 0 ? out : 0 */
+    int64_t ld_mask_ref;
+} grd_agg_args;
+int grd_agg_sum(const grd_agg_args* args, void* stream);
+
+/* K3/K6/K7 — dense fp32 GEMM with fused epilogue (training.py:76,128-129):
+ *   C[m,n] = epi( sum_k opA(A)[m,k] * opB(B)[k,n] )
+ * transA: A stored K x M (lda);  transB: B stored N x K (ldb).
+ * epi: acc *= row_scale[m]; acc *= col_mul[m,n] (ldcm); acc = relu_ref[m,n]>0 ? acc : 0;
+ * then C = acc (accumulate=0) or C += acc.  Pointers are nullable. */
+typedef struct grd_gemm_args {
+    int64_t m, n, k;
+    const float* a; int64_t lda; int32_t trans_a;
+    int32_t trans_b;
+    const float* b; int64_t ldb;
+    float* c; int64_t ldc;
+    const float* row_scale;
+    const float* elem_mul; int64_t ld_elem_mul;
+    const float* relu_ref; int64_t ld_relu_ref;
+    int32_t relu_out;          /* apply max(acc, 0) */
+    int32_t accumulate;
+} grd_gemm_args;
+int grd_gemm(const grd_gemm_args* args, void* stream);
+
+/* K6 — weight gradient  dW = A^T B  with K = number of rows (long), as a
+ * deterministic split-K: fixed row chunks write partials to `workspace`
+ * ([splits, M, N]), then one ordered reduction writes dW (or adds to it when
+ * `accumulate`, the ascending-pid sum of training.py:343) and, if w is
+ * non-null, applies the SGD step W -= lr * dW (training.py:352-354).
+ * workspace_elems must be >= grd_wgrad_workspace(m, n, k). */
+int64_t grd_wgrad_workspace(int64_t m, int64_t n, int64_t k);
+int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a,
+                  int64_t lda, const float* b, int64_t ldb, float* dw,
+                  int64_t lddw, int32_t accumulate, float* w, int64_t ldw,
+                  float lr, float* workspace, int64_t workspace_elems,
+                  void* stream);
+
+/* K4 — masked softmax cross-entropy (model.py:102-129): per masked row,
+ * loss -= log softmax(logits)[label]; grad = (softmax - onehot) / count *
+ * grad_scale[row] (grad_scale nullable); unmasked rows get zero gradient.
+ * stats_out (device, 4 doubles): {loss, accuracy, loss_sum, correct}.
+ * `partials` needs grd_loss_partials(n_rows) doubles of scratch. */
+int64_t grd_loss_partials(int64_t n_rows);
+int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t n_rows,
+                     int32_t n_classes, const int32_t* labels,
+                     const uint8_t* mask, int64_t mask_count,
+                     float* grad, int64_t ld_grad, const float* grad_scale,
+                     double* partials, double* stats_out, void* stream);
+
+/* Elementwise helpers. */
+/* y[i,:] = x[i,:] * m[i,:]  (dropout, training.py:178-185,297). */
+int grd_mul_rows(const float* x, int64_t ldx, const float* m, int64_t ldm,
+                 int64_t n_rows, int32_t width, float* y, int64_t ldy,
+                 void* stream);
+/* y[i,:] = (ref[i,:] > 0 ? x[i,:] : 0) * row_scale[i]  (ReLU derivative
+ * mask and degree scale, training.py:115-118,130-139); ref/row_scale
+ * nullable; in-place allowed. */
+int grd_mask_scale_rows(const float* x, int64_t ldx, const float* ref,
+                        int64_t ldref, const float* row_scale, int64_t n_rows,
+                        int32_t width, float* y, int64_t ldy, void* stream);
+/* Row-L2 normalisation forward / backward (training.py:75-80,119-127). */
+int grd_rownorm_fwd(const float* pre, int64_t ld, int64_t n_rows,
+                    int32_t width, int32_t relu, const int32_t* out_idx,
+                    float* out, int64_t ldo, void* stream);
+int grd_rownorm_bwd(const float* pre, int64_t ldp, const float* grad_y,
+                    int64_t ldg, const float* a_out, int64_t lda,
+                    int64_t n_rows, int32_t width, const float* row_scale,
+                    float* grad_pre, int64_t ldgp, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRINDER_B200_H */

@@ -1,0 +1,721 @@
+// sm_100a device kernels of the partition-wise GCN training step and their
+// extern "C" launchers (include/grinder_b200.h).
+//
+//   K1  gather_rows        training.py:301,330   acts[layer][gather_map]
+//   K2  agg_sum            training.py:38-65     neighbour sum + self, normalise
+//   K8  agg_sum (pull)     training.py:130-143   transposed aggregation
+//   K9  scatter_add_rows   training.py:166-175   global_grad[gather_map] += grad_GA
+//   K3/K6/K7 gemm          training.py:76,128-129 dense transform / dgrad
+//   K6  wgrad_sgd          training.py:128,343,352-354 split-K dW + SGD
+//   K4  softmax_xent       model.py:102-129      masked softmax-CE + accuracy
+//
+// Every reduction runs in a fixed order (no float atomics), so results are
+// bitwise reproducible and independent of partition schedule.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/grinder_b200.h"
+#include "grd_common.h"
+
+using namespace grd;
+
+namespace {
+
+constexpr int kWarp = 32;
+
+inline int launch_status(const char* what) {
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(static_cast<int>(err), "%s: %s", what, cudaGetErrorString(err));
+    return 0;
+}
+
+__device__ __forceinline__ float4 f4_fma(float s, const float4 v, float4 a) {
+    a.x = fmaf(s, v.x, a.x);
+    a.y = fmaf(s, v.y, a.y);
+    a.z = fmaf(s, v.z, a.z);
+    a.w = fmaf(s, v.w, a.w);
+    return a;
+}
+__device__ __forceinline__ float4 f4_add(float4 a, const float4 b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    return a;
+}
+__device__ __forceinline__ float4 f4_shfl_xor(float4 v, int off) {
+    v.x = __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y = __shfl_xor_sync(0xffffffffu, v.y, off);
+    v.z = __shfl_xor_sync(0xffffffffu, v.z, off);
+    v.w = __shfl_xor_sync(0xffffffffu, v.w, off);
+    return v;
+}
+__device__ __forceinline__ float4 ld_nc_f4(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// ------------------------------------------------------------------- K2 --
+// Warp per row (or per heavy-row segment).  The warp is split into
+// NG = 32/LPR lane groups; a group owns one edge at a time and each lane of
+// the group holds NV float4 column chunks of the row.  U edges per group are
+// loaded before they are summed to keep U*NG row reads in flight per warp.
+template <int LPR, int NV, int U>
+__device__ __forceinline__ void agg_accumulate(const grd_agg_args& a, int64_t beg, int64_t end,
+                                               int lane, int w4, float4 (&acc)[NV]) {
+    constexpr int NG = kWarp / LPR;
+    const int g = lane / LPR;
+    const int sub = lane % LPR;
+    const float* __restrict__ y = a.y;
+    const int32_t* __restrict__ idx = a.idx;
+    const float* __restrict__ ss = a.src_scale;
+    int64_t e = beg + g;
+    for (; e + int64_t(U - 1) * NG < end; e += int64_t(U) * NG) {
+        int32_t j[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = __ldg(idx + e + int64_t(u) * NG);
+        float4 v[U][NV];
+        float s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            s[u] = ss ? __ldg(ss + j[u]) : 1.0f;
+            const float* row = y + int64_t(j[u]) * a.ldy;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                const int q = sub + c * LPR;
+                v[u][c] = q < w4 ? ld_nc_f4(row + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[u], v[u][c], acc[c]);
+    }
+    for (; e < end; e += NG) {
+        const int32_t jj = __ldg(idx + e);
+        const float s = ss ? __ldg(ss + jj) : 1.0f;
+        const float* row = y + int64_t(jj) * a.ldy;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) acc[c] = f4_fma(s, ld_nc_f4(row + 4 * q), acc[c]);
+        }
+    }
+    // Fixed-order butterfly across lane groups.
+#pragma unroll
+    for (int off = kWarp / 2; off >= LPR; off >>= 1)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] = f4_add(acc[c], f4_shfl_xor(acc[c], off));
+}
+
+template <int LPR, int NV>
+__device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg,
+                                           int lane, int w4, float4 (&acc)[NV]) {
+    const int sub = lane % LPR;
+    const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
+    const int32_t srow = a.self_idx ? a.self_idx[r] : orow;
+    if (srow >= 0) {
+        const float s = a.src_scale ? a.src_scale[srow] : 1.0f;
+        const float* row = a.y + int64_t(srow) * a.ldy;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) acc[c] = f4_fma(s, ld_nc_f4(row + 4 * q), acc[c]);
+        }
+    }
+    const float div = static_cast<float>(deg + 1);
+    const float ps = a.post_scale ? a.post_scale[orow] : 1.0f;
+    if (lane >= LPR) return;
+    float* out = a.out + int64_t(orow) * a.ldo;
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = sub + c * LPR;
+        if (q >= w4) continue;
+        float4 v = acc[c];
+        if (a.post_div_deg) { v.x /= div; v.y /= div; v.z /= div; v.w /= div; }
+        if (a.post_scale) { v.x *= ps; v.y *= ps; v.z *= ps; v.w *= ps; }
+        if (a.relu) {
+            v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+        }
+        if (a.mask_ref) {
+            const float4 m = ld_nc_f4(a.mask_ref + int64_t(orow) * a.ld_mask_ref + 4 * q);
+            if (!(m.x > 0.f)) v.x = 0.f;
+            if (!(m.y > 0.f)) v.y = 0.f;
+            if (!(m.z > 0.f)) v.z = 0.f;
+            if (!(m.w > 0.f)) v.w = 0.f;
+        }
+        *reinterpret_cast<float4*>(out + 4 * q) = v;
+    }
+}
+
+template <int LPR, int NV, int U>
+__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const int w4 = (a.width + 3) / 4;
+    float4 acc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    if (item < a.n_rows) {
+        const int64_t r = item;
+        const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
+        if (a.heavy_threshold > 0 && end - beg > a.heavy_threshold) return;  // segmented
+        agg_accumulate<LPR, NV, U>(a, beg, end, lane, w4, acc);
+        agg_finish<LPR, NV>(a, r, end - beg, lane, w4, acc);
+        return;
+    }
+    const int64_t s = item - a.n_rows;
+    if (s >= a.n_segs) return;
+    const int32_t h = a.seg_heavy[s];
+    const int64_t r = a.heavy_rows[h];
+    const int64_t seg0 = a.heavy_seg_ptr[h], nseg = a.heavy_seg_ptr[h + 1] - seg0;
+    const int64_t rb = a.row_ptr[r], re = a.row_ptr[r + 1];
+    const int64_t beg = rb + (s - seg0) * a.seg_len;
+    const int64_t end = min(beg + int64_t(a.seg_len), re);
+    agg_accumulate<LPR, NV, U>(a, beg, end, lane, w4, acc);
+    const int ldp = 4 * w4;
+    const int sub = lane % LPR;
+    if (lane < LPR) {
+        float* part = a.seg_partial + s * ldp;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) __stcg(reinterpret_cast<float4*>(part + 4 * q), acc[c]);
+        }
+    }
+    __threadfence();
+    __syncwarp();
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(a.heavy_counter + h, 1);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket != nseg - 1) return;
+    // Last segment to finish: combine partials in segment order.
+    __threadfence();
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t t = 0; t < nseg; ++t) {
+        const float* part = a.seg_partial + (seg0 + t) * ldp;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) acc[c] = f4_add(acc[c], __ldcg(reinterpret_cast<const float4*>(part + 4 * q)));
+        }
+    }
+    agg_finish<LPR, NV>(a, r, re - rb, lane, w4, acc);
+    if (lane == 0) a.heavy_counter[h] = 0;
+}
+
+template <int LPR, int NV, int U>
+int launch_agg(const grd_agg_args& a, cudaStream_t st) {
+    const int64_t items = a.n_rows + a.n_segs;
+    if (items == 0) return 0;
+    const int64_t blocks = (items * kWarp + 255) / 256;
+    agg_sum_kernel<LPR, NV, U><<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+    return launch_status("agg_sum");
+}
+
+// ------------------------------------------------------------ K1 / K9 --
+template <bool kAdd>
+__global__ void __launch_bounds__(256) row_copy_kernel(const float* __restrict__ src, int64_t lds,
+                                                       const int32_t* __restrict__ idx, int64_t n_rows,
+                                                       int w4, float* __restrict__ dst, int64_t ldd) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (r >= n_rows) return;
+    const int32_t j = idx[r];
+    if (kAdd) {
+        const float* s = src + r * lds;
+        float* d = dst + int64_t(j) * ldd;
+        for (int q = lane; q < w4; q += kWarp) {
+            float4 v = *reinterpret_cast<float4*>(d + 4 * q);
+            v = f4_add(v, ld_nc_f4(s + 4 * q));
+            *reinterpret_cast<float4*>(d + 4 * q) = v;
+        }
+    } else {
+        const float* s = src + int64_t(j) * lds;
+        float* d = dst + r * ldd;
+        for (int q = lane; q < w4; q += kWarp)
+            *reinterpret_cast<float4*>(d + 4 * q) = ld_nc_f4(s + 4 * q);
+    }
+}
+
+// ----------------------------------------------------------- K3/K6/K7 --
+// Tiled fp32 SIMT GEMM (CUDA-core FMA path; fp32-exact products).
+constexpr int kBM = 128, kBN = 64, kBK = 16, kTM = 8, kTN = 4;
+constexpr int kGemmThreads = (kBM / kTM) * (kBN / kTN);  // 256
+
+struct GemmTile {
+    int64_t m, n, k, k0, k1;
+    const float* a; int64_t lda; bool ta;
+    const float* b; int64_t ldb; bool tb;
+};
+
+__device__ __forceinline__ void gemm_mainloop(const GemmTile& t, int64_t m0, int64_t n0,
+                                              float (&acc)[kTM][kTN]) {
+    __shared__ __align__(16) float As[2][kBK][kBM];
+    __shared__ __align__(16) float Bs[2][kBK][kBN];
+    const int tid = threadIdx.x;
+    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
+    // Per-thread load assignments: A tile = 128x16 = 2048 floats (8/thread),
+    // B tile = 16x64 = 1024 floats (4/thread).
+    float ra[8], rb[4];
+    auto load_a = [&](int64_t kb) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int li = tid + i * kGemmThreads;
+            int mm, kk;
+            if (!t.ta) { mm = li / kBK; kk = li % kBK; }   // row-major: k fastest
+            else       { kk = li / kBM; mm = li % kBM; }   // K x M: m fastest
+            const int64_t gm = m0 + mm, gk = kb + kk;
+            float v = 0.f;
+            if (gm < t.m && gk < t.k1)
+                v = t.ta ? __ldg(t.a + gk * t.lda + gm) : __ldg(t.a + gm * t.lda + gk);
+            ra[i] = v;
+        }
+    };
+    auto store_a = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int li = tid + i * kGemmThreads;
+            int mm, kk;
+            if (!t.ta) { mm = li / kBK; kk = li % kBK; }
+            else       { kk = li / kBM; mm = li % kBM; }
+            As[buf][kk][mm] = ra[i];
+        }
+    };
+    auto load_b = [&](int64_t kb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int li = tid + i * kGemmThreads;
+            int kk, nn;
+            if (!t.tb) { kk = li / kBN; nn = li % kBN; }   // K x N: n fastest
+            else       { nn = li / kBK; kk = li % kBK; }   // N x K: k fastest
+            const int64_t gk = kb + kk, gn = n0 + nn;
+            float v = 0.f;
+            if (gn < t.n && gk < t.k1)
+                v = t.tb ? __ldg(t.b + gn * t.ldb + gk) : __ldg(t.b + gk * t.ldb + gn);
+            rb[i] = v;
+        }
+    };
+    auto store_b = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int li = tid + i * kGemmThreads;
+            int kk, nn;
+            if (!t.tb) { kk = li / kBN; nn = li % kBN; }
+            else       { nn = li / kBK; kk = li % kBK; }
+            Bs[buf][kk][nn] = rb[i];
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < kTM; ++i)
+#pragma unroll
+        for (int j = 0; j < kTN; ++j) acc[i][j] = 0.f;
+    if (t.k0 >= t.k1) return;
+    load_a(t.k0);
+    load_b(t.k0);
+    store_a(0);
+    store_b(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t kb = t.k0; kb < t.k1; kb += kBK) {
+        const bool more = kb + kBK < t.k1;
+        if (more) { load_a(kb + kBK); load_b(kb + kBK); }
+#pragma unroll
+        for (int kk = 0; kk < kBK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * kTM]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * kTM + 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * kTN]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[4] = {b0.x, b0.y, b0.z, b0.w};
+#pragma unroll
+            for (int i = 0; i < kTM; ++i)
+#pragma unroll
+                for (int j = 0; j < kTN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+        if (more) {
+            store_a(buf ^ 1);
+            store_b(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kGemmThreads) gemm_kernel(const grd_gemm_args g) {
+    const int64_t m0 = int64_t(blockIdx.x) * kBM, n0 = int64_t(blockIdx.y) * kBN;
+    GemmTile t{g.m, g.n, g.k, 0, g.k, g.a, g.lda, g.trans_a != 0, g.b, g.ldb, g.trans_b != 0};
+    float acc[kTM][kTN];
+    gemm_mainloop(t, m0, n0, acc);
+    const int tid = threadIdx.x;
+    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+        const int64_t m = m0 + ty * kTM + i;
+        if (m >= g.m) continue;
+        const float rs = g.row_scale ? g.row_scale[m] : 1.0f;
+#pragma unroll
+        for (int j = 0; j < kTN; ++j) {
+            const int64_t n = n0 + tx * kTN + j;
+            if (n >= g.n) continue;
+            float v = acc[i][j];
+            if (g.row_scale) v *= rs;
+            if (g.elem_mul) v *= g.elem_mul[m * g.ld_elem_mul + n];
+            if (g.relu_ref && !(g.relu_ref[m * g.ld_relu_ref + n] > 0.f)) v = 0.f;
+            if (g.relu_out) v = fmaxf(v, 0.f);
+            float* c = g.c + m * g.ldc + n;
+            *c = g.accumulate ? *c + v : v;
+        }
+    }
+}
+
+// Split-K weight gradient: blockIdx.z selects a fixed K chunk.
+__global__ void __launch_bounds__(kGemmThreads) wgrad_partial_kernel(
+        int64_t m, int64_t n, int64_t k, int64_t kchunk, const float* a, int64_t lda,
+        const float* b, int64_t ldb, float* ws) {
+    const int64_t m0 = int64_t(blockIdx.x) * kBM, n0 = int64_t(blockIdx.y) * kBN;
+    const int64_t k0 = int64_t(blockIdx.z) * kchunk;
+    GemmTile t{m, n, k, k0, min(k0 + kchunk, k), a, lda, true, b, ldb, false};
+    float acc[kTM][kTN];
+    gemm_mainloop(t, m0, n0, acc);
+    float* out = ws + int64_t(blockIdx.z) * m * n;
+    const int tid = threadIdx.x;
+    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+        const int64_t mm = m0 + ty * kTM + i;
+        if (mm >= m) continue;
+#pragma unroll
+        for (int j = 0; j < kTN; ++j) {
+            const int64_t nn = n0 + tx * kTN + j;
+            if (nn < n) out[mm * n + nn] = acc[i][j];
+        }
+    }
+}
+
+__global__ void wgrad_reduce_kernel(int64_t m, int64_t n, int64_t splits, const float* ws,
+                                    float* dw, int64_t lddw, int accumulate, float* w, int64_t ldw,
+                                    float lr) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m * n) return;
+    float s = 0.f;
+    for (int64_t z = 0; z < splits; ++z) s += ws[z * m * n + i];
+    const int64_t r = i / n, c = i % n;
+    if (accumulate) s += dw[r * lddw + c];
+    dw[r * lddw + c] = s;
+    if (w) w[r * ldw + c] -= lr * s;
+}
+
+int64_t wgrad_splits(int64_t m, int64_t n, int64_t k) {
+    const int64_t tiles = ((m + kBM - 1) / kBM) * ((n + kBN - 1) / kBN);
+    int64_t splits = (296 + tiles - 1) / tiles;
+    const int64_t max_splits = (k + 511) / 512;
+    if (splits > max_splits) splits = max_splits;
+    if (splits < 1) splits = 1;
+    return splits;
+}
+
+// -------------------------------------------------------------------- K4 --
+constexpr int kLossBlocks = 1184;  // 148 SMs x 8
+
+__global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ logits, int64_t ldl,
+                                                   int64_t n_rows, int c, const int32_t* __restrict__ labels,
+                                                   const uint8_t* __restrict__ mask, float inv_count,
+                                                   float* __restrict__ grad, int64_t ldg,
+                                                   const float* __restrict__ gscale, double* partials) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x / kWarp;
+    double loss_acc = 0.0;
+    double correct = 0.0;
+    const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / kWarp);
+    for (int64_t r = int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows; r += nwarps) {
+        const float* row = logits + r * ldl;
+        float* grow = grad + r * ldg;
+        if (!mask[r]) {
+            for (int j = lane; j < c; j += kWarp) grow[j] = 0.f;
+            continue;
+        }
+        // max and first argmax (np.argmax semantics)
+        float mx = -INFINITY;
+        int arg = 0x7fffffff;
+        for (int j = lane; j < c; j += kWarp) {
+            const float v = row[j];
+            if (v > mx || (v == mx && j < arg)) { mx = v; arg = j; }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, mx, off);
+            const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+            if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+        }
+        float sum = 0.f;
+        for (int j = lane; j < c; j += kWarp) sum += expf(row[j] - mx);
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        const int y = labels[r];
+        const float scale = gscale ? gscale[r] : 1.0f;
+        for (int j = lane; j < c; j += kWarp) {
+            float p = expf(row[j] - mx) / sum;
+            if (j == y) p -= 1.0f;
+            grow[j] = p * inv_count * scale;
+        }
+        if (lane == 0) {
+            const float py = expf(row[y] - mx) / sum;
+            loss_acc -= static_cast<double>(logf(py));
+            correct += (arg == y) ? 1.0 : 0.0;
+        }
+    }
+    __shared__ double sl[8], sc[8];
+    if (lane == 0) { sl[warp] = loss_acc; sc[warp] = correct; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / kWarp); ++w) { a += sl[w]; b += sc[w]; }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+}
+
+__global__ void xent_finalize_kernel(const double* partials, int nblocks, double count, double* stats) {
+    if (threadIdx.x != 0) return;
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nblocks; ++i) { a += partials[2 * i]; b += partials[2 * i + 1]; }
+    stats[0] = a / count;
+    stats[1] = b / count;
+    stats[2] = a;
+    stats[3] = b;
+}
+
+// ------------------------------------------------------------ helpers --
+__global__ void mul_rows_kernel(const float* x, int64_t ldx, const float* m, int64_t ldm, int64_t n_rows,
+                                int width, float* y, int64_t ldy) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * width) return;
+    const int64_t r = i / width, c = i % width;
+    y[r * ldy + c] = x[r * ldx + c] * m[r * ldm + c];
+}
+
+__global__ void mask_scale_rows_kernel(const float* x, int64_t ldx, const float* ref, int64_t ldref,
+                                       const float* row_scale, int64_t n_rows, int width, float* y,
+                                       int64_t ldy) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * width) return;
+    const int64_t r = i / width, c = i % width;
+    float v = x[r * ldx + c];
+    if (ref && !(ref[r * ldref + c] > 0.f)) v = 0.f;
+    if (row_scale) v *= row_scale[r];
+    y[r * ldy + c] = v;
+}
+
+__global__ void rownorm_fwd_kernel(const float* pre, int64_t ld, int64_t n_rows, int width, int relu,
+                                   const int32_t* out_idx, float* out, int64_t ldo) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (r >= n_rows) return;
+    const float* p = pre + r * ld;
+    float ss = 0.f;
+    for (int j = lane; j < width; j += kWarp) ss = fmaf(p[j], p[j], ss);
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float nrm = sqrtf(ss);
+    float* o = out + int64_t(out_idx ? out_idx[r] : r) * ldo;
+    for (int j = lane; j < width; j += kWarp) {
+        float v = nrm > 0.f ? p[j] / nrm : 0.f;
+        if (relu) v = fmaxf(v, 0.f);
+        o[j] = v;
+    }
+}
+
+__global__ void rownorm_bwd_kernel(const float* pre, int64_t ldp, const float* gy, int64_t ldg,
+                                   const float* a_out, int64_t lda, int64_t n_rows, int width,
+                                   const float* row_scale, float* gp, int64_t ldgp) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (r >= n_rows) return;
+    const float* p = pre + r * ldp;
+    const float* g = gy + r * ldg;
+    const float* ao = a_out ? a_out + r * lda : nullptr;
+    float ss = 0.f;
+    for (int j = lane; j < width; j += kWarp) ss = fmaf(p[j], p[j], ss);
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float nrm = sqrtf(ss);
+    float inner = 0.f;
+    for (int j = lane; j < width; j += kWarp) {
+        const float u = nrm > 0.f ? p[j] / nrm : 0.f;
+        const float gj = (ao && !(ao[j] > 0.f)) ? 0.f : g[j];
+        inner = fmaf(u, gj, inner);
+    }
+    for (int off = 16; off > 0; off >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, off);
+    const float rs = row_scale ? row_scale[r] : 1.0f;
+    float* o = gp + r * ldgp;
+    for (int j = lane; j < width; j += kWarp) {
+        const float u = nrm > 0.f ? p[j] / nrm : 0.f;
+        const float gj = (ao && !(ao[j] > 0.f)) ? 0.f : g[j];
+        const float v = nrm > 0.f ? (gj - u * inner) / nrm : 0.f;
+        o[j] = v * rs;
+    }
+}
+
+inline unsigned blocks_for(int64_t threads, int per_block = 256) {
+    return static_cast<unsigned>((threads + per_block - 1) / per_block);
+}
+
+}  // namespace
+
+// =====================================================================
+// extern "C" launchers
+// =====================================================================
+extern "C" int grd_device_sm_count(int32_t* sm_count) {
+    clear_error();
+    int dev = 0, v = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "sm count: %s", cudaGetErrorString(e));
+    *sm_count = v;
+    return 0;
+}
+
+extern "C" int grd_gather_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n_rows,
+                               int32_t width, float* dst, int64_t ld_dst, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!src || !idx || !dst || width <= 0 || ld_src % 4 || ld_dst % 4)
+        return fail(kErrArg, "gather_rows: bad arguments");
+    row_copy_kernel<false><<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst);
+    return launch_status("gather_rows");
+}
+
+extern "C" int grd_scatter_add_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n_rows,
+                                    int32_t width, float* dst, int64_t ld_dst, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!src || !idx || !dst || width <= 0 || ld_src % 4 || ld_dst % 4)
+        return fail(kErrArg, "scatter_add_rows: bad arguments");
+    row_copy_kernel<true><<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst);
+    return launch_status("scatter_add_rows");
+}
+
+extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
+    clear_error();
+    if (!args) return fail(kErrArg, "agg_sum: null args");
+    const grd_agg_args& a = *args;
+    if (a.n_rows < 0 || a.width <= 0 || a.width > 1024 || !a.row_ptr || !a.y || !a.out)
+        return fail(kErrArg, "agg_sum: bad arguments (width %d)", a.width);
+    if (a.ldy % 4 || a.ldo % 4 || (reinterpret_cast<uintptr_t>(a.y) & 15) ||
+        (reinterpret_cast<uintptr_t>(a.out) & 15))
+        return fail(kErrArg, "agg_sum: rows must be 16-byte aligned (ld %% 4 == 0)");
+    if (a.n_segs > 0 && (!a.heavy_rows || !a.heavy_seg_ptr || !a.seg_heavy || !a.seg_partial ||
+                         !a.heavy_counter || a.seg_len <= 0))
+        return fail(kErrArg, "agg_sum: incomplete heavy-row split");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int w4 = (a.width + 3) / 4;
+    if (w4 <= 1) return launch_agg<1, 1, 8>(a, st);
+    if (w4 <= 2) return launch_agg<2, 1, 8>(a, st);
+    if (w4 <= 4) return launch_agg<4, 1, 8>(a, st);
+    if (w4 <= 8) return launch_agg<8, 1, 8>(a, st);
+    if (w4 <= 16) return launch_agg<16, 1, 8>(a, st);
+    if (w4 <= 32) return launch_agg<32, 1, 8>(a, st);
+    if (w4 <= 64) return launch_agg<32, 2, 4>(a, st);
+    if (w4 <= 128) return launch_agg<32, 4, 2>(a, st);
+    return launch_agg<32, 8, 1>(a, st);
+}
+
+extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
+    clear_error();
+    if (!args) return fail(kErrArg, "gemm: null args");
+    const grd_gemm_args& g = *args;
+    if (g.m < 0 || g.n < 0 || g.k < 0 || !g.a || !g.b || !g.c)
+        return fail(kErrArg, "gemm: bad arguments");
+    if (g.m == 0 || g.n == 0) return 0;
+    dim3 grid(static_cast<unsigned>((g.m + kBM - 1) / kBM), static_cast<unsigned>((g.n + kBN - 1) / kBN));
+    gemm_kernel<<<grid, kGemmThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+    return launch_status("gemm");
+}
+
+extern "C" int64_t grd_wgrad_workspace(int64_t m, int64_t n, int64_t k) {
+    return wgrad_splits(m, n, k) * m * n;
+}
+
+extern "C" int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, const float* b,
+                             int64_t ldb, float* dw, int64_t lddw, int32_t accumulate, float* w, int64_t ldw,
+                             float lr, float* workspace, int64_t workspace_elems, void* stream) {
+    clear_error();
+    if (m <= 0 || n <= 0 || k < 0 || !a || !b || !dw || !workspace)
+        return fail(kErrArg, "wgrad: bad arguments");
+    const int64_t splits = wgrad_splits(m, n, k);
+    if (workspace_elems < splits * m * n) return fail(kErrArg, "wgrad: workspace too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int64_t kchunk = (k + splits - 1) / splits;
+    kchunk = (kchunk + kBK - 1) / kBK * kBK;
+    dim3 grid(static_cast<unsigned>((m + kBM - 1) / kBM), static_cast<unsigned>((n + kBN - 1) / kBN),
+              static_cast<unsigned>(splits));
+    wgrad_partial_kernel<<<grid, kGemmThreads, 0, st>>>(m, n, k, kchunk, a, lda, b, ldb, workspace);
+    int rc = launch_status("wgrad_partial");
+    if (rc) return rc;
+    wgrad_reduce_kernel<<<blocks_for(m * n), 256, 0, st>>>(m, n, splits, workspace, dw, lddw, accumulate, w,
+                                                          ldw, lr);
+    return launch_status("wgrad_reduce");
+}
+
+extern "C" int64_t grd_loss_partials(int64_t n_rows) {
+    (void)n_rows;
+    return 2 * kLossBlocks;
+}
+
+extern "C" int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t n_rows, int32_t n_classes,
+                                const int32_t* labels, const uint8_t* mask, int64_t mask_count, float* grad,
+                                int64_t ld_grad, const float* grad_scale, double* partials, double* stats_out,
+                                void* stream) {
+    clear_error();
+    if (!logits || !labels || !mask || !grad || !partials || !stats_out || n_classes <= 0)
+        return fail(kErrArg, "softmax_xent: bad arguments");
+    if (mask_count <= 0) return fail(kErrArg, "loss mask selects no vertices");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const float inv = static_cast<float>(1.0 / static_cast<double>(mask_count));
+    xent_kernel<<<kLossBlocks, 256, 0, st>>>(logits, ld_logits, n_rows, n_classes, labels, mask, inv, grad,
+                                             ld_grad, grad_scale, partials);
+    int rc = launch_status("softmax_xent");
+    if (rc) return rc;
+    xent_finalize_kernel<<<1, 32, 0, st>>>(partials, kLossBlocks, static_cast<double>(mask_count), stats_out);
+    return launch_status("softmax_xent_finalize");
+}
+
+extern "C" int grd_mul_rows(const float* x, int64_t ldx, const float* m, int64_t ldm, int64_t n_rows,
+                            int32_t width, float* y, int64_t ldy, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!x || !m || !y) return fail(kErrArg, "mul_rows: bad arguments");
+    mul_rows_kernel<<<blocks_for(n_rows * width), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, ldx, m, ldm, n_rows, width, y, ldy);
+    return launch_status("mul_rows");
+}
+
+extern "C" int grd_mask_scale_rows(const float* x, int64_t ldx, const float* ref, int64_t ldref,
+                                   const float* row_scale, int64_t n_rows, int32_t width, float* y,
+                                   int64_t ldy, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!x || !y) return fail(kErrArg, "mask_scale_rows: bad arguments");
+    mask_scale_rows_kernel<<<blocks_for(n_rows * width), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, ldx, ref, ldref, row_scale, n_rows, width, y, ldy);
+    return launch_status("mask_scale_rows");
+}
+
+extern "C" int grd_rownorm_fwd(const float* pre, int64_t ld, int64_t n_rows, int32_t width, int32_t relu,
+                               const int32_t* out_idx, float* out, int64_t ldo, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!pre || !out) return fail(kErrArg, "rownorm_fwd: bad arguments");
+    rownorm_fwd_kernel<<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        pre, ld, n_rows, width, relu, out_idx, out, ldo);
+    return launch_status("rownorm_fwd");
+}
+
+extern "C" int grd_rownorm_bwd(const float* pre, int64_t ldp, const float* grad_y, int64_t ldg,
+                               const float* a_out, int64_t lda, int64_t n_rows, int32_t width,
+                               const float* row_scale, float* grad_pre, int64_t ldgp, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!pre || !grad_y || !grad_pre) return fail(kErrArg, "rownorm_bwd: bad arguments");
+    rownorm_bwd_kernel<<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        pre, ldp, grad_y, ldg, a_out, lda, n_rows, width, row_scale, grad_pre, ldgp);
+    return launch_status("rownorm_bwd");
+}

@@ -1,0 +1,524 @@
+"""Device engine of the partition-wise GCN training step.
+
+Two execution paths share the same kernels (ops.py -> libgrinder_b200.so):
+
+* ``LayerwiseEngine`` — the fast path.  All partitions of a layer are one
+  launch over the concatenated plan (rows = targets of partition 0, then 1,
+  ...; edges pre-composed to global source ids ``gather_map[src_pos]``), so
+  the gathered block GA_p is never materialised in HBM.  Per layer the
+  engine picks the cheaper association of the GCN layer:
+
+    transform-first (d_out <= d_in):  P = X W,  out = act(A_hat P)
+        backward: H = A_hat^T gp,  dW = X^T H,  dX = H W^T
+    aggregate-first (d_out >  d_in):  N = A_hat X,  out = act(N W)
+        backward: N recomputed (regather), dW = N^T gp, dX = A_hat^T (gp W^T)
+
+  Both equal the reference's (A_hat GA) W (training.py:72-83,103-143) up to
+  fp32 rounding; transform-first aggregates at the narrower width and
+  needs no forward recompute.  The transposed aggregation A_hat^T is a
+  deterministic pull over the graph's own CSR (out-edges), so no float
+  atomics and no per-partition scatter are needed.  Degree scales, ReLU
+  masks and the next layer's pre-scale are fused into the producing
+  kernel's epilogue, and the SGD step into the weight-gradient reduction.
+
+* ``PartitionEngine`` — the literal per-(layer, partition) schedule of
+  training.py:259-358: gather GA_p, layer forward, regather (or snapshot)
+  in backward, per-partition grad_GA / grad_W, ascending-pid scatter.  It
+  serves the reference's per-partition operators, ``grad_probe``,
+  ``use_snapshots`` and tier-manager hooks.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import ops
+from .ops import AggSpec, ld_of
+
+__all__ = ["DeviceGraph", "DevicePartition", "LayerOps", "LayerwiseEngine", "PartitionEngine",
+           "dropout_mask"]
+
+
+def dropout_mask(dropout_rate: float, dropout_seed: int, epoch: int, layer: int,
+                 shape: tuple[int, int]) -> np.ndarray | None:
+    """Seeded keep-mask / keep (training.py:178-185), drawn on the host."""
+    if dropout_rate == 0.0:
+        return None
+    seq = np.random.SeedSequence(dropout_seed, spawn_key=(epoch, layer))
+    keep = 1.0 - dropout_rate
+    return (np.random.Generator(np.random.PCG64(seq)).random(shape) < keep) / keep
+
+
+class DeviceGraph:
+    """HBM-resident plan of one (graph, labeling): forward in-CSR in perm
+    order, the out-CSR for the transposed pull, and per-vertex degree scales."""
+
+    def __init__(self, graph, plan, device):
+        f = plan.flat
+        self.device = device
+        self.num_vertices = plan.num_vertices
+        self.num_edges = int(f.in_ptr[-1])
+        self.num_partitions = plan.num_partitions
+        self.part_ptr = f.part_ptr.copy()
+        # forward: rows = perm order, output row = vertex, self = vertex
+        self.fwd = AggSpec.build(f.in_ptr, f.in_src, device, out_idx=f.perm)
+        # transposed pull: rows = vertices, neighbours = out-edges (u -> v)
+        self.bwd = AggSpec.build(graph.src_ptr, graph.dst_idx, device)
+        self._deg = f.in_degree.astype(np.float64)
+        self._scales: dict[str, torch.Tensor] = {}
+        self._partitions: dict[int, "DevicePartition"] = {}
+        self.plan = plan
+
+    def scale(self, name: str | None) -> torch.Tensor | None:
+        if name is None:
+            return None
+        t = self._scales.get(name)
+        if t is None:
+            t = torch.from_numpy(_degree_scale(name, self._deg).astype(np.float32)).to(self.device)
+            self._scales[name] = t
+        return t
+
+    def partition(self, q: int) -> "DevicePartition":
+        part = self._partitions.get(q)
+        if part is None:
+            part = DevicePartition.from_plan(self.plan, q, self.device)
+            self._partitions[q] = part
+        return part
+
+
+class DevicePartition:
+    """One partition's local topology on the device (plan.py:21-48) plus its
+    CSC-by-gather-row transpose for the local backward pull."""
+
+    def __init__(self, pid, targets, gather_map, tgt_ptr, src_pos, self_pos, target_indeg,
+                 gather_indeg, device):
+        self.pid = pid
+        self.dev = device
+        self.num_targets = int(len(targets))
+        self.num_gather = int(len(gather_map))
+        tgt_ptr = np.asarray(tgt_ptr, dtype=np.int64)
+        src_pos = np.asarray(src_pos, dtype=np.int64)
+        self_pos = np.asarray(self_pos, dtype=np.int64)
+        self.targets = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.int32)).to(device)
+        self.gather_map = torch.from_numpy(np.ascontiguousarray(gather_map, dtype=np.int32)).to(device)
+        self.fwd = AggSpec.build(tgt_ptr, src_pos, device, self_idx=self_pos)
+        # Transposed local aggregation: for gather row g, its targets in
+        # ascending order (np.add.at's edge order, training.py:141), self last.
+        local_t = np.repeat(np.arange(self.num_targets, dtype=np.int64), np.diff(tgt_ptr))
+        order = np.argsort(src_pos, kind="stable")
+        csc_ptr = np.zeros(self.num_gather + 1, dtype=np.int64)
+        np.cumsum(np.bincount(src_pos, minlength=self.num_gather), out=csc_ptr[1:])
+        self_t = np.full(self.num_gather, -1, dtype=np.int32)
+        self_t[self_pos] = np.arange(self.num_targets, dtype=np.int32)
+        self.bwd = AggSpec.build(csc_ptr, local_t[order], device, self_idx=self_t)
+        self._deg = {"targets": np.asarray(target_indeg, dtype=np.float64),
+                     "gather": np.asarray(gather_indeg, dtype=np.float64)}
+        self._scales: dict = {}
+
+    @classmethod
+    def from_topology(cls, topo, device) -> "DevicePartition":
+        return cls(topo.partition_id, topo.targets, topo.gather_map, topo.tgt_ptr, topo.src_pos,
+                   topo.self_pos, topo.target_indeg, topo.gather_indeg, device)
+
+    @classmethod
+    def from_plan(cls, plan, q: int, device) -> "DevicePartition":
+        f = plan.flat
+        r0, r1 = int(f.part_ptr[q]), int(f.part_ptr[q + 1])
+        e0, e1 = int(f.in_ptr[r0]), int(f.in_ptr[r1])
+        g0, g1 = int(f.gather_ptr[q]), int(f.gather_ptr[q + 1])
+        targets = f.perm[r0:r1]
+        gmap = f.gather_map[g0:g1]
+        return cls(q, targets, gmap, f.in_ptr[r0:r1 + 1] - f.in_ptr[r0], f.in_src_pos[e0:e1],
+                   f.self_pos[r0:r1], f.in_degree[targets], f.in_degree[gmap], device)
+
+    def scale(self, name: str | None, rows: str) -> torch.Tensor | None:
+        """Degree scale over the target rows or gather rows of this partition."""
+        if name is None:
+            return None
+        key = (name, rows)
+        t = self._scales.get(key)
+        if t is None:
+            t = torch.from_numpy(_degree_scale(name, self._deg[rows]).astype(np.float32)).to(self.dev)
+            self._scales[key] = t
+        return t
+
+
+def _degree_scale(name: str, deg: np.ndarray) -> np.ndarray:
+    if name == "inv_deg1":
+        return 1.0 / (deg + 1.0)
+    if name == "s":
+        return 1.0 / np.sqrt(deg + 1.0)
+    if name == "s_inv_deg1":
+        return 1.0 / (np.sqrt(deg + 1.0) * (deg + 1.0))
+    raise KeyError(name)
+
+
+class _LayerCfg:
+    def __init__(self, layer: int, dims: list[int], mode: str, row_normalize: bool, last: bool):
+        self.layer = layer
+        self.d_in, self.d_out = dims[layer], dims[layer + 1]
+        self.transform_first = self.d_out <= self.d_in
+        self.sym = mode == "symmetric_norm"
+        self.rownorm = row_normalize
+        self.last = last
+
+    # scale applied to the upstream gradient before this layer's pull (TF)
+    # or after its dgrad GEMM (AF): mean -> 1/(deg+1), sym -> 1/sqrt(deg+1)
+    @property
+    def pre_scale(self) -> str:
+        return "s" if self.sym else "inv_deg1"
+
+
+class _Weights:
+    """fp32 device copies of W_l and dW_l, zero padded to [ld(d_in), ld(d_out)]."""
+
+    def __init__(self, model, device):
+        self.w = []
+        self.dw = []
+        for w in model.weights:
+            t = torch.zeros((ld_of(w.shape[0]), ld_of(w.shape[1])), dtype=torch.float32, device=device)
+            t[: w.shape[0], : w.shape[1]] = torch.from_numpy(np.asarray(w, dtype=np.float32)).to(device)
+            self.w.append(t)
+            self.dw.append(torch.zeros_like(t))
+
+    def load(self, model) -> None:
+        for t, w in zip(self.w, model.weights):
+            t[: w.shape[0], : w.shape[1]].copy_(torch.from_numpy(np.asarray(w, dtype=np.float32)))
+
+    def export(self, model) -> None:
+        model.weights = [t[: w.shape[0], : w.shape[1]].double().cpu().numpy()
+                         for t, w in zip(self.w, model.weights)]
+        model.weight_grads = [t[: w.shape[0], : w.shape[1]].double().cpu().numpy()
+                              for t, w in zip(self.dw, model.weights)]
+
+
+class _EngineBase:
+    def __init__(self, dg: DeviceGraph, model, features: torch.Tensor, labels: np.ndarray,
+                 train_mask: np.ndarray):
+        self.dg = dg
+        dev = dg.device
+        self.device = dev
+        self.V = dg.num_vertices
+        self.dims = model.dims
+        self.L = model.num_layers
+        self.mode = model.aggregation_mode
+        self.model = model
+        self.cfg = [_LayerCfg(l, self.dims, self.mode, model.row_normalize, l == self.L - 1)
+                    for l in range(self.L)]
+        self.wts = _Weights(model, dev)
+        self.acts = [features] + [ops.zeros_rows(self.V, d, dev) for d in self.dims[1:]]
+        self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
+        self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
+        self.mask_count = int(np.count_nonzero(train_mask))
+        if self.mask_count == 0:
+            raise ValueError("loss mask selects no vertices")
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.partials = ops.loss_partials(self.V, dev)
+        self.maxw = max(self.dims)
+        self.dropout_rate = model.dropout_rate
+        self.dropout_seed = model.dropout_seed
+        self.dmask = [None] * self.L
+        self.xd = ops.zeros_rows(self.V, self.maxw, dev) if self.dropout_rate > 0 else None
+
+    def set_dropout(self, epoch: int) -> None:
+        if self.dropout_rate == 0.0:
+            return
+        for l in range(self.L):
+            m = dropout_mask(self.dropout_rate, self.dropout_seed, epoch, l, (self.V, self.dims[l]))
+            t = ops.zeros_rows(self.V, self.dims[l], self.device)
+            t[:, : self.dims[l]] = torch.from_numpy(m.astype(np.float32)).to(self.device)
+            self.dmask[l] = t
+
+    def layer_input(self, l: int) -> torch.Tensor:
+        """A_l, or A_l * M_l under dropout (recomputed on every use)."""
+        x = self.acts[l]
+        if self.dmask[l] is None:
+            return x
+        ops.mul_rows(x, self.dmask[l], self.xd, self.V, self.dims[l])
+        return self.xd
+
+
+class LayerwiseEngine(_EngineBase):
+    """Fused layer-wide epoch over an HBM-resident graph (module docstring)."""
+
+    def __init__(self, dg, model, features, labels, train_mask):
+        super().__init__(dg, model, features, labels, train_mask)
+        dev = self.device
+        self.t1 = ops.zeros_rows(self.V, self.maxw, dev)
+        self.g = ops.zeros_rows(self.V, self.maxw, dev)
+        self.h = ops.zeros_rows(self.V, self.maxw, dev)
+
+    # ---------------------------------------------------------- forward --
+    def _forward_layer(self, l: int, x: torch.Tensor, out: torch.Tensor, relu: bool) -> None:
+        c, dg = self.cfg[l], self.dg
+        W = self.wts.w[l]
+        s = dg.scale("s") if c.sym else None
+        if c.transform_first:
+            ops.gemm(x, W, self.t1, self.V, c.d_out, c.d_in, row_scale=s)
+            ops.agg_sum(dg.fwd, self.t1, out, c.d_out, post_div_deg=not c.sym, post_scale=s, relu=relu)
+        else:
+            ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
+            ops.gemm(self.t1, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
+
+    def forward(self) -> None:
+        for l, c in enumerate(self.cfg):
+            x = self.layer_input(l)
+            out = self.acts[l + 1]
+            self._forward_layer(l, x, out, relu=not c.last and not c.rownorm)
+            if c.rownorm:
+                ops.rownorm_fwd(out, out, self.V, c.d_out, relu=not c.last)
+
+    # --------------------------------------------------------- backward --
+    def _consumer_epilogue(self, l: int):
+        """(relu_ref, row_scale) the producer of dA_{l+1} applies for layer l."""
+        c = self.cfg[l]
+        if c.rownorm:
+            return None, None
+        ref = None if c.last else self.acts[l + 1]
+        scale = self.dg.scale(c.pre_scale) if c.transform_first else None
+        return ref, scale
+
+    def loss(self) -> None:
+        c = self.cfg[-1]
+        _, scale = self._consumer_epilogue(self.L - 1)
+        ops.softmax_xent(self.acts[-1], self.V, c.d_out, self.labels, self.mask, self.mask_count,
+                         self.g, self.stats, self.partials, grad_scale=scale)
+
+    def backward(self, lr: float) -> None:
+        dg = self.dg
+        for l in reversed(range(self.L)):
+            c = self.cfg[l]
+            W, dW = self.wts.w[l], self.wts.dw[l]
+            x = self.layer_input(l)
+            s = dg.scale("s") if c.sym else None
+            have_n = False
+            if c.rownorm:
+                # regather + recompute pre-activation, then the row-norm backward
+                if c.transform_first:
+                    ops.gemm(x, W, self.t1, self.V, c.d_out, c.d_in, row_scale=s)
+                    ops.agg_sum(dg.fwd, self.t1, self.h, c.d_out, post_div_deg=not c.sym, post_scale=s)
+                else:
+                    ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym,
+                                post_scale=s)
+                    ops.gemm(self.t1, W, self.h, self.V, c.d_out, c.d_in)
+                    have_n = True
+                ops.rownorm_bwd(self.h, self.g, self.g, self.V, c.d_out,
+                                a_out=None if c.last else self.acts[l + 1],
+                                row_scale=dg.scale(c.pre_scale) if c.transform_first else None)
+            prev = self._consumer_epilogue(l - 1) if l > 0 else (None, None)
+            dmask = self.dmask[l]
+            if c.transform_first:
+                # H = A_hat^T (gp * pre_scale)
+                ops.agg_sum(dg.bwd, self.g, self.h, c.d_out, post_scale=s)
+                if l > 0:
+                    ops.gemm(self.h, W, self.g, self.V, c.d_in, c.d_out, trans_b=True,
+                             row_scale=prev[1], elem_mul=dmask, relu_ref=prev[0])
+                ops.wgrad_sgd(x, self.h, dW, c.d_in, c.d_out, self.V, w=W, lr=lr)
+            else:
+                if not have_n:   # regather: recompute the normalised aggregate
+                    ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym,
+                                post_scale=s)
+                ops.gemm(self.g, W, self.h, self.V, c.d_in, c.d_out, trans_b=True,
+                         row_scale=dg.scale(c.pre_scale))
+                ops.wgrad_sgd(self.t1, self.g, dW, c.d_in, c.d_out, self.V, w=W, lr=lr)
+                if l > 0:
+                    post = self._combine(s is not None, prev[1])
+                    ops.agg_sum(dg.bwd, self.h, self.g, c.d_in, post_scale=post,
+                                mask_ref=None if dmask is not None else prev[0])
+                    if dmask is not None:
+                        ops.mul_rows(self.g, dmask, self.g, self.V, c.d_in)
+                        if prev[0] is not None:
+                            ops.mask_scale_rows(self.g, self.g, self.V, c.d_in, ref=prev[0])
+
+    def _combine(self, sym: bool, consumer_scale) -> torch.Tensor | None:
+        if consumer_scale is None:
+            return self.dg.scale("s") if sym else None
+        if not sym:
+            return consumer_scale
+        # s * (consumer pre-scale): s*s = 1/(deg+1) (mean consumer is impossible
+        # here: one model has one mode), so the consumer's scale is s.
+        return self.dg.scale("inv_deg1")
+
+    def epoch(self, lr: float) -> None:
+        self.forward()
+        self.loss()
+        self.backward(lr)
+
+
+class LayerOps:
+    """Per-(layer, partition) operators on device tensors (training.py:72-143):
+    forward of one partition from its gathered rows GA_p and the
+    regather-based backward returning (grad_GA, grad_W)."""
+
+    def __init__(self, model, device, weights: "_Weights | None" = None):
+        self.device = device
+        self.dims = model.dims
+        self.L = model.num_layers
+        self.cfg = [_LayerCfg(l, self.dims, model.aggregation_mode, model.row_normalize,
+                              l == self.L - 1) for l in range(self.L)]
+        self.wts = weights if weights is not None else _Weights(model, device)
+
+    def layer_forward(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
+        """out = act(norm(aggregate(GA)) @ W) for one partition (training.py:86-100)."""
+        c = self.cfg[l]
+        W = self.wts.w[l]
+        pre = self._pre(l, ga, part)
+        if c.rownorm:
+            ops.rownorm_fwd(pre, pre, part.num_targets, c.d_out, relu=not c.last)
+        return pre
+
+    def _pre(self, l: int, ga: torch.Tensor, part: DevicePartition, relu_default: bool = True):
+        c = self.cfg[l]
+        W = self.wts.w[l]
+        dev = self.device
+        relu = relu_default and not c.last and not c.rownorm
+        out = ops.zeros_rows(part.num_targets, c.d_out, dev)
+        s_g = part.scale("s", "gather") if c.sym else None
+        s_t = part.scale("s", "targets") if c.sym else None
+        if c.transform_first:
+            p = ops.zeros_rows(part.num_gather, c.d_out, dev)
+            ops.gemm(ga, W, p, part.num_gather, c.d_out, c.d_in, row_scale=s_g)
+            ops.agg_sum(part.fwd, p, out, c.d_out, post_div_deg=not c.sym, post_scale=s_t, relu=relu)
+        else:
+            n = self._norm(l, ga, part)
+            ops.gemm(n, W, out, part.num_targets, c.d_out, c.d_in, relu_out=relu)
+        return out
+
+    def _norm(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
+        c = self.cfg[l]
+        n = ops.zeros_rows(part.num_targets, c.d_in, self.device)
+        ops.agg_sum(part.fwd, ga, n, c.d_in,
+                    src_scale=part.scale("s", "gather") if c.sym else None,
+                    post_div_deg=not c.sym,
+                    post_scale=part.scale("s", "targets") if c.sym else None)
+        return n
+
+    def backward_from_ga(self, l: int, ga: torch.Tensor, a_out: torch.Tensor, grad_out: torch.Tensor,
+                         part: DevicePartition) -> tuple[torch.Tensor, torch.Tensor]:
+        """(grad_GA [G, d_in], grad_W [d_in, d_out]) of one partition
+        (training.py:103-143), recomputing from the (re)gathered input."""
+        c = self.cfg[l]
+        W = self.wts.w[l]
+        dev = self.device
+        T, G = part.num_targets, part.num_gather
+        pre_scale = part.scale(c.pre_scale, "targets") if c.transform_first else None
+        gp = ops.zeros_rows(T, c.d_out, dev)
+        if c.rownorm:
+            pre = self._pre(l, ga, part, relu_default=False)
+            ops.rownorm_bwd(pre, grad_out, gp, T, c.d_out, a_out=None if c.last else a_out,
+                            row_scale=pre_scale)
+        else:
+            ops.mask_scale_rows(grad_out, gp, T, c.d_out, ref=None if c.last else a_out,
+                                row_scale=pre_scale)
+        s_g = part.scale("s", "gather") if c.sym else None
+        grad_w = torch.zeros_like(self.wts.w[l])
+        grad_ga = ops.zeros_rows(G, c.d_in, dev)
+        if c.transform_first:
+            h = ops.zeros_rows(G, c.d_out, dev)
+            ops.agg_sum(part.bwd, gp, h, c.d_out, post_scale=s_g)
+            ops.wgrad_sgd(ga, h, grad_w, c.d_in, c.d_out, G)
+            ops.gemm(h, W, grad_ga, G, c.d_in, c.d_out, trans_b=True)
+        else:
+            n = self._norm(l, ga, part)
+            ops.wgrad_sgd(n, gp, grad_w, c.d_in, c.d_out, T)
+            gn = ops.zeros_rows(T, c.d_in, dev)
+            ops.gemm(gp, W, gn, T, c.d_in, c.d_out, trans_b=True,
+                     row_scale=part.scale(c.pre_scale, "targets"))
+            ops.agg_sum(part.bwd, gn, grad_ga, c.d_in, post_scale=s_g)
+        return grad_ga, grad_w
+
+
+class PartitionEngine(_EngineBase):
+    """Per-(layer, partition) execution, literally following training.py:259-358."""
+
+    def __init__(self, dg, model, features, labels, train_mask):
+        super().__init__(dg, model, features, labels, train_mask)
+        self.grad_cur = ops.zeros_rows(self.V, self.maxw, self.device)
+        self.grad_prev = ops.zeros_rows(self.V, self.maxw, self.device)
+        self.ops = LayerOps(model, self.device, self.wts)
+        self.eye = {}
+
+    def _add_into(self, dst: torch.Tensor, src: torch.Tensor) -> None:
+        rows = src.shape[0]
+        idx = self.eye.get(rows)
+        if idx is None:
+            idx = torch.arange(rows, dtype=torch.int32, device=self.device)
+            self.eye[rows] = idx
+        ops.scatter_add_rows(src, idx, dst, src.shape[1])
+
+    # ---- the epoch -----------------------------------------------------
+    def epoch(self, epoch: int, lr: float, order_of, hierarchy=None, use_snapshots=False,
+              grad_probe=None, to_host=None) -> None:
+        dg = self.dg
+        P = dg.num_partitions
+        snapshots = {}
+        if hierarchy is not None:
+            hierarchy.begin_epoch()
+        for l, c in enumerate(self.cfg):
+            x = self.layer_input(l)
+            out = self.acts[l + 1]
+            out.zero_()
+            for pid in order_of(l, "forward"):
+                part = dg.partition(pid)
+                ga = ops.zeros_rows(part.num_gather, c.d_in, self.device)
+                ops.gather_rows(x, part.gather_map, ga, c.d_in)
+                res = self.ops.layer_forward(l, ga, part)
+                ops.scatter_add_rows(res, part.targets, out, c.d_out)
+                if use_snapshots:
+                    snapshots[(l, pid)] = ga
+                if hierarchy is not None:
+                    hierarchy.forward_partition(l, pid)
+            if hierarchy is not None:
+                hierarchy.end_forward_layer(l)
+        c = self.cfg[-1]
+        ops.softmax_xent(self.acts[-1], self.V, c.d_out, self.labels, self.mask, self.mask_count,
+                         self.grad_cur, self.stats, self.partials)
+        self.check_loss(epoch)
+        if hierarchy is not None:
+            hierarchy.loss_stage()
+        for dw in self.wts.dw:
+            dw.zero_()
+        for l in reversed(range(self.L)):
+            c = self.cfg[l]
+            x = self.layer_input(l)
+            results = {}
+            for pid in order_of(l, "backward"):
+                part = dg.partition(pid)
+                if use_snapshots:
+                    ga = snapshots.pop((l, pid))
+                else:
+                    ga = ops.zeros_rows(part.num_gather, c.d_in, self.device)
+                    ops.gather_rows(x, part.gather_map, ga, c.d_in)
+                a_out = ops.zeros_rows(part.num_targets, c.d_out, self.device)
+                ops.gather_rows(self.acts[l + 1], part.targets, a_out, c.d_out)
+                g = ops.zeros_rows(part.num_targets, c.d_out, self.device)
+                ops.gather_rows(self.grad_cur, part.targets, g, c.d_out)
+                results[pid] = self.ops.backward_from_ga(l, ga, a_out, g, part)
+                if hierarchy is not None:
+                    hierarchy.backward_partition(l, pid)
+            if l > 0:
+                self.grad_prev.zero_()
+            for pid in range(P):
+                grad_ga, grad_w = results[pid]
+                if grad_probe is not None:
+                    grad_probe(epoch, l, pid, to_host(grad_ga, c.d_in), to_host(grad_w, c.d_out, c.d_in))
+                self._add_into(self.wts.dw[l], grad_w)
+                if l > 0:
+                    ops.scatter_add_rows(grad_ga, dg.partition(pid).gather_map, self.grad_prev, c.d_in)
+            if l > 0 and self.dmask[l] is not None:
+                ops.mul_rows(self.grad_prev, self.dmask[l], self.grad_prev, self.V, c.d_in)
+            if hierarchy is not None:
+                hierarchy.end_backward_layer(l)
+            self.grad_cur, self.grad_prev = self.grad_prev, self.grad_cur
+        for l in range(self.L):
+            w, dw = self.wts.w[l], self.wts.dw[l]
+            ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
+        if hierarchy is not None:
+            hierarchy.end_epoch()
+
+    def check_loss(self, epoch: int) -> None:
+        loss = float(self.stats[0].item())
+        if not np.isfinite(loss):
+            raise ValueError(f"non-finite loss {loss} at epoch {epoch}; "
+                             f"reduce the learning rate or check the inputs")

@@ -1,0 +1,226 @@
+"""Thin launch wrappers over the C ABI for torch CUDA tensors.
+
+Every function launches one of the library's sm_100a kernels on torch's
+current stream; no torch compute op is used on the training path.  Dense
+device matrices are fp32, row-major, with ``ld = round_up(width, 4)`` and
+zero padding columns (see include/grinder_b200.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["AggSpec", "agg_sum", "gather_rows", "gemm", "ld_of", "mask_scale_rows",
+           "mul_rows", "rownorm_bwd", "rownorm_fwd", "scatter_add_rows", "softmax_xent",
+           "stream_ptr", "wgrad_sgd", "zeros_rows"]
+
+HEAVY_THRESHOLD = 128   # rows above this degree are split ...
+SEGMENT_EDGES = 128     # ... into segments of this many edges
+
+
+def ld_of(width: int) -> int:
+    return (int(width) + 3) // 4 * 4
+
+
+def zeros_rows(rows: int, width: int, device) -> torch.Tensor:
+    """Zero-initialised [rows, ld_of(width)] fp32 matrix (padding stays 0)."""
+    return torch.zeros((int(rows), ld_of(width)), dtype=torch.float32, device=device)
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _ld(t: torch.Tensor) -> int:
+    return int(t.stride(0))
+
+
+@dataclass
+class AggSpec:
+    """A static CSR over which rows are sum-aggregated, uploaded once, with
+    its deterministic heavy-row segmentation (include/grinder_b200.h K2)."""
+
+    n_rows: int
+    row_ptr: torch.Tensor            # int64 [n_rows+1]
+    idx: torch.Tensor                # int32 [nnz]
+    out_idx: torch.Tensor | None     # int32 [n_rows]
+    self_idx: torch.Tensor | None    # int32 [n_rows]
+    heavy_rows: torch.Tensor | None
+    heavy_seg_ptr: torch.Tensor | None
+    seg_heavy: torch.Tensor | None
+    heavy_counter: torch.Tensor | None
+    n_heavy: int
+    n_segs: int
+    nnz: int
+    _partial: torch.Tensor | None = None
+
+    @classmethod
+    def build(cls, row_ptr: np.ndarray, idx: np.ndarray, device, out_idx=None, self_idx=None,
+              heavy_threshold: int = HEAVY_THRESHOLD, seg_len: int = SEGMENT_EDGES) -> "AggSpec":
+        row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        n = row_ptr.size - 1
+        deg = np.diff(row_ptr)
+        heavy = np.flatnonzero(deg > heavy_threshold).astype(np.int32)
+        nseg = (deg[heavy] + seg_len - 1) // seg_len
+        seg_ptr = np.zeros(heavy.size + 1, dtype=np.int64)
+        np.cumsum(nseg, out=seg_ptr[1:])
+        seg_heavy = np.repeat(np.arange(heavy.size, dtype=np.int32), nseg)
+
+        def up(a, dt):
+            if a is None:
+                return None
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+
+        has_heavy = heavy.size > 0
+        return cls(
+            n_rows=n, row_ptr=up(row_ptr, np.int64), idx=up(idx, np.int32),
+            out_idx=up(out_idx, np.int32), self_idx=up(self_idx, np.int32),
+            heavy_rows=up(heavy, np.int32) if has_heavy else None,
+            heavy_seg_ptr=up(seg_ptr, np.int64) if has_heavy else None,
+            seg_heavy=up(seg_heavy, np.int32) if has_heavy else None,
+            heavy_counter=torch.zeros(max(heavy.size, 1), dtype=torch.int32, device=device)
+            if has_heavy else None,
+            n_heavy=int(heavy.size), n_segs=int(seg_heavy.size), nnz=int(row_ptr[-1]),
+        )
+
+    def partial(self, width: int) -> torch.Tensor | None:
+        if self.n_segs == 0:
+            return None
+        need = self.n_segs * ld_of(width)
+        if self._partial is None or self._partial.numel() < need:
+            self._partial = torch.empty(need, dtype=torch.float32, device=self.row_ptr.device)
+        return self._partial
+
+
+def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
+            src_scale=None, post_scale=None, post_div_deg=False, relu=False,
+            mask_ref=None) -> None:
+    a = _lib.GrdAggArgs()
+    a.n_rows = spec.n_rows
+    a.row_ptr = _p(spec.row_ptr)
+    a.idx = _p(spec.idx)
+    a.out_idx = _p(spec.out_idx)
+    a.self_idx = _p(spec.self_idx)
+    a.y = _p(y)
+    a.ldy = _ld(y)
+    a.src_scale = _p(src_scale)
+    a.post_scale = _p(post_scale)
+    a.post_div_deg = int(bool(post_div_deg))
+    a.relu = int(bool(relu))
+    a.out = _p(out)
+    a.ldo = _ld(out)
+    a.width = int(width)
+    a.heavy_threshold = HEAVY_THRESHOLD if spec.n_segs else 0
+    a.n_heavy = spec.n_heavy
+    a.heavy_rows = _p(spec.heavy_rows)
+    a.heavy_seg_ptr = _p(spec.heavy_seg_ptr)
+    a.seg_heavy = _p(spec.seg_heavy)
+    a.n_segs = spec.n_segs
+    a.seg_len = SEGMENT_EDGES
+    a.seg_partial = _p(spec.partial(width))
+    a.heavy_counter = _p(spec.heavy_counter)
+    a.mask_ref = _p(mask_ref)
+    a.ld_mask_ref = _ld(mask_ref) if mask_ref is not None else 0
+    _lib.check(_lib.lib().grd_agg_sum(ctypes.byref(a), stream_ptr()), "agg_sum")
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
+         trans_a=False, trans_b=False, row_scale=None, elem_mul=None, relu_ref=None,
+         relu_out=False, accumulate=False) -> None:
+    """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim."""
+    g = _lib.GrdGemmArgs()
+    g.m, g.n, g.k = int(m), int(n), int(k)
+    g.a, g.lda, g.trans_a = _p(a), _ld(a), int(bool(trans_a))
+    g.b, g.ldb, g.trans_b = _p(b), _ld(b), int(bool(trans_b))
+    g.c, g.ldc = _p(c), _ld(c)
+    g.row_scale = _p(row_scale)
+    g.elem_mul = _p(elem_mul)
+    g.ld_elem_mul = _ld(elem_mul) if elem_mul is not None else 0
+    g.relu_ref = _p(relu_ref)
+    g.ld_relu_ref = _ld(relu_ref) if relu_ref is not None else 0
+    g.relu_out = int(bool(relu_out))
+    g.accumulate = int(bool(accumulate))
+    _lib.check(_lib.lib().grd_gemm(ctypes.byref(g), stream_ptr()), "gemm")
+
+
+_WS: dict = {}
+
+
+def _workspace(device, elems: int) -> torch.Tensor:
+    key = str(device)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < elems:
+        ws = torch.empty(max(elems, 1), dtype=torch.float32, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def wgrad_sgd(a: torch.Tensor, b: torch.Tensor, dw: torch.Tensor, m: int, n: int, k: int, *,
+              accumulate=False, w: torch.Tensor | None = None, lr: float = 0.0) -> None:
+    """dw[:m,:n] (=|+=) a[:k,:m]^T @ b[:k,:n]; then w -= lr*dw if w given."""
+    L = _lib.lib()
+    need = int(L.grd_wgrad_workspace(m, n, k))
+    ws = _workspace(dw.device, need)
+    _lib.check(L.grd_wgrad_sgd(int(m), int(n), int(k), _p(a), _ld(a), _p(b), _ld(b), _p(dw), _ld(dw),
+                               int(bool(accumulate)), _p(w), _ld(w) if w is not None else 0,
+                               float(lr), _p(ws), ws.numel(), stream_ptr()), "wgrad_sgd")
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor, width: int) -> None:
+    _lib.check(_lib.lib().grd_gather_rows(_p(src), _ld(src), _p(idx), idx.numel(), int(width),
+                                          _p(dst), _ld(dst), stream_ptr()), "gather_rows")
+
+
+def scatter_add_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor, width: int) -> None:
+    _lib.check(_lib.lib().grd_scatter_add_rows(_p(src), _ld(src), _p(idx), idx.numel(), int(width),
+                                               _p(dst), _ld(dst), stream_ptr()), "scatter_add_rows")
+
+
+def mul_rows(x: torch.Tensor, m: torch.Tensor, y: torch.Tensor, n_rows: int, width: int) -> None:
+    _lib.check(_lib.lib().grd_mul_rows(_p(x), _ld(x), _p(m), _ld(m), int(n_rows), int(width), _p(y),
+                                       _ld(y), stream_ptr()), "mul_rows")
+
+
+def mask_scale_rows(x: torch.Tensor, y: torch.Tensor, n_rows: int, width: int, *, ref=None,
+                    row_scale=None) -> None:
+    _lib.check(_lib.lib().grd_mask_scale_rows(
+        _p(x), _ld(x), _p(ref), _ld(ref) if ref is not None else 0, _p(row_scale), int(n_rows),
+        int(width), _p(y), _ld(y), stream_ptr()), "mask_scale_rows")
+
+
+def rownorm_fwd(pre: torch.Tensor, out: torch.Tensor, n_rows: int, width: int, relu: bool,
+                out_idx=None) -> None:
+    _lib.check(_lib.lib().grd_rownorm_fwd(_p(pre), _ld(pre), int(n_rows), int(width), int(relu),
+                                          _p(out_idx), _p(out), _ld(out), stream_ptr()), "rownorm_fwd")
+
+
+def rownorm_bwd(pre: torch.Tensor, grad_y: torch.Tensor, grad_pre: torch.Tensor, n_rows: int,
+                width: int, *, a_out=None, row_scale=None) -> None:
+    _lib.check(_lib.lib().grd_rownorm_bwd(
+        _p(pre), _ld(pre), _p(grad_y), _ld(grad_y), _p(a_out), _ld(a_out) if a_out is not None else 0,
+        int(n_rows), int(width), _p(row_scale), _p(grad_pre), _ld(grad_pre), stream_ptr()),
+        "rownorm_bwd")
+
+
+def softmax_xent(logits: torch.Tensor, n_rows: int, n_classes: int, labels: torch.Tensor,
+                 mask: torch.Tensor, mask_count: int, grad: torch.Tensor, stats: torch.Tensor,
+                 partials: torch.Tensor, grad_scale=None) -> None:
+    """stats (float64 cuda[4]) <- {loss, accuracy, loss_sum, correct}."""
+    _lib.check(_lib.lib().grd_softmax_xent(
+        _p(logits), _ld(logits), int(n_rows), int(n_classes), _p(labels), _p(mask), int(mask_count),
+        _p(grad), _ld(grad), _p(grad_scale), _p(partials), _p(stats), stream_ptr()), "softmax_xent")
+
+
+def loss_partials(n_rows: int, device) -> torch.Tensor:
+    return torch.empty(int(_lib.lib().grd_loss_partials(int(n_rows))), dtype=torch.float64,
+                       device=device)

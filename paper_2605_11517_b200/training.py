@@ -1,0 +1,277 @@
+"""Public training API (reference: grinder/training.py), executed on the GPU.
+
+Same names, signatures, return values and ValueError behaviour as the
+reference:
+
+* ``partitioned_train(dataset, plan, model, epochs, lr, hierarchy=None,
+  use_snapshots=False, grad_probe=None, partition_order=None)``
+  -> ``(ModelState, [(epoch, loss, acc)], ledger)`` (training.py:259-358)
+* ``layer_forward`` / ``regather_backward`` / ``scatter_accumulate`` — the
+  per-(layer, partition) operators (training.py:86-175)
+* ``reference_train`` / ``compute_gradients`` — the monolithic (P = 1)
+  execution (training.py:193-256)
+
+Inputs may be the reference's numpy arrays; everything computes in fp32 on
+the device through libgrinder_b200.so (no CPU fallback).  Without observers
+(``grad_probe``, ``use_snapshots``, ``hierarchy``) the fused layer-wide
+engine runs and each epoch is replayed from a captured CUDA graph; with
+observers the literal per-partition schedule runs so every hook and probe
+sees per-partition tensors in the reference's order.
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import ops
+from .dataset import LabeledDataset
+from .engine import DeviceGraph, DevicePartition, LayerOps, LayerwiseEngine, PartitionEngine
+from .model import ModelState, copy_model
+from .plan import PartitionPlan, PartitionTopology, build_partition_plan
+
+__all__ = [
+    "compute_gradients",
+    "layer_forward",
+    "partitioned_train",
+    "reference_train",
+    "regather_backward",
+    "scatter_accumulate",
+    "trace_to_csv",
+    "write_trace_csv",
+    "TrainSession",
+]
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_11517_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_dev(mat: np.ndarray, dev, width: int | None = None) -> torch.Tensor:
+    mat = np.asarray(mat)
+    rows, cols = mat.shape
+    t = ops.zeros_rows(rows, cols if width is None else width, dev)
+    t[:, :cols] = torch.from_numpy(np.ascontiguousarray(mat, dtype=np.float32)).to(dev)
+    return t
+
+
+def _to_host(t: torch.Tensor, cols: int, rows: int | None = None) -> np.ndarray:
+    r = t.shape[0] if rows is None else rows
+    return t[:r, :cols].double().cpu().numpy()
+
+
+# --------------------------------------------------------------------------
+# per-(layer, partition) operators
+# --------------------------------------------------------------------------
+def layer_forward(layer: int, input_rows: np.ndarray, topology: PartitionTopology,
+                  model: ModelState) -> np.ndarray:
+    """One layer over one partition: gathered rows in, target rows out."""
+    weight = model.weights[layer]
+    if input_rows.ndim != 2 or input_rows.shape[0] != topology.gather_map.size:
+        raise ValueError(f"input has {input_rows.shape[0]} rows, gather map needs "
+                         f"{topology.gather_map.size}")
+    if input_rows.shape[1] != weight.shape[0]:
+        raise ValueError(f"input width {input_rows.shape[1]} != layer {layer} input dim "
+                         f"{weight.shape[0]}")
+    dev = _device()
+    lops = LayerOps(model, dev)
+    part = DevicePartition.from_topology(topology, dev)
+    out = lops.layer_forward(layer, _to_dev(input_rows, dev), part)
+    return _to_host(out, weight.shape[1])
+
+
+def regather_backward(layer: int, partition: int, A_out: np.ndarray, grad_out: np.ndarray,
+                      cached_A_in: np.ndarray, plan: PartitionPlan, model: ModelState
+                      ) -> tuple[np.ndarray, np.ndarray]:
+    """Backward of one (layer, partition) from inputs regathered out of the
+    resident layer activations (training.py:146-163)."""
+    topo = plan.topologies[partition]
+    if cached_A_in is None or cached_A_in.shape[0] < plan.num_vertices:
+        raise ValueError(f"partition {partition} input activations are not resident; the "
+                         f"hierarchy must load them before backward")
+    if A_out.shape[0] != topo.targets.size or grad_out.shape != A_out.shape:
+        raise ValueError("output rows must match the partition's target count")
+    dev = _device()
+    lops = LayerOps(model, dev)
+    part = DevicePartition.from_topology(topo, dev)
+    d_in, d_out = model.dims[layer], model.dims[layer + 1]
+    a_in = _to_dev(cached_A_in, dev)
+    ga = ops.zeros_rows(part.num_gather, d_in, dev)
+    ops.gather_rows(a_in, part.gather_map, ga, d_in)
+    grad_ga, grad_w = lops.backward_from_ga(layer, ga, _to_dev(A_out, dev), _to_dev(grad_out, dev),
+                                            part)
+    return _to_host(grad_ga, d_in), _to_host(grad_w, d_out, d_in)
+
+
+def scatter_accumulate(grad_GA: np.ndarray, gather_map: np.ndarray,
+                       global_grad: np.ndarray) -> np.ndarray:
+    """global_grad[gather_map] += grad_GA in place (training.py:166-175)."""
+    dev = _device()
+    width = global_grad.shape[1]
+    g = _to_dev(global_grad, dev)
+    idx = torch.from_numpy(np.asarray(gather_map, dtype=np.int32)).to(dev)
+    ops.scatter_add_rows(_to_dev(grad_GA, dev), idx, g, width)
+    global_grad[...] = _to_host(g, width)
+    return global_grad
+
+
+# --------------------------------------------------------------------------
+# sessions: device-resident state reused across calls
+# --------------------------------------------------------------------------
+class TrainSession:
+    """Device-resident training state for one (dataset, plan, model config).
+
+    Uploads the plan once (cached on the plan object), keeps activations,
+    gradients and fp32 weights in HBM, and replays the fused epoch from a
+    CUDA graph.  ``partitioned_train`` uses one internally; benchmarks and
+    multi-epoch drivers can hold one explicitly.
+    """
+
+    def __init__(self, dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
+                 layerwise: bool = True, features: torch.Tensor | None = None):
+        if plan.num_vertices != dataset.graph.num_vertices:
+            raise ValueError("plan was built for a different graph")
+        self.dev = _device()
+        key = ("device_graph", str(self.dev))
+        dg = plan.device_cache.get(key)
+        if dg is None:
+            dg = DeviceGraph(dataset.graph, plan, self.dev)
+            plan.device_cache[key] = dg
+        self.dg = dg
+        self.model = copy_model(model)
+        self.dataset = dataset
+        if features is None:
+            features = self.upload_features(dataset, self.dev)
+        cls = LayerwiseEngine if layerwise else PartitionEngine
+        self.engine = cls(dg, self.model, features, dataset.labels, dataset.train_mask)
+        self.layerwise = layerwise
+        self._graph = None
+        self._graph_lr = None
+        self.stats_host = torch.zeros(4, dtype=torch.float64).pin_memory()
+
+    @staticmethod
+    def upload_features(dataset: LabeledDataset, dev) -> torch.Tensor:
+        f32 = dataset.features32()
+        n, f = f32.shape
+        t = ops.zeros_rows(n, f, dev)
+        src = torch.from_numpy(f32)
+        if t.shape[1] == f:
+            t.copy_(src, non_blocking=False)
+        else:
+            t[:, :f].copy_(src)
+        return t
+
+    def _capture(self, lr: float) -> None:
+        eng = self.engine
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            # warm-up outside capture so lazily built scale arrays / heavy-row
+            # scratch exist before the graph records their addresses
+            snap = [w.clone() for w in eng.wts.w]
+            eng.epoch(lr)
+            for w, s in zip(eng.wts.w, snap):
+                w.copy_(s)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            eng.epoch(lr)
+        self._graph, self._graph_lr = g, lr
+
+    def run_epoch(self, epoch: int, lr: float, use_graph: bool = True) -> None:
+        """Enqueue one fused epoch (loss stats land in engine.stats)."""
+        eng = self.engine
+        if eng.dropout_rate > 0.0:
+            eng.set_dropout(epoch)
+            use_graph = False   # fresh masks every epoch
+        if not use_graph:
+            eng.epoch(lr)
+            return
+        if self._graph is None or self._graph_lr != lr:
+            self._capture(lr)
+        self._graph.replay()
+
+    def read_stats(self) -> tuple[float, float]:
+        self.stats_host.copy_(self.engine.stats)
+        s = self.stats_host.numpy()
+        return float(s[0]), float(s[1])
+
+    def train(self, epochs: int, lr: float, hierarchy=None, use_snapshots=False, grad_probe=None,
+              partition_order=None, use_graph: bool = True):
+        P = self.dg.num_partitions
+
+        def order_of(layer: int, phase: str) -> list[int]:
+            if partition_order is not None:
+                return list(partition_order(layer, phase))
+            if hierarchy is not None:
+                return list(hierarchy.partition_order(layer, phase))
+            return list(range(P))
+
+        trace = []
+        for epoch in range(epochs):
+            if self.layerwise:
+                self.run_epoch(epoch, lr, use_graph=use_graph)
+                loss, acc = self.read_stats()
+                if not np.isfinite(loss):
+                    raise ValueError(f"non-finite loss {loss} at epoch {epoch}; "
+                                     f"reduce the learning rate or check the inputs")
+            else:
+                eng = self.engine
+                eng.set_dropout(epoch)
+                eng.epoch(epoch, lr, order_of, hierarchy=hierarchy, use_snapshots=use_snapshots,
+                          grad_probe=grad_probe, to_host=_to_host)
+                loss, acc = self.read_stats()
+            trace.append((epoch, loss, acc))
+        self.engine.wts.export(self.model)
+        return self.model, trace
+
+
+def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState, epochs: int,
+                      lr: float, hierarchy=None, use_snapshots: bool = False, grad_probe=None,
+                      partition_order=None):
+    """Partition-wise training with on-demand input regathering
+    (training.py:259-358).  Returns (model, trace, ledger)."""
+    if plan.num_vertices != dataset.graph.num_vertices:
+        raise ValueError("plan was built for a different graph")
+    observed = hierarchy is not None or use_snapshots or grad_probe is not None \
+        or partition_order is not None
+    session = TrainSession(dataset, plan, model, layerwise=not observed)
+    trained, trace = session.train(epochs, lr, hierarchy=hierarchy, use_snapshots=use_snapshots,
+                                   grad_probe=grad_probe, partition_order=partition_order)
+    if epochs == 0:
+        trained = copy_model(model)
+    return trained, trace, getattr(hierarchy, "ledger", None)
+
+
+def _whole_graph_plan(dataset: LabeledDataset) -> PartitionPlan:
+    n = dataset.graph.num_vertices
+    return build_partition_plan(dataset.graph, np.zeros(n, dtype=np.int32), 1)
+
+
+def reference_train(dataset: LabeledDataset, model: ModelState, epochs: int, lr: float):
+    """Whole-graph training (training.py:193-206): the P = 1 plan."""
+    trained, trace, _ = partitioned_train(dataset, _whole_graph_plan(dataset), model, epochs, lr)
+    return trained, trace
+
+
+def compute_gradients(dataset: LabeledDataset, model: ModelState):
+    """Monolithic loss, train accuracy and per-layer weight gradients
+    (training.py:231-236), without updating the weights."""
+    session = TrainSession(dataset, _whole_graph_plan(dataset), model)
+    trained, trace = session.train(1, 0.0, use_graph=False)
+    _, loss, acc = trace[0]
+    return loss, acc, trained.weight_grads
+
+
+def trace_to_csv(trace: list[tuple[int, float, float]]) -> str:
+    rows = ["epoch,loss,train_acc"] + [f"{e},{l!r},{a!r}" for e, l, a in trace]
+    return "\n".join(rows) + "\n"
+
+
+def write_trace_csv(path: str | Path, trace: list[tuple[int, float, float]]) -> None:
+    Path(path).write_text(trace_to_csv(trace))

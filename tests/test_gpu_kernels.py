@@ -1,0 +1,184 @@
+"""Kernel-level parity of the sm_100a library against float64 numpy."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from conftest import rel_l2  # noqa: E402
+from oracle import gcn  # noqa: E402
+from paper_2605_11517_b200 import ops  # noqa: E402
+
+DEV = "cuda"
+
+
+def _dev(mat, width=None):
+    mat = np.asarray(mat)
+    t = ops.zeros_rows(mat.shape[0], mat.shape[1] if width is None else width, DEV)
+    t[:, : mat.shape[1]] = torch.from_numpy(mat.astype(np.float32))
+    return t
+
+
+def _host(t, cols):
+    return t[:, :cols].double().cpu().numpy()
+
+
+def _random_csr(rng, n_rows, n_src, max_deg, hubs=()):
+    deg = rng.integers(0, max_deg + 1, size=n_rows)
+    for r, d in hubs:
+        deg[r] = d
+    ptr = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(deg, out=ptr[1:])
+    idx = rng.integers(0, n_src, size=int(ptr[-1])).astype(np.int32)
+    return ptr, idx
+
+
+@pytest.mark.parametrize("width", [1, 3, 4, 10, 16, 33, 64, 100, 128, 256, 300])
+def test_agg_sum_matches_numpy(width):
+    rng = np.random.default_rng(width)
+    n_rows, n_src = 700, 500
+    ptr, idx = _random_csr(rng, n_rows, n_src, 40, hubs=[(5, 1000), (77, 129), (300, 5000)])
+    out_idx = rng.permutation(n_rows).astype(np.int32)
+    self_idx = rng.integers(-1, n_src, size=n_rows).astype(np.int32)
+    y = rng.normal(size=(n_src, width))
+    src_scale = rng.uniform(0.1, 1.0, size=n_src)
+    post_scale = rng.uniform(0.1, 2.0, size=n_rows)
+    spec = ops.AggSpec.build(ptr, idx, DEV, out_idx=out_idx, self_idx=self_idx)
+    assert spec.n_segs > 0
+    yt = _dev(y)
+    out = ops.zeros_rows(n_rows, width, DEV)
+    ss = torch.from_numpy(src_scale.astype(np.float32)).to(DEV)
+    ps = torch.from_numpy(post_scale.astype(np.float32)).to(DEV)
+    ops.agg_sum(spec, yt, out, width, src_scale=ss, post_scale=ps, post_div_deg=True, relu=True)
+    want = np.zeros((n_rows, width))
+    for r in range(n_rows):
+        acc = (src_scale[idx[ptr[r]:ptr[r + 1]], None] * y[idx[ptr[r]:ptr[r + 1]]]).sum(axis=0)
+        if self_idx[r] >= 0:
+            acc = acc + src_scale[self_idx[r]] * y[self_idx[r]]
+        acc = acc / (ptr[r + 1] - ptr[r] + 1) * post_scale[out_idx[r]]
+        want[out_idx[r]] = np.maximum(acc, 0.0)
+    got = _host(out, width)
+    assert rel_l2(got, want) < 1e-6
+    # deterministic: a second launch is bitwise identical (heavy rows included)
+    out2 = ops.zeros_rows(n_rows, width, DEV)
+    ops.agg_sum(spec, yt, out2, width, src_scale=ss, post_scale=ps, post_div_deg=True, relu=True)
+    assert torch.equal(out, out2)
+    # padding columns stay zero
+    if out.shape[1] > width:
+        assert not out[:, width:].any()
+
+
+def test_agg_sum_mask_ref_and_defaults():
+    rng = np.random.default_rng(0)
+    n = 300
+    ptr, idx = _random_csr(rng, n, n, 12, hubs=[(3, 600)])
+    y = rng.normal(size=(n, 8))
+    ref = rng.normal(size=(n, 8))
+    spec = ops.AggSpec.build(ptr, idx, DEV)
+    out = ops.zeros_rows(n, 8, DEV)
+    ops.agg_sum(spec, _dev(y), out, 8, mask_ref=_dev(ref))
+    want = np.stack([y[idx[ptr[r]:ptr[r + 1]]].sum(axis=0) + y[r] for r in range(n)])
+    want = np.where(ref > 0, want, 0.0)
+    assert rel_l2(_host(out, 8), want) < 1e-6
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
+@pytest.mark.parametrize("m,n,k", [(1000, 64, 128), (257, 10, 64), (131, 47, 100), (64, 256, 300)])
+def test_gemm_matches_numpy(ta, tb, m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    a = rng.normal(size=(k, m) if ta else (m, k))
+    b = rng.normal(size=(n, k) if tb else (k, n))
+    rs = rng.uniform(0.5, 1.5, size=m)
+    em = rng.uniform(0.0, 2.0, size=(m, n))
+    rr = rng.normal(size=(m, n))
+    c = ops.zeros_rows(m, n, DEV)
+    ops.gemm(_dev(a), _dev(b), c, m, n, k, trans_a=ta, trans_b=tb,
+             row_scale=torch.from_numpy(rs.astype(np.float32)).to(DEV), elem_mul=_dev(em),
+             relu_ref=_dev(rr))
+    full = (a.T if ta else a) @ (b.T if tb else b)
+    want = np.where(rr > 0, full * rs[:, None] * em, 0.0)
+    assert rel_l2(_host(c, n), want) < 1e-6
+
+
+def test_gemm_relu_out_and_accumulate():
+    rng = np.random.default_rng(1)
+    a, b, c0 = rng.normal(size=(50, 12)), rng.normal(size=(12, 9)), rng.normal(size=(50, 9))
+    c = _dev(c0)
+    ops.gemm(_dev(a), _dev(b), c, 50, 9, 12, relu_out=True, accumulate=True)
+    assert rel_l2(_host(c, 9), c0 + np.maximum(a @ b, 0)) < 1e-6
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000)])
+def test_wgrad_sgd(m, n, k):
+    rng = np.random.default_rng(k)
+    a = rng.normal(size=(k, m)).astype(np.float32)
+    b = rng.normal(size=(k, n)).astype(np.float32)
+    w0 = rng.normal(size=(m, n))
+    dw = ops.zeros_rows(m, n, DEV)
+    w = _dev(w0)
+    ops.wgrad_sgd(_dev(a), _dev(b), dw, m, n, k, w=w, lr=0.25)
+    want = a.astype(np.float64).T @ b.astype(np.float64)
+    assert rel_l2(_host(dw, n), want) < 1e-5
+    assert rel_l2(_host(w, n), w0 - 0.25 * want) < 1e-5
+    dw2 = ops.zeros_rows(m, n, DEV)
+    ops.wgrad_sgd(_dev(a), _dev(b), dw2, m, n, k)
+    assert torch.equal(dw, dw2)
+    ops.wgrad_sgd(_dev(a), _dev(b), dw2, m, n, k, accumulate=True)
+    assert rel_l2(_host(dw2, n), 2 * want) < 1e-5
+
+
+@pytest.mark.parametrize("n,c", [(1000, 10), (777, 47), (300, 172), (64, 1)])
+def test_softmax_xent(n, c):
+    rng = np.random.default_rng(c)
+    logits = rng.normal(size=(n, c)) * 3
+    labels = rng.integers(0, c, size=n)
+    mask = rng.random(n) < 0.5
+    mask[0] = True
+    loss, grad = gcn.softmax_xent(logits, labels, mask)
+    acc = gcn.accuracy(logits, labels, mask)
+    g = ops.zeros_rows(n, c, DEV)
+    stats = torch.zeros(4, dtype=torch.float64, device=DEV)
+    ops.softmax_xent(_dev(logits), n, c, torch.from_numpy(labels.astype(np.int32)).to(DEV),
+                     torch.from_numpy(mask.astype(np.uint8)).to(DEV), int(mask.sum()), g, stats,
+                     ops.loss_partials(n, DEV))
+    s = stats.cpu().numpy()
+    assert s[0] == pytest.approx(loss, rel=1e-5)
+    assert s[1] == pytest.approx(acc, abs=1.5 / mask.sum())
+    assert rel_l2(_host(g, c), grad) < 1e-5
+
+
+def test_gather_and_scatter_rows():
+    rng = np.random.default_rng(3)
+    src = rng.normal(size=(100, 20))
+    idx = rng.permutation(100)[:60].astype(np.int32)
+    it = torch.from_numpy(idx).to(DEV)
+    dst = ops.zeros_rows(60, 20, DEV)
+    ops.gather_rows(_dev(src), it, dst, 20)
+    np.testing.assert_array_equal(_host(dst, 20), src[idx].astype(np.float32))
+    acc = _dev(np.ones((100, 20)))
+    ops.scatter_add_rows(dst, it, acc, 20)
+    want = np.ones((100, 20), dtype=np.float32)
+    want[idx] += src[idx].astype(np.float32)
+    np.testing.assert_array_equal(_host(acc, 20), want)
+
+
+def test_rownorm_kernels():
+    rng = np.random.default_rng(5)
+    pre = rng.normal(size=(50, 7))
+    pre[3] = 0.0
+    out = ops.zeros_rows(50, 7, DEV)
+    ops.rownorm_fwd(_dev(pre), out, 50, 7, relu=True)
+    norms = np.linalg.norm(pre, axis=1, keepdims=True)
+    unit = np.divide(pre, norms, out=np.zeros_like(pre), where=norms > 0)
+    assert rel_l2(_host(out, 7), np.maximum(unit, 0)) < 1e-6
+    g, a = rng.normal(size=(50, 7)), rng.normal(size=(50, 7))
+    gp = ops.zeros_rows(50, 7, DEV)
+    ops.rownorm_bwd(_dev(pre), _dev(g), gp, 50, 7, a_out=_dev(a))
+    gy = g * (a > 0)
+    want = np.divide(gy - unit * (unit * gy).sum(1, keepdims=True), norms,
+                     out=np.zeros_like(gy), where=norms > 0)
+    assert rel_l2(_host(gp, 7), want) < 1e-6

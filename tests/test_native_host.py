@@ -1,0 +1,136 @@
+"""Host-side native code (generator, partitioner, plan) — bit-exact with
+the reference (golden digests) and with the oracle.  Runs on CPU."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import graph as ograph, partition as opart, plan as oplan
+from paper_2605_11517_b200 import (PartitionerParams, build_csr, build_partition_plan,
+                                   generate_kronecker, random_partition,
+                                   switching_aware_partition)
+
+
+def _digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("scale,deg,seed", [(4, 2, 0), (6, 6, 3), (8, 8, 0), (9, 5, 17), (10, 12, 4)])
+def test_generator_matches_oracle(scale, deg, seed):
+    g = generate_kronecker(scale, deg, seed)
+    ptr, dst = ograph.kronecker(scale, deg, seed)
+    np.testing.assert_array_equal(g.src_ptr, ptr)
+    np.testing.assert_array_equal(g.dst_idx, dst)
+    g.validate()
+
+
+def test_generator_thread_count_invariant():
+    a = generate_kronecker(12, 8, 5, num_threads=1)
+    b = generate_kronecker(12, 8, 5, num_threads=7)
+    np.testing.assert_array_equal(a.dst_idx, b.dst_idx)
+
+
+def test_generator_rejects_bad_args():
+    with pytest.raises(ValueError):
+        generate_kronecker(3, 4, 0)
+    with pytest.raises(ValueError):
+        generate_kronecker(6, 0, 0)
+
+
+def test_build_csr_dedup_and_order():
+    g = build_csr([(2, 1), (0, 2), (2, 0), (0, 2), (2, 1), (1, 0)], 3)
+    assert g.src_ptr.tolist() == [0, 1, 2, 4]
+    assert g.dst_idx.tolist() == [2, 0, 1, 0]
+    empty = build_csr([], 4)
+    assert empty.num_edges == 0 and empty.src_ptr.tolist() == [0] * 5
+    with pytest.raises(ValueError):
+        build_csr([(0, 5)], 3)
+
+
+@pytest.mark.parametrize("scale,deg,P,depth", [(7, 6, 3, 2), (8, 8, 4, 2), (8, 8, 4, 3), (9, 4, 6, 2)])
+def test_partitioner_matches_oracle(scale, deg, P, depth):
+    g = generate_kronecker(scale, deg, scale)
+    res = switching_aware_partition(g, P, PartitionerParams(seed=scale + 2, group_depth=depth))
+    ref = opart.partition(g.src_ptr, g.dst_idx, P, group_depth=depth, seed=scale + 2)
+    np.testing.assert_array_equal(res.labels, ref["labels"])
+    assert res.objective_trace == ref["objective_trace"]
+    assert res.initial_objective == ref["initial_objective"]
+    assert res.iterations == ref["iterations"]
+    assert res.converged == ref["converged"]
+    assert res.max_size_per_iteration == ref["max_size_per_iteration"]
+
+
+def test_partitioner_capacity_and_single_partition():
+    g = generate_kronecker(8, 8, 1)
+    res = switching_aware_partition(g, 4, PartitionerParams(seed=1, beta=1.2, alpha_balance=1.1))
+    cap = int(np.floor(1.2 * g.num_vertices / 4 + 1e-9))
+    assert max(res.max_size_per_iteration[1:]) <= cap
+    one = switching_aware_partition(g, 1)
+    assert one.iterations == 0 and one.converged and not one.labels.any()
+
+
+def test_random_partition_balanced():
+    lab = random_partition(103, 5, seed=2)
+    counts = np.bincount(lab, minlength=5)
+    assert counts.max() - counts.min() <= 1
+    np.testing.assert_array_equal(lab, opart.random_labels(103, 5, 2))
+
+
+def test_config1_generator_partitioner_plan_exact(config1_golden):
+    gold = config1_golden
+    g = generate_kronecker(17, 8, seed=0)
+    assert _digest(g.src_ptr, g.dst_idx) == str(gold["graph_digest"])
+    res = switching_aware_partition(g, 8, PartitionerParams(seed=2))
+    np.testing.assert_array_equal(res.labels, gold["sa_labels"].astype(np.int32))
+    assert res.objective_trace == gold["sa_objective_trace"].tolist()
+    assert res.initial_objective == float(gold["sa_initial_objective"])
+    assert res.iterations == int(gold["sa_iterations"])
+    assert res.converged == bool(gold["sa_converged"])
+    assert res.max_size_per_iteration == gold["sa_max_sizes"].tolist()
+    plan = build_partition_plan(g, res.labels, 8)
+    for q, t in enumerate(plan.topologies):
+        assert _digest(t.targets, t.gather_map, t.tgt_ptr, t.src_pos, t.edge_local_target,
+                       t.self_pos, t.target_indeg, t.gather_indeg) == str(gold[f"plan_digest_{q}"])
+
+
+@pytest.mark.parametrize("scale,deg,P", [(6, 4, 3), (8, 8, 5), (9, 6, 8)])
+def test_plan_matches_oracle(scale, deg, P):
+    g = generate_kronecker(scale, deg, scale)
+    labels = random_partition(g.num_vertices, P, seed=scale)
+    plan = build_partition_plan(g, labels, P)
+    ref = oplan.build_plan(g.src_ptr, g.dst_idx, labels, P)
+    for a, b in zip(plan.topologies, ref):
+        for f in ("targets", "gather_map", "tgt_ptr", "src_pos", "edge_local_target", "self_pos",
+                  "target_indeg", "gather_indeg"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_plan_kat_and_edge_cases():
+    # reference test_training.py:45-56 — partition 0 gathers [0, 1, 4, 6, 7]
+    g = build_csr([(4, 0), (6, 1), (7, 1), (0, 1), (1, 0), (2, 3), (3, 2), (5, 4)], 8)
+    plan = build_partition_plan(g, np.array([0, 0, 1, 1, 2, 2, 3, 3], dtype=np.int32), 4)
+    assert plan.gather_maps[0].tolist() == [0, 1, 4, 6, 7]
+    assert plan.target_ranges[0].tolist() == [0, 1]
+    # empty partitions (test_training.py:91-96)
+    g2 = build_csr([(0, 1), (1, 0)], 2)
+    plan2 = build_partition_plan(g2, np.zeros(2, dtype=np.int32), 3)
+    assert plan2.empty_partitions == [1, 2]
+    assert plan2.topologies[1].num_edges == 0
+    with pytest.raises(ValueError):
+        build_partition_plan(g2, np.array([0, 3], dtype=np.int32), 3)
+    with pytest.raises(ValueError):
+        build_partition_plan(g2, np.zeros(3, dtype=np.int32), 1)
+    # single partition = whole graph
+    g3 = generate_kronecker(6, 6, seed=3)
+    p3 = build_partition_plan(g3, np.zeros(g3.num_vertices, dtype=np.int32), 1)
+    np.testing.assert_array_equal(p3.gather_maps[0], np.arange(g3.num_vertices))
+    assert p3.topologies[0].num_edges == g3.num_edges
