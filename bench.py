@@ -1,0 +1,363 @@
+"""Benchmark of the partition-wise full-graph training step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A step is one full-graph training epoch (forward over every partition, loss,
+regather backward, SGD) of the named synthetic workload.  Prints ONE JSON
+line (rank 0).  Metric (BASELINE.json): aggregated edges/s = L*|E| per epoch
+over all GPUs, plus epoch time; ``roofline`` covers the dominant kernel and
+``agg_roofline`` the aggregation kernels (north star: >= 60% of HBM peak).
+
+--impl reference times the reference algorithm's CPU implementation — the
+float64 numpy port in oracle/ (the reference is pure Python and cannot be
+shipped to the GPU box; oracle/ is pinned to its golden vectors) — on the
+host cores, on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# name -> synthetic workload (BASELINE.json configs; seeds follow the
+# reference CLI: graph S, dataset S+1, partitioner S+2, model S+3; lr 0.01)
+WORKLOADS = {
+    "config1": dict(
+        desc="configs[0]: 2-layer GCN hidden 64, generate_kronecker(17, 8): 131,072 V / "
+             "1,048,576 E, 128 feats, 10 classes, 8 switching-aware partitions",
+        scale=17, deg=8, F=128, C=10, L=2, H=64, P=8, mode="mean_self_loop"),
+}
+DEFAULT_WORKLOAD = "config1"
+LR = 0.01
+SEED = 0
+
+
+def rank_info():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def build_workload(spec):
+    import paper_2605_11517_b200 as g2
+    t0 = time.perf_counter()
+    g = g2.generate_kronecker(spec["scale"], spec["deg"], seed=SEED)
+    t_gen = time.perf_counter() - t0
+    ds = g2.make_random_dataset(g, feature_dim=spec["F"], num_classes=spec["C"], seed=SEED + 1)
+    t1 = time.perf_counter()
+    part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2))
+    t_part = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    plan = g2.build_partition_plan(g, part.labels, spec["P"])
+    t_plan = time.perf_counter() - t2
+    model = g2.create_model(spec["F"], spec["C"], num_layers=spec["L"], hidden_dim=spec["H"],
+                            seed=SEED + 3, aggregation_mode=spec["mode"])
+    prep = {"generate_s": round(t_gen, 3), "partition_s": round(t_part, 3),
+            "plan_s": round(t_plan, 3), "partitioner_iterations": part.iterations}
+    return g, ds, plan, model, prep
+
+
+class ClockSampler:
+    """NVML sampling of SM clock / throttle reasons while the timed region runs."""
+
+    REASONS = {
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4,
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(index).uuid)
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(
+                    uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(0 if pynvml.nvmlDeviceGetCount() == 1 else index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+        self.active = False
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            if self.nv is not None and self.active:
+                try:
+                    mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                    getr = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                        self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                    mask = getr(self.h)
+                    self.samples.append((mhz, util))
+                    for name, bit in self.REASONS.items():
+                        if mask & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
+    def summary(self):
+        self._stop.set()
+        loaded = [m for m, u in self.samples if u > 0] or [m for m, _ in self.samples]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1671.0)), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def flush_l2(buf):
+    buf.add_(1.0)   # 512 MiB write evicts the 126 MB L2 between timed steps
+
+
+def run_ours(args, spec, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_11517_b200 as g2
+    from paper_2605_11517_b200 import ops
+    from paper_2605_11517_b200.training import TrainSession
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g, ds, plan, model, prep = build_workload(spec)
+    L, E = spec["L"], g.num_edges
+    sess = TrainSession(ds, plan, model)
+    flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    # ---- instrumented epoch: per-kernel CUDA-event timing + launch count --
+    sess.run_epoch(0, LR, use_graph=False)
+    torch.cuda.synchronize()
+    ops.RECORDER.reset()
+    ops.RECORDER.timing = True
+    flush_l2(flush)
+    sess.engine.epoch(LR)
+    torch.cuda.synchronize()
+    ops.RECORDER.timing = False
+    launches_per_epoch = ops.RECORDER.launches
+    per_kernel = {}
+    for name, nbytes, flops, s, e in ops.RECORDER.records:
+        k = per_kernel.setdefault(name, {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "launches": 0})
+        k["ms"] += s.elapsed_time(e)
+        k["bytes"] += nbytes
+        k["flops"] += flops
+        k["launches"] += 1
+    ops.RECORDER.reset()
+
+    # ---- timed region: K graph-replayed epochs, L2 flushed between steps --
+    for w in range(args.warmup):
+        flush_l2(flush)
+        sess.run_epoch(w, LR)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.active = True
+    events = []
+    for k in range(args.steps):
+        flush_l2(flush)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        sess.run_epoch(args.warmup + k, LR)
+        e.record()
+        events.append((s, e))
+    torch.cuda.synchronize()
+    clocks.active = False
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in events]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    loss, acc = sess.read_stats()
+
+    # ---- e2e: public API, host buffers, H2D/D2H inside the timed region --
+    f32 = torch.empty(ds.features.shape, dtype=torch.float32).pin_memory()
+    f32.numpy()[...] = ds.features
+    ds_e2e = g2.LabeledDataset(graph=ds.graph, features=f32.numpy(), labels=ds.labels,
+                               train_mask=ds.train_mask)
+    for _ in range(max(1, args.warmup)):
+        g2.partitioned_train(ds_e2e, plan, model, epochs=1, lr=LR)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        trained, trace, _ = g2.partitioned_train(ds_e2e, plan, model, epochs=1, lr=LR)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = ds.features.size * 4 + ds.labels.size * 4 + ds.train_mask.size + \
+        sum(w.size * 4 for w in model.weights)
+    d2h = sum(w.size * 8 * 2 for w in model.weights) + 32
+
+    clock = clocks.summary()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    hbm_peak, tf_peak, peak_kind = load_peaks()
+    dom = max(per_kernel, key=lambda n: per_kernel[n]["ms"])
+    epoch_ms_instr = sum(k["ms"] for k in per_kernel.values())
+
+    def roof(name):
+        k = per_kernel[name]
+        gbs = k["bytes"] / (k["ms"] * 1e-3) / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None,
+                "peak_source": peak_kind, "launches_per_epoch": k["launches"],
+                "ms_per_epoch": round(k["ms"], 4),
+                "share_of_epoch": round(k["ms"] / epoch_ms_instr, 4)}
+
+    traffic_file = ROOT / "profiles" / "traffic.json"
+    roofline = roof(dom)
+    agg_roof = roof("agg_sum")
+    if traffic_file.exists():
+        tr = json.loads(traffic_file.read_text()).get(args.workload, {})
+        for r in (roofline, agg_roof):
+            if r["kernel"] in tr:
+                r["traffic"] = tr[r["kernel"]]
+    edges_per_epoch = L * E
+    value = world * edges_per_epoch / (ms_per_step * 1e-3)
+    out = {
+        "metric": "aggregated edges/s (L*|E| per full-graph training epoch)",
+        "value": round(value, 1),
+        "unit": "edges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "epoch_s": round(ms_per_step * 1e-3, 7),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (bit-exact reference generator / dataset / partitioner; random-init weights)",
+        "config": {
+            "workload": args.workload, "desc": spec["desc"], "num_vertices": g.num_vertices,
+            "num_edges": E, "layers": L, "hidden": spec["H"], "features": spec["F"],
+            "classes": spec["C"], "partitions": spec["P"], "aggregation": spec["mode"],
+            "parallelism": "single" if world == 1 else f"replicas{world}",
+            "l2": "flushed (512 MiB write) before every timed step", "lr": LR,
+            "preprocess": prep, "loss_last_step": loss, "acc_last_step": acc,
+        },
+        "e2e": {"value": round(world * edges_per_epoch / e2e_s, 1), "unit": "edges/s",
+                "s_per_step": round(e2e_s, 6), "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "api": "paper_2605_11517_b200.partitioned_train(..., epochs=1) with pinned host features"},
+        "roofline": roofline,
+        "agg_roofline": agg_roof,
+        "kernels": {n: {"ms_per_epoch": round(k["ms"], 4), "launches": k["launches"],
+                        "GB_per_epoch": round(k["bytes"] / 1e9, 4),
+                        "GFLOP_per_epoch": round(k["flops"] / 1e9, 4)}
+                    for n, k in sorted(per_kernel.items(), key=lambda kv: -kv[1]["ms"])},
+        "clocks": clock,
+        "gpu_launches": launches_per_epoch * args.steps,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(spec, g, ds, plan, model)
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+def oracle_epoch_seconds(spec, ds, plan, model, epochs=1):
+    from oracle import gcn
+    topos = plan.topologies
+    t0 = time.perf_counter()
+    gcn.train_partitioned(ds.features, ds.labels, ds.train_mask, topos, model.weights, epochs, LR,
+                          mode=spec["mode"])
+    return (time.perf_counter() - t0) / epochs
+
+
+def cpu_baseline(spec, g, ds, plan, model):
+    secs = oracle_epoch_seconds(spec, ds, plan, model)
+    return {"value": round(spec["L"] * g.num_edges / secs, 1), "unit": "edges/s",
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one full epoch of {spec['desc'].split(':')[0]} in oracle/gcn.py "
+                      f"(float64 numpy restatement of the reference, pinned to its golden "
+                      f"vectors; OpenBLAS on all host threads): {secs:.2f} s"}
+
+
+def run_reference(args, spec, rank, world):
+    if rank != 0:
+        return None
+    g, ds, plan, model, prep = build_workload(spec)
+    for _ in range(args.warmup):
+        oracle_epoch_seconds(spec, ds, plan, model)
+    times = [oracle_epoch_seconds(spec, ds, plan, model) for _ in range(args.steps)]
+    secs = sum(times) / len(times)
+    value = spec["L"] * g.num_edges / secs
+    return {
+        "impl": "reference",
+        "metric": "aggregated edges/s (L*|E| per full-graph training epoch)",
+        "value": round(value, 1), "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 3), "epoch_s": round(secs, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "desc": spec["desc"],
+                                        "num_edges": g.num_edges, "preprocess": prep},
+        "cpu_baseline": {"value": round(value, 1), "unit": "edges/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": "one full epoch per step, oracle/gcn.py"},
+        "e2e": {"value": round(value, 1), "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank, world, local_rank = rank_info()
+    spec = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        out = run_reference(args, spec, rank, world)
+    else:
+        out = run_ours(args, spec, rank, world, local_rank)
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -162,11 +162,16 @@ typedef struct grd_agg_args {
 } grd_agg_args;
 int grd_agg_sum(const grd_agg_args* args, void* stream);
 
-/* K3/K6/K7 — dense fp32 GEMM with fused epilogue (training.py:76,128-129):
+/* K3/K6/K7 — dense fp32 GEMM on tcgen05 tensor cores, 3xTF32 split
+ * (fp32-grade accuracy), with fused epilogue (training.py:76,128-129):
  *   C[m,n] = epi( sum_k opA(A)[m,k] * opB(B)[k,n] )
- * transA: A stored K x M (lda);  transB: B stored N x K (ldb).
- * epi: acc *= row_scale[m]; acc *= col_mul[m,n] (ldcm); acc = relu_ref[m,n]>0 ? acc : 0;
- * then C = acc (accumulate=0) or C += acc.  Pointers are nullable. */
+ * transA: A stored K x M (lda);  transB: B stored N x K (ldb).  B (the
+ * weight operand) is pre-split into `workspace`, which needs
+ * grd_gemm_workspace(n, k) floats.  Leading dimensions must be multiples of
+ * 4 and matrices 16-byte aligned (TMA).
+ * epi: acc *= row_scale[m]; acc *= elem_mul[m,n]; acc = relu_ref[m,n]>0 ? acc : 0;
+ * relu_out: max(acc,0); then C = acc (accumulate=0) or C += acc.  Epilogue
+ * pointers are nullable; columns up to round_up(n,4) are written. */
 typedef struct grd_gemm_args {
     int64_t m, n, k;
     const float* a; int64_t lda; int32_t trans_a;
@@ -178,7 +183,10 @@ typedef struct grd_gemm_args {
     const float* relu_ref; int64_t ld_relu_ref;
     int32_t relu_out;          /* apply max(acc, 0) */
     int32_t accumulate;
+    float* workspace;          /* >= grd_gemm_workspace(n, k) floats */
+    int64_t workspace_elems;
 } grd_gemm_args;
+int64_t grd_gemm_workspace(int64_t n, int64_t k);
 int grd_gemm(const grd_gemm_args* args, void* stream);
 
 /* K6 — weight gradient  dW = A^T B  with K = number of rows (long), as a

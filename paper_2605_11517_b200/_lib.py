@@ -85,6 +85,8 @@ class GrdGemmArgs(ctypes.Structure):
         ("ld_relu_ref", c_i64),
         ("relu_out", c_i32),
         ("accumulate", c_i32),
+        ("workspace", c_vp),
+        ("workspace_elems", c_i64),
     ]
 
 
@@ -104,6 +106,7 @@ SIGNATURES = {
     "grd_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_agg_sum": (c_i32, [ctypes.POINTER(GrdAggArgs), c_vp]),
     "grd_gemm": (c_i32, [ctypes.POINTER(GrdGemmArgs), c_vp]),
+    "grd_gemm_workspace": (c_i64, [c_i64, c_i64]),
     "grd_wgrad_workspace": (c_i64, [c_i64, c_i64, c_i64]),
     "grd_wgrad_sgd": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32,
                               c_vp, c_i64, c_f32, c_vp, c_i64, c_vp]),

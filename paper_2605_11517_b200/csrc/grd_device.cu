@@ -17,6 +17,7 @@
 
 #include "../../include/grinder_b200.h"
 #include "grd_common.h"
+#include "grd_gemm_tc.h"
 
 using namespace grd;
 
@@ -53,76 +54,72 @@ __device__ __forceinline__ float4 ld_nc_f4(const float* p) {
 }
 
 // ------------------------------------------------------------------- K2 --
-// Warp per row (or per heavy-row segment).  The warp is split into
-// NG = 32/LPR lane groups; a group owns one edge at a time and each lane of
-// the group holds NV float4 column chunks of the row.  U edges per group are
-// loaded before they are summed to keep U*NG row reads in flight per warp.
+// The warp is split into NG = 32/LPR lane groups of LPR lanes; each lane of a
+// group holds NV float4 column chunks of a row (width <= 4*LPR*NV).
+//  * light rows (degree <= heavy_threshold): one row per lane GROUP, so a
+//    warp keeps NG rows in flight; each group walks its own edge list with
+//    U row loads issued before they are summed (sequential per row).
+//  * heavy-row segments: one segment per WARP, the NG groups splitting its
+//    edges, combined by a fixed-order butterfly; the last segment of a row
+//    to finish sums the segment partials in segment order (deterministic).
+template <int LPR, int NV>
+__device__ __forceinline__ void load_row(const float* row, int sub, int w4, float4 (&v)[NV]) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = sub + c * LPR;
+        v[c] = q < w4 ? ld_nc_f4(row + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// acc += sum over edges e = beg + first, beg + first + stride, ... < end
 template <int LPR, int NV, int U>
-__device__ __forceinline__ void agg_accumulate(const grd_agg_args& a, int64_t beg, int64_t end,
-                                               int lane, int w4, float4 (&acc)[NV]) {
-    constexpr int NG = kWarp / LPR;
-    const int g = lane / LPR;
-    const int sub = lane % LPR;
+__device__ __forceinline__ void agg_edges(const grd_agg_args& a, int64_t beg, int64_t end, int stride,
+                                          int sub, int w4, float4 (&acc)[NV]) {
     const float* __restrict__ y = a.y;
     const int32_t* __restrict__ idx = a.idx;
     const float* __restrict__ ss = a.src_scale;
-    int64_t e = beg + g;
-    for (; e + int64_t(U - 1) * NG < end; e += int64_t(U) * NG) {
+    int64_t e = beg;
+    for (; e + int64_t(U - 1) * stride < end; e += int64_t(U) * stride) {
         int32_t j[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) j[u] = __ldg(idx + e + int64_t(u) * NG);
+        for (int u = 0; u < U; ++u) j[u] = __ldg(idx + e + int64_t(u) * stride);
         float4 v[U][NV];
         float s[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             s[u] = ss ? __ldg(ss + j[u]) : 1.0f;
-            const float* row = y + int64_t(j[u]) * a.ldy;
-#pragma unroll
-            for (int c = 0; c < NV; ++c) {
-                const int q = sub + c * LPR;
-                v[u][c] = q < w4 ? ld_nc_f4(row + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+            load_row<LPR, NV>(y + int64_t(j[u]) * a.ldy, sub, w4, v[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[u], v[u][c], acc[c]);
     }
-    for (; e < end; e += NG) {
+    for (; e < end; e += stride) {
         const int32_t jj = __ldg(idx + e);
         const float s = ss ? __ldg(ss + jj) : 1.0f;
-        const float* row = y + int64_t(jj) * a.ldy;
+        float4 v[NV];
+        load_row<LPR, NV>(y + int64_t(jj) * a.ldy, sub, w4, v);
 #pragma unroll
-        for (int c = 0; c < NV; ++c) {
-            const int q = sub + c * LPR;
-            if (q < w4) acc[c] = f4_fma(s, ld_nc_f4(row + 4 * q), acc[c]);
-        }
+        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s, v[c], acc[c]);
     }
-    // Fixed-order butterfly across lane groups.
-#pragma unroll
-    for (int off = kWarp / 2; off >= LPR; off >>= 1)
-#pragma unroll
-        for (int c = 0; c < NV; ++c) acc[c] = f4_add(acc[c], f4_shfl_xor(acc[c], off));
 }
 
+// self term, post-scale, activation, mask, store — by the LPR lanes of a group
 template <int LPR, int NV>
-__device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg,
-                                           int lane, int w4, float4 (&acc)[NV]) {
-    const int sub = lane % LPR;
+__device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg, int sub,
+                                           int w4, float4 (&acc)[NV]) {
     const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
     const int32_t srow = a.self_idx ? a.self_idx[r] : orow;
     if (srow >= 0) {
         const float s = a.src_scale ? a.src_scale[srow] : 1.0f;
-        const float* row = a.y + int64_t(srow) * a.ldy;
+        float4 v[NV];
+        load_row<LPR, NV>(a.y + int64_t(srow) * a.ldy, sub, w4, v);
 #pragma unroll
-        for (int c = 0; c < NV; ++c) {
-            const int q = sub + c * LPR;
-            if (q < w4) acc[c] = f4_fma(s, ld_nc_f4(row + 4 * q), acc[c]);
-        }
+        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s, v[c], acc[c]);
     }
     const float div = static_cast<float>(deg + 1);
     const float ps = a.post_scale ? a.post_scale[orow] : 1.0f;
-    if (lane >= LPR) return;
     float* out = a.out + int64_t(orow) * a.ldo;
 #pragma unroll
     for (int c = 0; c < NV; ++c) {
@@ -147,23 +144,27 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
 }
 
 template <int LPR, int NV, int U>
-__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a) {
+__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a, int64_t light_warps) {
+    constexpr int NG = kWarp / LPR;
     const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const int g = lane / LPR;
+    const int sub = lane % LPR;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const int w4 = (a.width + 3) / 4;
     float4 acc[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    if (item < a.n_rows) {
-        const int64_t r = item;
+    if (warp < light_warps) {
+        const int64_t r = warp * NG + g;
+        if (r >= a.n_rows) return;
         const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
         if (a.heavy_threshold > 0 && end - beg > a.heavy_threshold) return;  // segmented
-        agg_accumulate<LPR, NV, U>(a, beg, end, lane, w4, acc);
-        agg_finish<LPR, NV>(a, r, end - beg, lane, w4, acc);
+        agg_edges<LPR, NV, U>(a, beg, end, 1, sub, w4, acc);
+        agg_finish<LPR, NV>(a, r, end - beg, sub, w4, acc);
         return;
     }
-    const int64_t s = item - a.n_rows;
+    const int64_t s = warp - light_warps;
     if (s >= a.n_segs) return;
     const int32_t h = a.seg_heavy[s];
     const int64_t r = a.heavy_rows[h];
@@ -171,9 +172,12 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a) {
     const int64_t rb = a.row_ptr[r], re = a.row_ptr[r + 1];
     const int64_t beg = rb + (s - seg0) * a.seg_len;
     const int64_t end = min(beg + int64_t(a.seg_len), re);
-    agg_accumulate<LPR, NV, U>(a, beg, end, lane, w4, acc);
+    agg_edges<LPR, NV, 4>(a, beg + g, end, NG, sub, w4, acc);
+#pragma unroll
+    for (int off = kWarp / 2; off >= LPR; off >>= 1)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] = f4_add(acc[c], f4_shfl_xor(acc[c], off));
     const int ldp = 4 * w4;
-    const int sub = lane % LPR;
     if (lane < LPR) {
         float* part = a.seg_partial + s * ldp;
 #pragma unroll
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a) {
     if (ticket != nseg - 1) return;
     // Last segment to finish: combine partials in segment order.
     __threadfence();
+    if (lane >= LPR) return;
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t t = 0; t < nseg; ++t) {
@@ -200,16 +205,18 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a) {
             if (q < w4) acc[c] = f4_add(acc[c], __ldcg(reinterpret_cast<const float4*>(part + 4 * q)));
         }
     }
-    agg_finish<LPR, NV>(a, r, re - rb, lane, w4, acc);
+    agg_finish<LPR, NV>(a, r, re - rb, sub, w4, acc);
     if (lane == 0) a.heavy_counter[h] = 0;
 }
 
 template <int LPR, int NV, int U>
 int launch_agg(const grd_agg_args& a, cudaStream_t st) {
-    const int64_t items = a.n_rows + a.n_segs;
-    if (items == 0) return 0;
-    const int64_t blocks = (items * kWarp + 255) / 256;
-    agg_sum_kernel<LPR, NV, U><<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+    constexpr int NG = kWarp / LPR;
+    const int64_t light_warps = (a.n_rows + NG - 1) / NG;
+    const int64_t warps = light_warps + a.n_segs;
+    if (warps == 0) return 0;
+    const int64_t blocks = (warps * kWarp + 255) / 256;
+    agg_sum_kernel<LPR, NV, U><<<static_cast<unsigned>(blocks), 256, 0, st>>>(a, light_warps);
     return launch_status("agg_sum");
 }
 
@@ -238,177 +245,36 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const float* __restrict__
     }
 }
 
-// ----------------------------------------------------------- K3/K6/K7 --
-// Tiled fp32 SIMT GEMM (CUDA-core FMA path; fp32-exact products).
-constexpr int kBM = 128, kBN = 64, kBK = 16, kTM = 8, kTN = 4;
-constexpr int kGemmThreads = (kBM / kTM) * (kBN / kTN);  // 256
-
-struct GemmTile {
-    int64_t m, n, k, k0, k1;
-    const float* a; int64_t lda; bool ta;
-    const float* b; int64_t ldb; bool tb;
-};
-
-__device__ __forceinline__ void gemm_mainloop(const GemmTile& t, int64_t m0, int64_t n0,
-                                              float (&acc)[kTM][kTN]) {
-    __shared__ __align__(16) float As[2][kBK][kBM];
-    __shared__ __align__(16) float Bs[2][kBK][kBN];
-    const int tid = threadIdx.x;
-    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
-    // Per-thread load assignments: A tile = 128x16 = 2048 floats (8/thread),
-    // B tile = 16x64 = 1024 floats (4/thread).
-    float ra[8], rb[4];
-    auto load_a = [&](int64_t kb) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int li = tid + i * kGemmThreads;
-            int mm, kk;
-            if (!t.ta) { mm = li / kBK; kk = li % kBK; }   // row-major: k fastest
-            else       { kk = li / kBM; mm = li % kBM; }   // K x M: m fastest
-            const int64_t gm = m0 + mm, gk = kb + kk;
-            float v = 0.f;
-            if (gm < t.m && gk < t.k1)
-                v = t.ta ? __ldg(t.a + gk * t.lda + gm) : __ldg(t.a + gm * t.lda + gk);
-            ra[i] = v;
-        }
-    };
-    auto store_a = [&](int buf) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int li = tid + i * kGemmThreads;
-            int mm, kk;
-            if (!t.ta) { mm = li / kBK; kk = li % kBK; }
-            else       { kk = li / kBM; mm = li % kBM; }
-            As[buf][kk][mm] = ra[i];
-        }
-    };
-    auto load_b = [&](int64_t kb) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int li = tid + i * kGemmThreads;
-            int kk, nn;
-            if (!t.tb) { kk = li / kBN; nn = li % kBN; }   // K x N: n fastest
-            else       { nn = li / kBK; kk = li % kBK; }   // N x K: k fastest
-            const int64_t gk = kb + kk, gn = n0 + nn;
-            float v = 0.f;
-            if (gn < t.n && gk < t.k1)
-                v = t.tb ? __ldg(t.b + gn * t.ldb + gk) : __ldg(t.b + gk * t.ldb + gn);
-            rb[i] = v;
-        }
-    };
-    auto store_b = [&](int buf) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int li = tid + i * kGemmThreads;
-            int kk, nn;
-            if (!t.tb) { kk = li / kBN; nn = li % kBN; }
-            else       { nn = li / kBK; kk = li % kBK; }
-            Bs[buf][kk][nn] = rb[i];
-        }
-    };
-#pragma unroll
-    for (int i = 0; i < kTM; ++i)
-#pragma unroll
-        for (int j = 0; j < kTN; ++j) acc[i][j] = 0.f;
-    if (t.k0 >= t.k1) return;
-    load_a(t.k0);
-    load_b(t.k0);
-    store_a(0);
-    store_b(0);
-    __syncthreads();
-    int buf = 0;
-    for (int64_t kb = t.k0; kb < t.k1; kb += kBK) {
-        const bool more = kb + kBK < t.k1;
-        if (more) { load_a(kb + kBK); load_b(kb + kBK); }
-#pragma unroll
-        for (int kk = 0; kk < kBK; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * kTM]);
-            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * kTM + 4]);
-            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * kTN]);
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bv[4] = {b0.x, b0.y, b0.z, b0.w};
-#pragma unroll
-            for (int i = 0; i < kTM; ++i)
-#pragma unroll
-                for (int j = 0; j < kTN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-        }
-        if (more) {
-            store_a(buf ^ 1);
-            store_b(buf ^ 1);
-            __syncthreads();
-            buf ^= 1;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kGemmThreads) gemm_kernel(const grd_gemm_args g) {
-    const int64_t m0 = int64_t(blockIdx.x) * kBM, n0 = int64_t(blockIdx.y) * kBN;
-    GemmTile t{g.m, g.n, g.k, 0, g.k, g.a, g.lda, g.trans_a != 0, g.b, g.ldb, g.trans_b != 0};
-    float acc[kTM][kTN];
-    gemm_mainloop(t, m0, n0, acc);
-    const int tid = threadIdx.x;
-    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
-#pragma unroll
-    for (int i = 0; i < kTM; ++i) {
-        const int64_t m = m0 + ty * kTM + i;
-        if (m >= g.m) continue;
-        const float rs = g.row_scale ? g.row_scale[m] : 1.0f;
-#pragma unroll
-        for (int j = 0; j < kTN; ++j) {
-            const int64_t n = n0 + tx * kTN + j;
-            if (n >= g.n) continue;
-            float v = acc[i][j];
-            if (g.row_scale) v *= rs;
-            if (g.elem_mul) v *= g.elem_mul[m * g.ld_elem_mul + n];
-            if (g.relu_ref && !(g.relu_ref[m * g.ld_relu_ref + n] > 0.f)) v = 0.f;
-            if (g.relu_out) v = fmaxf(v, 0.f);
-            float* c = g.c + m * g.ldc + n;
-            *c = g.accumulate ? *c + v : v;
-        }
-    }
-}
-
-// Split-K weight gradient: blockIdx.z selects a fixed K chunk.
-__global__ void __launch_bounds__(kGemmThreads) wgrad_partial_kernel(
-        int64_t m, int64_t n, int64_t k, int64_t kchunk, const float* a, int64_t lda,
-        const float* b, int64_t ldb, float* ws) {
-    const int64_t m0 = int64_t(blockIdx.x) * kBM, n0 = int64_t(blockIdx.y) * kBN;
-    const int64_t k0 = int64_t(blockIdx.z) * kchunk;
-    GemmTile t{m, n, k, k0, min(k0 + kchunk, k), a, lda, true, b, ldb, false};
-    float acc[kTM][kTN];
-    gemm_mainloop(t, m0, n0, acc);
-    float* out = ws + int64_t(blockIdx.z) * m * n;
-    const int tid = threadIdx.x;
-    const int tx = tid % (kBN / kTN), ty = tid / (kBN / kTN);
-#pragma unroll
-    for (int i = 0; i < kTM; ++i) {
-        const int64_t mm = m0 + ty * kTM + i;
-        if (mm >= m) continue;
-#pragma unroll
-        for (int j = 0; j < kTN; ++j) {
-            const int64_t nn = n0 + tx * kTN + j;
-            if (nn < n) out[mm * n + nn] = acc[i][j];
-        }
-    }
-}
-
-__global__ void wgrad_reduce_kernel(int64_t m, int64_t n, int64_t splits, const float* ws,
+// ----------------------------------------------------------- K6 reduce --
+// Split-K partials of the tensor-core weight gradient are summed here in a
+// fixed order (no float atomics), fused with the SGD step.
+__global__ void wgrad_reduce_kernel(int64_t m, int64_t n, int64_t splits, int64_t ldp, const float* ws,
                                     float* dw, int64_t lddw, int accumulate, float* w, int64_t ldw,
                                     float lr) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // warp per output element: lane z sums splits z, z+32, ...; fixed butterfly
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     if (i >= m * n) return;
     float s = 0.f;
-    for (int64_t z = 0; z < splits; ++z) s += ws[z * m * n + i];
     const int64_t r = i / n, c = i % n;
+    for (int64_t z = lane; z < splits; z += kWarp) s += __ldcg(ws + (z * m + r) * ldp + c);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane != 0) return;
     if (accumulate) s += dw[r * lddw + c];
     dw[r * lddw + c] = s;
     if (w) w[r * ldw + c] -= lr * s;
 }
 
 int64_t wgrad_splits(int64_t m, int64_t n, int64_t k) {
-    const int64_t tiles = ((m + kBM - 1) / kBM) * ((n + kBN - 1) / kBN);
-    int64_t splits = (296 + tiles - 1) / tiles;
-    const int64_t max_splits = (k + 511) / 512;
+    const int64_t bn = n >= 128 ? 128 : (n + 31) / 32 * 32;   // MN-major B tile width
+    const int64_t tiles = ((m + 127) / 128) * ((n + bn - 1) / bn);
+    // >= one wave of CTAs, and K chunks of <= 8192 rows so each fp32 TMEM
+    // accumulation stays short (partials are then reduced in a fixed tree)
+    int64_t splits = (148 + tiles - 1) / tiles;
+    const int64_t min_splits = (k + 8191) / 8192;
+    if (splits < min_splits) splits = min_splits;
+    const int64_t max_splits = (k + 1023) / 1024;
     if (splits > max_splits) splits = max_splits;
     if (splits < 1) splits = 1;
     return splits;
@@ -473,14 +339,25 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
     }
 }
 
-__global__ void xent_finalize_kernel(const double* partials, int nblocks, double count, double* stats) {
-    if (threadIdx.x != 0) return;
+// One block of 1024 threads: strided partial sums, then a fixed-order tree.
+__global__ void __launch_bounds__(1024) xent_finalize_kernel(const double* partials, int nblocks,
+                                                             double count, double* stats) {
+    __shared__ double sa[1024], sb[1024];
     double a = 0.0, b = 0.0;
-    for (int i = 0; i < nblocks; ++i) { a += partials[2 * i]; b += partials[2 * i + 1]; }
-    stats[0] = a / count;
-    stats[1] = b / count;
-    stats[2] = a;
-    stats[3] = b;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) { a += partials[2 * i]; b += partials[2 * i + 1]; }
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) { sa[threadIdx.x] += sa[threadIdx.x + w]; sb[threadIdx.x] += sb[threadIdx.x + w]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        stats[0] = sa[0] / count;
+        stats[1] = sb[0] / count;
+        stats[2] = sa[0];
+        stats[3] = sb[0];
+    }
 }
 
 // ------------------------------------------------------------ helpers --
@@ -607,12 +484,12 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
         return fail(kErrArg, "agg_sum: incomplete heavy-row split");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int w4 = (a.width + 3) / 4;
-    if (w4 <= 1) return launch_agg<1, 1, 8>(a, st);
-    if (w4 <= 2) return launch_agg<2, 1, 8>(a, st);
-    if (w4 <= 4) return launch_agg<4, 1, 8>(a, st);
-    if (w4 <= 8) return launch_agg<8, 1, 8>(a, st);
-    if (w4 <= 16) return launch_agg<16, 1, 8>(a, st);
-    if (w4 <= 32) return launch_agg<32, 1, 8>(a, st);
+    if (w4 <= 1) return launch_agg<1, 1, 4>(a, st);
+    if (w4 <= 2) return launch_agg<2, 1, 4>(a, st);
+    if (w4 <= 4) return launch_agg<4, 1, 4>(a, st);
+    if (w4 <= 8) return launch_agg<8, 1, 4>(a, st);
+    if (w4 <= 16) return launch_agg<16, 1, 4>(a, st);
+    if (w4 <= 32) return launch_agg<32, 1, 4>(a, st);
     if (w4 <= 64) return launch_agg<32, 2, 4>(a, st);
     if (w4 <= 128) return launch_agg<32, 4, 2>(a, st);
     return launch_agg<32, 8, 1>(a, st);
@@ -625,13 +502,36 @@ extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
     if (g.m < 0 || g.n < 0 || g.k < 0 || !g.a || !g.b || !g.c)
         return fail(kErrArg, "gemm: bad arguments");
     if (g.m == 0 || g.n == 0) return 0;
-    dim3 grid(static_cast<unsigned>((g.m + kBM - 1) / kBM), static_cast<unsigned>((g.n + kBN - 1) / kBN));
-    gemm_kernel<<<grid, kGemmThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
-    return launch_status("gemm");
+    GrdTcGemm t{};
+    t.m = g.m; t.n = g.n; t.k = g.k;
+    t.a = g.a; t.lda = g.lda; t.trans_a = g.trans_a;
+    t.b = g.b; t.ldb = g.ldb; t.trans_b = g.trans_b;
+    t.c = g.c; t.ldc = g.ldc;
+    t.row_scale = g.row_scale;
+    t.elem_mul = g.elem_mul; t.ld_elem_mul = g.ld_elem_mul;
+    t.relu_ref = g.relu_ref; t.ld_relu_ref = g.ld_relu_ref;
+    t.relu_out = g.relu_out; t.accumulate = g.accumulate;
+    t.k_splits = 1;
+    if (g.lda % 4 || g.ldb % 4 || g.ldc % 4 || (reinterpret_cast<uintptr_t>(g.a) & 15) ||
+        (reinterpret_cast<uintptr_t>(g.c) & 15))
+        return fail(kErrArg, "gemm: leading dims must be multiples of 4 and rows 16-byte aligned");
+    const int64_t need = grd_tc_pack_elems(g.n, g.k);
+    if (!g.workspace || g.workspace_elems < need)
+        return fail(kErrArg, "gemm: workspace needs %lld floats", (long long)need);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = grd_tc_pack_b(g.b, g.ldb, g.trans_b, g.n, g.k, g.workspace, st);
+    if (e == cudaSuccess) {
+        t.b_packed = g.workspace;
+        e = grd_tc_gemm(t, st);
+    }
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "gemm: %s", cudaGetErrorString(e));
+    return 0;
 }
 
+extern "C" int64_t grd_gemm_workspace(int64_t n, int64_t k) { return grd_tc_pack_elems(n, k); }
+
 extern "C" int64_t grd_wgrad_workspace(int64_t m, int64_t n, int64_t k) {
-    return wgrad_splits(m, n, k) * m * n;
+    return wgrad_splits(m, n, k) * m * ((n + 3) / 4 * 4);
 }
 
 extern "C" int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, const float* b,
@@ -641,17 +541,30 @@ extern "C" int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a, in
     if (m <= 0 || n <= 0 || k < 0 || !a || !b || !dw || !workspace)
         return fail(kErrArg, "wgrad: bad arguments");
     const int64_t splits = wgrad_splits(m, n, k);
-    if (workspace_elems < splits * m * n) return fail(kErrArg, "wgrad: workspace too small");
+    if (workspace_elems < splits * m * ((n + 3) / 4 * 4)) return fail(kErrArg, "wgrad: workspace too small");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int64_t kchunk = (k + splits - 1) / splits;
-    kchunk = (kchunk + kBK - 1) / kBK * kBK;
-    dim3 grid(static_cast<unsigned>((m + kBM - 1) / kBM), static_cast<unsigned>((n + kBN - 1) / kBN),
-              static_cast<unsigned>(splits));
-    wgrad_partial_kernel<<<grid, kGemmThreads, 0, st>>>(m, n, k, kchunk, a, lda, b, ldb, workspace);
-    int rc = launch_status("wgrad_partial");
-    if (rc) return rc;
-    wgrad_reduce_kernel<<<blocks_for(m * n), 256, 0, st>>>(m, n, splits, workspace, dw, lddw, accumulate, w,
-                                                          ldw, lr);
+    if (lda % 4 || ldb % 4 || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+        return fail(kErrArg, "wgrad: leading dims must be multiples of 4 and rows 16-byte aligned");
+    const int64_t ldp = (n + 3) / 4 * 4;
+    int64_t used = 1;
+    if (k == 0) {
+        cudaMemsetAsync(workspace, 0, sizeof(float) * m * ldp, st);
+    } else {
+        int64_t kchunk = (k + splits - 1) / splits;
+        kchunk = (kchunk + 31) / 32 * 32;
+        used = (k + kchunk - 1) / kchunk;
+        GrdTcGemm t{};
+        t.m = m; t.n = n; t.k = k;
+        t.a = a; t.lda = lda; t.trans_a = 1;      // A^T: a stored K x M
+        t.b = b; t.ldb = ldb; t.trans_b = 0;      // b stored K x N
+        t.k_splits = static_cast<int>(used);
+        t.k_chunk = kchunk;
+        t.partial = workspace;
+        const cudaError_t e = grd_tc_gemm(t, st);
+        if (e != cudaSuccess) return fail(static_cast<int>(e), "wgrad: %s", cudaGetErrorString(e));
+    }
+    wgrad_reduce_kernel<<<blocks_for(m * n * kWarp), 256, 0, st>>>(m, n, used, ldp, workspace, dw, lddw,
+                                                                    accumulate, w, ldw, lr);
     return launch_status("wgrad_reduce");
 }
 
@@ -674,7 +587,7 @@ extern "C" int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t 
                                              ld_grad, grad_scale, partials);
     int rc = launch_status("softmax_xent");
     if (rc) return rc;
-    xent_finalize_kernel<<<1, 32, 0, st>>>(partials, kLossBlocks, static_cast<double>(mask_count), stats_out);
+    xent_finalize_kernel<<<1, 1024, 0, st>>>(partials, kLossBlocks, static_cast<double>(mask_count), stats_out);
     return launch_status("softmax_xent_finalize");
 }
 

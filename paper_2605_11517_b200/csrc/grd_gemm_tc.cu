@@ -1,0 +1,586 @@
+// Dense fp32 GEMM on the 5th-generation tensor cores (tcgen05, sm_100a) with
+// the 3xTF32 split, for the GNN dense transforms (training.py:76,128-129):
+//   C = epi(opA(A) opB(B)) at fp32-grade accuracy.
+//
+// 3xTF32:  A = Ah + Al, B = Bh + Bl, Ah = A & 0xffffe000 (exact TF32),
+//          Al = A - Ah;  C ~= Al*Bh + Ah*Bl + Ah*Bh  (kind::tf32 MMAs,
+//          fp32 accumulation in TMEM; the dropped Al*Bl is ~2^-22 relative).
+//
+// Warp-specialised persistent kernel (10 warps):
+//   warp 0     producer: TMA tensor copies of raw A (and, for the weight
+//              gradient, raw B) into a ring of shared-memory stages; the
+//              weight operand of forward/dgrad GEMMs is pre-split into hi/lo
+//              K-major tiles by a small pack kernel and arrives by one 1-D
+//              bulk copy per stage;
+//   warp 1     MMA issuer: one elected thread, 12 tcgen05.mma per 32-deep K
+//              block, tcgen05.commit releases the stage / publishes a tile;
+//   warps 2-5  converters: split each raw stage into hi (in place) and lo;
+//   warps 6-9  epilogue: tcgen05.ld of the double-buffered TMEM accumulator,
+//              fused row-scale / element-multiply / ReLU-mask / ReLU /
+//              accumulate, 128-byte row stores (or split-K partial tiles).
+// Shared-memory tiles use the canonical SWIZZLE_128B layouts: K-major for
+// row-major activations (TMA box 32 K x 128 rows), MN-major for the
+// weight-gradient operands whose rows run along K (TMA boxes 32 x 32).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+
+#include "grd_gemm_tc.h"
+
+namespace grd_tc {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;
+constexpr int kWarps = 14;
+constexpr int kThreads = kWarps * 32;
+constexpr int kConvWarp0 = 2;
+constexpr int kConvThreads = 256;
+constexpr int kEpiWarp0 = 10;
+
+enum OpMode : int {
+    kKMajorTma = 0,     // raw, K-contiguous rows, one TMA box (32 x rows)
+    kMNMajorTma = 1,    // raw, rows contiguous along MN: TMA boxes (32 MN x 32 K) into a
+                        // staging area, transposed to K-major by the converters
+    kPacked = 2,        // pre-split hi/lo K-major tiles, one bulk copy
+};
+
+struct Params {
+    int64_t m, n, k;
+    int bn;
+    int a_mode, b_mode;
+    const float* b_packed;          // kPacked: [ntile][kblock][hi|lo][bn x 32]
+    int64_t kchunk;                 // split-K chunk (multiple of 32)
+    int splits;
+    int stages;
+    float* c; int64_t ldc;
+    const float* row_scale;
+    const float* elem_mul; int64_t ld_elem_mul;
+    const float* relu_ref; int64_t ld_relu_ref;
+    int relu_out;
+    int accumulate;
+    float* partial; int64_t ld_partial;   // split-K: [z][m][ld_partial]
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, version 1.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1u) << 46;
+    d |= static_cast<uint64_t>(2u) << 61;
+    return d;
+}
+
+// kind::tf32, D fp32, M = 128, N = bn; a/b major: 0 = K, 1 = MN.
+__device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+           (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(bn >> 3) << 17) |
+           (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                       uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float4 hi4(float4 v) {
+    v.x = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+    v.y = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+    v.z = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+    v.w = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+    return v;
+}
+
+// Split a raw tile in place: hi over raw, lo into `lo` (same swizzled layout).
+__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t bytes, int ctid, int nthr) {
+    float4* r4 = reinterpret_cast<float4*>(raw);
+    float4* l4 = reinterpret_cast<float4*>(lo);
+    for (uint32_t i = ctid; i < bytes / 16; i += nthr) {
+        const float4 v = r4[i];
+        const float4 h = hi4(v);
+        r4[i] = h;
+        l4[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    }
+}
+
+// Transpose-and-split an MN-major raw tile (R/32 TMA atoms of 32 MN x 32 K,
+// element (mn, k) of atom j at j*4096 + k*128 + swizzled chunk) into K-major
+// hi/lo tiles.  Lane l of a warp handles (mn & 7, k & 3) = (l & 7, l >> 3):
+// conflict-free stores, 2-way-conflicted loads.
+__device__ __forceinline__ void transpose_split(const uint8_t* raw, uint8_t* hi, uint8_t* lo, int rows,
+                                                int ctid, int nthr) {
+    const int total = rows * 32;
+    for (int i = ctid; i < total; i += nthr) {
+        const int atom = i >> 10, within = i & 1023;
+        const int w = within >> 5, l = within & 31;
+        const int k = (w & 7) * 4 + (l >> 3);
+        const int mn = (w >> 3) * 8 + (l & 7);
+        const float v = *reinterpret_cast<const float*>(
+            raw + atom * 4096 + k * 128 + ((((mn >> 2) ^ (k & 7)) & 7) << 4) + (mn & 3) * 4);
+        const int row = atom * 32 + mn;
+        const uint32_t off = static_cast<uint32_t>(row) * 128u + ((static_cast<uint32_t>((k >> 2) ^ (row & 7))) << 4) +
+                             static_cast<uint32_t>(k & 3) * 4u;
+        const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        *reinterpret_cast<float*>(hi + off) = h;
+        *reinterpret_cast<float*>(lo + off) = v - h;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int bn = p.bn;
+    const int S = p.stages;
+    const uint32_t a_bytes = kBM * 128u;
+    const uint32_t b_bytes = static_cast<uint32_t>(bn) * 128u;
+    // stage: A hi | A lo | B hi | B lo | [A raw] | [B raw]  (raw only for MN-major)
+    const uint32_t a_raw_off = 2u * (a_bytes + b_bytes);
+    const uint32_t b_raw_off = a_raw_off + (p.a_mode == kMNMajorTma ? a_bytes : 0u);
+    const uint32_t stage_bytes = b_raw_off + (p.b_mode == kMNMajorTma ? b_bytes : 0u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+    uint64_t* full = bars;             // [S]
+    uint64_t* conv = bars + S;         // [S]
+    uint64_t* empty = bars + 2 * S;    // [S]
+    uint64_t* tfull = bars + 3 * S;    // [2]
+    uint64_t* tempty = bars + 3 * S + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t mt = (p.m + kBM - 1) / kBM;
+    const int64_t nt = (p.n + bn - 1) / bn;
+    const int64_t ntiles = mt * nt * p.splits;
+    const int64_t nkb_full = (p.kchunk + kBK - 1) / kBK;
+    uint32_t tmem_cols = 32;
+    while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(conv + s, kConvThreads);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+        if (p.b_mode != kPacked) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    auto kblocks_of = [&](int z) -> int64_t {
+        const int64_t k0 = int64_t(z) * p.kchunk;
+        const int64_t k1 = min(k0 + p.kchunk, p.k);
+        return k1 > k0 ? (k1 - k0 + kBK - 1) / kBK : 0;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer --
+        if (lane == 0) {
+            uint64_t g = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int z = static_cast<int>(t / (mt * nt));
+                const int64_t r = t % (mt * nt);
+                const int64_t m0 = (r / nt) * kBM, ntile = r % nt, n0 = ntile * bn;
+                const int64_t nkb = kblocks_of(z);
+                for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = static_cast<int>(g % S);
+                    if (g >= static_cast<uint64_t>(S)) mbar_wait(empty + s, static_cast<uint32_t>((g / S - 1) & 1));
+                    uint8_t* st = smem + s * stage_bytes;
+                    const int64_t k0 = int64_t(z) * p.kchunk + kb * kBK;
+                    uint32_t bytes = a_bytes;
+                    bytes += (p.b_mode == kPacked) ? 2u * b_bytes : b_bytes;
+                    mbar_expect_tx(full + s, bytes);
+                    if (p.a_mode == kKMajorTma) {
+                        tma_2d(st, &map_a, static_cast<int32_t>(k0), static_cast<int32_t>(m0), full + s);
+                    } else {
+                        for (int j = 0; j < kBM / 32; ++j)
+                            tma_2d(st + a_raw_off + j * 4096, &map_a, static_cast<int32_t>(m0 + 32 * j),
+                                   static_cast<int32_t>(k0), full + s);
+                    }
+                    uint8_t* bdst = st + 2 * a_bytes;
+                    if (p.b_mode == kPacked) {
+                        const int64_t kbg = (k0 / kBK);
+                        const int64_t nkb_all = (p.k + kBK - 1) / kBK;
+                        const float* src = p.b_packed + (ntile * nkb_all + kbg) * (2 * int64_t(bn) * kBK);
+                        bulk_copy(bdst, src, 2u * b_bytes, full + s);
+                    } else if (p.b_mode == kKMajorTma) {
+                        tma_2d(bdst, &map_b, static_cast<int32_t>(k0), static_cast<int32_t>(n0), full + s);
+                    } else {
+                        for (int j = 0; j < bn / 32; ++j)
+                            tma_2d(st + b_raw_off + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
+                                   static_cast<int32_t>(k0), full + s);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA issuer --
+        if (lane == 0) {
+            // every operand reaches the tensor core K-major (MN-major inputs are
+            // transposed by the converters): advance 32 B per 8-deep MMA
+            const uint32_t idesc = make_idesc(bn, 0, 0);
+            const uint32_t a_step = 32u, b_step = 32u;
+            const uint32_t a_lbo = 16u, b_lbo = 16u, a_sbo = 1024u, b_sbo = 1024u;
+            uint64_t g = 0;
+            int64_t i = 0;   // tiles with K work (empty split-K tiles are skipped)
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int z = static_cast<int>(t / (mt * nt));
+                const int64_t nkb = kblocks_of(z);
+                if (nkb == 0) continue;
+                const int acc = static_cast<int>(i & 1);
+                if (i >= 2) mbar_wait(tempty + acc, static_cast<uint32_t>((i / 2 - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t tacc = tmem + static_cast<uint32_t>(acc * bn);
+                for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = static_cast<int>(g % S);
+                    mbar_wait(conv + s, static_cast<uint32_t>((g / S) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    uint8_t* st = smem + s * stage_bytes;
+                    const uint32_t ah = smem_u32(st), al = smem_u32(st + a_bytes);
+                    const uint32_t bh = smem_u32(st + 2 * a_bytes), bl = smem_u32(st + 2 * a_bytes + b_bytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 8; ++kk) {
+                        const uint64_t dah = make_desc(ah + kk * a_step, a_lbo, a_sbo);
+                        const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo);
+                        const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo);
+                        const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo);
+                        mma_tf32(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                        mma_tf32(tacc, dah, dbl, idesc, 1u);
+                        mma_tf32(tacc, dah, dbh, idesc, 1u);
+                    }
+                    mma_commit(empty + s);
+                }
+                mma_commit(tfull + acc);
+                ++i;
+            }
+        }
+    } else if (warp < kEpiWarp0) {
+        // -------------------------------------------------- converters --
+        const int ctid = threadIdx.x - kConvWarp0 * 32;
+        uint64_t g = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int z = static_cast<int>(t / (mt * nt));
+            const int64_t nkb = kblocks_of(z);
+            for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+                const int s = static_cast<int>(g % S);
+                mbar_wait(full + s, static_cast<uint32_t>((g / S) & 1));
+                uint8_t* st = smem + s * stage_bytes;
+                if (p.a_mode == kKMajorTma) split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads);
+                else transpose_split(st + a_raw_off, st, st + a_bytes, kBM, ctid, kConvThreads);
+                uint8_t* bh = st + 2 * a_bytes;
+                if (p.b_mode == kKMajorTma) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads);
+                else if (p.b_mode == kMNMajorTma) transpose_split(st + b_raw_off, bh, bh + b_bytes, bn, ctid, kConvThreads);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(conv + s);
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue --
+        const int q = warp & 3;                       // TMEM lane quarter
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int64_t i = 0;   // same work counter as the MMA issuer
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int z = static_cast<int>(t / (mt * nt));
+            const int64_t r = t % (mt * nt);
+            const int64_t m0 = (r / nt) * kBM, n0 = (r % nt) * bn;
+            const int acc = static_cast<int>(i & 1);
+            const bool has_k = kblocks_of(z) > 0;
+            if (has_k) {
+                mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+            const int64_t row = m0 + q * 32 + lane;
+            const bool row_ok = row < p.m;
+            const float rs = (row_ok && p.row_scale) ? p.row_scale[row] : 1.0f;
+            const int64_t n_pad = (p.n + 3) / 4 * 4;
+            for (int c0 = 0; c0 < bn; c0 += 32) {
+                float v[32];
+                if (has_k) {
+                    tmem_ld32(tmem + lane_base + static_cast<uint32_t>(acc * bn + c0), v);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                }
+                if (!row_ok || n0 + c0 >= n_pad) continue;
+                if (p.partial) {
+                    float* out = p.partial + (int64_t(z) * p.m + row) * p.ld_partial + n0 + c0;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        if (n0 + c0 + j < n_pad) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    continue;
+                }
+                float* crow = p.c + row * p.ldc + n0 + c0;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    const int64_t n = n0 + c0 + j;
+                    if (n >= n_pad) continue;
+                    float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    if (p.row_scale) { x.x *= rs; x.y *= rs; x.z *= rs; x.w *= rs; }
+                    if (p.elem_mul) {
+                        const float4 e = *reinterpret_cast<const float4*>(p.elem_mul + row * p.ld_elem_mul + n);
+                        x.x *= e.x; x.y *= e.y; x.z *= e.z; x.w *= e.w;
+                    }
+                    if (p.relu_ref) {
+                        const float4 e = *reinterpret_cast<const float4*>(p.relu_ref + row * p.ld_relu_ref + n);
+                        if (!(e.x > 0.f)) x.x = 0.f;
+                        if (!(e.y > 0.f)) x.y = 0.f;
+                        if (!(e.z > 0.f)) x.z = 0.f;
+                        if (!(e.w > 0.f)) x.w = 0.f;
+                    }
+                    if (p.relu_out) {
+                        x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+                    }
+                    if (p.accumulate) {
+                        const float4 o = *reinterpret_cast<const float4*>(crow + j);
+                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                    }
+                    *reinterpret_cast<float4*>(crow + j) = x;
+                }
+            }
+            if (has_k) {
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                mbar_arrive(tempty + acc);
+                ++i;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+    }
+}
+
+// Pack the (small) weight operand into pre-split K-major SW128 tiles:
+// out[ntile][kblock][hi|lo][bn rows x 32 K]; element (n, k) of opB.
+__global__ void pack_b_kernel(const float* __restrict__ b, int64_t ldb, int trans_b, int64_t n, int64_t k, int bn,
+                              float* __restrict__ out) {
+    const int64_t nkb = (k + kBK - 1) / kBK;
+    const int64_t ntile = (n + bn - 1) / bn;
+    const int64_t total = ntile * nkb * int64_t(bn) * kBK;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int kk = static_cast<int>(i % kBK);
+        const int64_t rest = i / kBK;
+        const int rr = static_cast<int>(rest % bn);
+        const int64_t tile = rest / bn;            // ntile * nkb + kb
+        const int64_t kb = tile % nkb, nti = tile / nkb;
+        const int64_t gn = nti * bn + rr, gk = kb * kBK + kk;
+        float v = 0.f;
+        if (gn < n && gk < k) v = trans_b ? b[gn * ldb + gk] : b[gk * ldb + gn];
+        const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        const uint32_t off = static_cast<uint32_t>(rr) * 128u +
+                             ((static_cast<uint32_t>(kk >> 2) ^ (rr & 7)) << 4) + (static_cast<uint32_t>(kk & 3) << 2);
+        float* base = out + tile * (2 * int64_t(bn) * kBK);
+        base[off / 4] = h;
+        base[int64_t(bn) * kBK + off / 4] = v - h;
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    });
+    return fn;
+}
+
+// 2-D fp32 tensor map over a row-major matrix [rows][cols] (leading dim ld),
+// box = box_cols (inner) x box_rows, SWIZZLE_128B, zero OOB fill.
+bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
+              uint32_t box_rows) {
+    EncodeFn fn = encoder();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int pick_bn(int64_t n) {
+    if (n > 128) return n >= 256 ? 256 : static_cast<int>((n + 31) / 32 * 32);
+    int bn = static_cast<int>((n + 15) / 16 * 16);
+    return bn < 16 ? 16 : bn;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace grd_tc
+
+using namespace grd_tc;
+
+int64_t grd_tc_pack_elems(int64_t n, int64_t k) {
+    const int bn = pick_bn(n);
+    return ((n + bn - 1) / bn) * ((k + kBK - 1) / kBK) * 2 * int64_t(bn) * kBK;
+}
+
+int grd_tc_bn(int64_t n) { return pick_bn(n); }
+
+cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
+    Params p{};
+    p.m = g.m;
+    p.n = g.n;
+    p.k = g.k;
+    p.bn = pick_bn(g.n);
+    p.splits = g.k_splits > 1 ? g.k_splits : 1;
+    p.kchunk = p.splits > 1 ? g.k_chunk : (g.k > 0 ? (g.k + kBK - 1) / kBK * kBK : kBK);
+    p.c = g.c;
+    p.ldc = g.ldc;
+    p.row_scale = g.row_scale;
+    p.elem_mul = g.elem_mul;
+    p.ld_elem_mul = g.ld_elem_mul;
+    p.relu_ref = g.relu_ref;
+    p.ld_relu_ref = g.ld_relu_ref;
+    p.relu_out = g.relu_out;
+    p.accumulate = g.accumulate;
+    p.partial = g.partial;
+    p.ld_partial = (g.n + 3) / 4 * 4;
+    CUtensorMap map_a{}, map_b{};
+    // A(m, k): K-major TMA when stored M x K, MN-major boxes when stored K x M.
+    if (!g.trans_a) {
+        p.a_mode = kKMajorTma;
+        if (!make_map(&map_a, g.a, g.m, g.k, g.lda, 32, 128)) return cudaErrorInvalidValue;
+    } else {
+        p.a_mode = kMNMajorTma;
+        if (!make_map(&map_a, g.a, g.k, g.m, g.lda, 32, 32)) return cudaErrorInvalidValue;
+    }
+    if (g.b_packed) {
+        p.b_mode = kPacked;
+        p.b_packed = g.b_packed;
+        map_b = map_a;
+    } else if (g.trans_b) {
+        p.b_mode = kKMajorTma;   // B stored N x K
+        if (!make_map(&map_b, g.b, g.n, g.k, g.ldb, 32, static_cast<uint32_t>(p.bn))) return cudaErrorInvalidValue;
+    } else {
+        p.b_mode = kMNMajorTma;  // B stored K x N
+        if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32)) return cudaErrorInvalidValue;
+    }
+    if (p.b_mode == kMNMajorTma) {    // raw staging: keep two stages in shared memory
+        p.bn = p.bn > 128 ? 128 : (p.bn + 31) / 32 * 32;
+        if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32)) return cudaErrorInvalidValue;
+    }
+    uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.bn) * 128u);
+    if (p.a_mode == kMNMajorTma) stage += kBM * 128u;
+    if (p.b_mode == kMNMajorTma) stage += static_cast<uint32_t>(p.bn) * 128u;
+    p.stages = static_cast<int>((220u * 1024u) / stage);
+    if (p.stages > 4) p.stages = 4;
+    if (p.stages < 2) p.stages = 2;
+    const size_t smem = static_cast<size_t>(p.stages) * stage + 1024 + 256;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t tiles = ((g.m + kBM - 1) / kBM) * ((g.n + p.bn - 1) / p.bn) * p.splits;
+    const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+    gemm_tf32x3_ws<<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+    return cudaGetLastError();
+}
+
+cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,
+                          cudaStream_t st) {
+    const int bn = pick_bn(n);
+    const int64_t total = grd_tc_pack_elems(n, k) / 2;
+    const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    pack_b_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(b, ldb, trans_b, n, k, bn, out);
+    return cudaGetLastError();
+}

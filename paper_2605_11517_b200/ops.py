@@ -24,6 +24,37 @@ HEAVY_THRESHOLD = 128   # rows above this degree are split ...
 SEGMENT_EDGES = 128     # ... into segments of this many edges
 
 
+class Recorder:
+    """Launch accounting for the benchmark: counts this library's kernel
+    launches and, when ``timing`` is on, brackets each op with CUDA events on
+    the launching stream together with its algorithmic bytes / flops."""
+
+    def __init__(self):
+        self.launches = 0
+        self.timing = False
+        self.records: list = []
+
+    def reset(self) -> None:
+        self.launches = 0
+        self.records = []
+
+
+RECORDER = Recorder()
+
+
+def _launch(name: str, nlaunch: int, nbytes: float, flops: float, fn) -> None:
+    RECORDER.launches += nlaunch
+    if not RECORDER.timing:
+        fn()
+        return
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    fn()
+    end.record()
+    RECORDER.records.append((name, float(nbytes), float(flops), start, end))
+
+
 def ld_of(width: int) -> int:
     return (int(width) + 3) // 4 * 4
 
@@ -131,7 +162,13 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
     a.heavy_counter = _p(spec.heavy_counter)
     a.mask_ref = _p(mask_ref)
     a.ld_mask_ref = _ld(mask_ref) if mask_ref is not None else 0
-    _lib.check(_lib.lib().grd_agg_sum(ctypes.byref(a), stream_ptr()), "agg_sum")
+    R, E, w = spec.n_rows, spec.nnz, int(width)
+    nbytes = 8 * (R + 1) + 4 * E + 4 * w * (E + R) + 4 * w * R
+    nbytes += 4 * R * ((spec.out_idx is not None) + (spec.self_idx is not None)
+                       + (post_scale is not None))
+    nbytes += 4 * (E + R) * (src_scale is not None) + 4 * w * R * (mask_ref is not None)
+    _launch("agg_sum", 1, nbytes, 2.0 * w * (E + R),
+            lambda: _lib.check(_lib.lib().grd_agg_sum(ctypes.byref(a), stream_ptr()), "agg_sum"))
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
@@ -150,18 +187,30 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: i
     g.ld_relu_ref = _ld(relu_ref) if relu_ref is not None else 0
     g.relu_out = int(bool(relu_out))
     g.accumulate = int(bool(accumulate))
-    _lib.check(_lib.lib().grd_gemm(ctypes.byref(g), stream_ptr()), "gemm")
+    m, n, k = int(m), int(n), int(k)
+    need = int(_lib.lib().grd_gemm_workspace(n, k))
+    ws = _workspace(("pack", c.device), need)
+    g.workspace = _p(ws)
+    g.workspace_elems = ws.numel()
+    nbytes = 4 * (m * k + k * n + m * n) + 4 * m * (row_scale is not None)
+    nbytes += 4 * m * n * ((elem_mul is not None) + (relu_ref is not None) + bool(accumulate))
+    _launch("gemm", 2, nbytes, 2.0 * m * n * k,
+            lambda: _lib.check(_lib.lib().grd_gemm(ctypes.byref(g), stream_ptr()), "gemm"))
 
 
 _WS: dict = {}
 
 
-def _workspace(device, elems: int) -> torch.Tensor:
-    key = str(device)
-    ws = _WS.get(key)
+def _workspace(key, elems: int) -> torch.Tensor:
+    """Scratch buffers of the library (grown on demand, reused; allocated
+    before CUDA-graph capture by the engine's warm-up epoch)."""
+    if not isinstance(key, tuple):
+        key = ("wgrad", key)
+    device = key[1]
+    ws = _WS.get((key[0], str(device)))
     if ws is None or ws.numel() < elems:
         ws = torch.empty(max(elems, 1), dtype=torch.float32, device=device)
-        _WS[key] = ws
+        _WS[(key[0], str(device))] = ws
     return ws
 
 
@@ -171,54 +220,67 @@ def wgrad_sgd(a: torch.Tensor, b: torch.Tensor, dw: torch.Tensor, m: int, n: int
     L = _lib.lib()
     need = int(L.grd_wgrad_workspace(m, n, k))
     ws = _workspace(dw.device, need)
-    _lib.check(L.grd_wgrad_sgd(int(m), int(n), int(k), _p(a), _ld(a), _p(b), _ld(b), _p(dw), _ld(dw),
-                               int(bool(accumulate)), _p(w), _ld(w) if w is not None else 0,
-                               float(lr), _p(ws), ws.numel(), stream_ptr()), "wgrad_sgd")
+    nbytes = 4 * (k * m + k * n + m * n) + 8 * m * n * (w is not None) + 4 * m * n * bool(accumulate)
+    _launch("wgrad_sgd", 2, nbytes, 2.0 * m * n * k, lambda: _lib.check(L.grd_wgrad_sgd(
+        int(m), int(n), int(k), _p(a), _ld(a), _p(b), _ld(b), _p(dw), _ld(dw),
+        int(bool(accumulate)), _p(w), _ld(w) if w is not None else 0, float(lr), _p(ws),
+        ws.numel(), stream_ptr()), "wgrad_sgd"))
 
 
 def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor, width: int) -> None:
-    _lib.check(_lib.lib().grd_gather_rows(_p(src), _ld(src), _p(idx), idx.numel(), int(width),
-                                          _p(dst), _ld(dst), stream_ptr()), "gather_rows")
+    n = idx.numel()
+    _launch("gather_rows", 1, 4 * n + 8 * n * int(width), 0, lambda: _lib.check(
+        _lib.lib().grd_gather_rows(_p(src), _ld(src), _p(idx), n, int(width), _p(dst), _ld(dst),
+                                   stream_ptr()), "gather_rows"))
 
 
 def scatter_add_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor, width: int) -> None:
-    _lib.check(_lib.lib().grd_scatter_add_rows(_p(src), _ld(src), _p(idx), idx.numel(), int(width),
-                                               _p(dst), _ld(dst), stream_ptr()), "scatter_add_rows")
+    n = idx.numel()
+    _launch("scatter_add_rows", 1, 4 * n + 12 * n * int(width), n * int(width), lambda: _lib.check(
+        _lib.lib().grd_scatter_add_rows(_p(src), _ld(src), _p(idx), n, int(width), _p(dst), _ld(dst),
+                                        stream_ptr()), "scatter_add_rows"))
 
 
 def mul_rows(x: torch.Tensor, m: torch.Tensor, y: torch.Tensor, n_rows: int, width: int) -> None:
-    _lib.check(_lib.lib().grd_mul_rows(_p(x), _ld(x), _p(m), _ld(m), int(n_rows), int(width), _p(y),
-                                       _ld(y), stream_ptr()), "mul_rows")
+    _launch("mul_rows", 1, 12 * int(n_rows) * int(width), int(n_rows) * int(width), lambda: _lib.check(
+        _lib.lib().grd_mul_rows(_p(x), _ld(x), _p(m), _ld(m), int(n_rows), int(width), _p(y), _ld(y),
+                                stream_ptr()), "mul_rows"))
 
 
 def mask_scale_rows(x: torch.Tensor, y: torch.Tensor, n_rows: int, width: int, *, ref=None,
                     row_scale=None) -> None:
-    _lib.check(_lib.lib().grd_mask_scale_rows(
-        _p(x), _ld(x), _p(ref), _ld(ref) if ref is not None else 0, _p(row_scale), int(n_rows),
-        int(width), _p(y), _ld(y), stream_ptr()), "mask_scale_rows")
+    _launch("mask_scale_rows", 1, 12 * int(n_rows) * int(width), int(n_rows) * int(width),
+            lambda: _lib.check(_lib.lib().grd_mask_scale_rows(
+                _p(x), _ld(x), _p(ref), _ld(ref) if ref is not None else 0, _p(row_scale),
+                int(n_rows), int(width), _p(y), _ld(y), stream_ptr()), "mask_scale_rows"))
 
 
 def rownorm_fwd(pre: torch.Tensor, out: torch.Tensor, n_rows: int, width: int, relu: bool,
                 out_idx=None) -> None:
-    _lib.check(_lib.lib().grd_rownorm_fwd(_p(pre), _ld(pre), int(n_rows), int(width), int(relu),
-                                          _p(out_idx), _p(out), _ld(out), stream_ptr()), "rownorm_fwd")
+    _launch("rownorm_fwd", 1, 8 * int(n_rows) * int(width), 3 * int(n_rows) * int(width),
+            lambda: _lib.check(_lib.lib().grd_rownorm_fwd(
+                _p(pre), _ld(pre), int(n_rows), int(width), int(relu), _p(out_idx), _p(out), _ld(out),
+                stream_ptr()), "rownorm_fwd"))
 
 
 def rownorm_bwd(pre: torch.Tensor, grad_y: torch.Tensor, grad_pre: torch.Tensor, n_rows: int,
                 width: int, *, a_out=None, row_scale=None) -> None:
-    _lib.check(_lib.lib().grd_rownorm_bwd(
-        _p(pre), _ld(pre), _p(grad_y), _ld(grad_y), _p(a_out), _ld(a_out) if a_out is not None else 0,
-        int(n_rows), int(width), _p(row_scale), _p(grad_pre), _ld(grad_pre), stream_ptr()),
-        "rownorm_bwd")
+    _launch("rownorm_bwd", 1, 16 * int(n_rows) * int(width), 8 * int(n_rows) * int(width),
+            lambda: _lib.check(_lib.lib().grd_rownorm_bwd(
+                _p(pre), _ld(pre), _p(grad_y), _ld(grad_y), _p(a_out),
+                _ld(a_out) if a_out is not None else 0, int(n_rows), int(width), _p(row_scale),
+                _p(grad_pre), _ld(grad_pre), stream_ptr()), "rownorm_bwd"))
 
 
 def softmax_xent(logits: torch.Tensor, n_rows: int, n_classes: int, labels: torch.Tensor,
                  mask: torch.Tensor, mask_count: int, grad: torch.Tensor, stats: torch.Tensor,
                  partials: torch.Tensor, grad_scale=None) -> None:
     """stats (float64 cuda[4]) <- {loss, accuracy, loss_sum, correct}."""
-    _lib.check(_lib.lib().grd_softmax_xent(
-        _p(logits), _ld(logits), int(n_rows), int(n_classes), _p(labels), _p(mask), int(mask_count),
-        _p(grad), _ld(grad), _p(grad_scale), _p(partials), _p(stats), stream_ptr()), "softmax_xent")
+    n, c = int(n_rows), int(n_classes)
+    nbytes = 8 * n * c + 9 * n + 4 * n * (grad_scale is not None)
+    _launch("softmax_xent", 2, nbytes, 6.0 * n * c, lambda: _lib.check(_lib.lib().grd_softmax_xent(
+        _p(logits), _ld(logits), n, c, _p(labels), _p(mask), int(mask_count), _p(grad), _ld(grad),
+        _p(grad_scale), _p(partials), _p(stats), stream_ptr()), "softmax_xent"))
 
 
 def loss_partials(n_rows: int, device) -> torch.Tensor:

@@ -42,6 +42,8 @@ __all__ = [
     "trace_to_csv",
     "write_trace_csv",
     "TrainSession",
+    "pinned_features",
+    "session_for",
 ]
 
 
@@ -133,7 +135,7 @@ class TrainSession:
     """
 
     def __init__(self, dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
-                 layerwise: bool = True, features: torch.Tensor | None = None):
+                 layerwise: bool = True):
         if plan.num_vertices != dataset.graph.num_vertices:
             raise ValueError("plan was built for a different graph")
         self.dev = _device()
@@ -145,26 +147,46 @@ class TrainSession:
         self.dg = dg
         self.model = copy_model(model)
         self.dataset = dataset
-        if features is None:
-            features = self.upload_features(dataset, self.dev)
+        features = ops.zeros_rows(dataset.graph.num_vertices, dataset.feature_dim, self.dev)
         cls = LayerwiseEngine if layerwise else PartitionEngine
         self.engine = cls(dg, self.model, features, dataset.labels, dataset.train_mask)
+        self.upload_features(dataset)
         self.layerwise = layerwise
         self._graph = None
         self._graph_lr = None
         self.stats_host = torch.zeros(4, dtype=torch.float64).pin_memory()
 
-    @staticmethod
-    def upload_features(dataset: LabeledDataset, dev) -> torch.Tensor:
-        f32 = dataset.features32()
-        n, f = f32.shape
-        t = ops.zeros_rows(n, f, dev)
-        src = torch.from_numpy(f32)
-        if t.shape[1] == f:
-            t.copy_(src, non_blocking=False)
+    def signature(self) -> tuple:
+        m = self.model
+        return (tuple(m.dims), m.aggregation_mode, m.row_normalize, m.dropout_rate,
+                m.dropout_seed, self.layerwise)
+
+    def upload_features(self, dataset: LabeledDataset) -> int:
+        """H2D of the features from pinned host memory; returns bytes moved."""
+        src = pinned_features(dataset)
+        dst = self.engine.acts[0]
+        f = src.shape[1]
+        if dst.shape[1] == f:
+            dst.copy_(src, non_blocking=True)
         else:
-            t[:, :f].copy_(src)
-        return t
+            dst[:, :f].copy_(src, non_blocking=True)
+        return src.numel() * 4
+
+    def reset(self, dataset: LabeledDataset, model: ModelState) -> int:
+        """Re-bind the session to (dataset, model): uploads features, labels,
+        mask and weights into the existing buffers (a captured CUDA graph
+        stays valid).  Returns the H2D bytes."""
+        eng = self.engine
+        moved = self.upload_features(dataset)
+        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)))
+        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)))
+        eng.mask_count = int(np.count_nonzero(dataset.train_mask))
+        self.model = copy_model(model)
+        eng.wts.load(self.model)
+        self.dataset = dataset
+        moved += eng.labels.numel() * 4 + eng.mask.numel()
+        moved += sum(w.size * 4 for w in self.model.weights)
+        return moved
 
     def _capture(self, lr: float) -> None:
         eng = self.engine
@@ -240,12 +262,46 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
         raise ValueError("plan was built for a different graph")
     observed = hierarchy is not None or use_snapshots or grad_probe is not None \
         or partition_order is not None
-    session = TrainSession(dataset, plan, model, layerwise=not observed)
+    session = session_for(dataset, plan, model, layerwise=not observed)
     trained, trace = session.train(epochs, lr, hierarchy=hierarchy, use_snapshots=use_snapshots,
                                    grad_probe=grad_probe, partition_order=partition_order)
     if epochs == 0:
         trained = copy_model(model)
     return trained, trace, getattr(hierarchy, "ledger", None)
+
+
+def pinned_features(dataset: LabeledDataset) -> torch.Tensor:
+    """Host fp32 features to upload.  fp32 features are used in place (a
+    page-locked array gives a true async H2D); f64 features are converted
+    on every call into a page-locked staging buffer kept on the dataset, so
+    in-place edits of ``dataset.features`` are always seen."""
+    feats = dataset.features
+    if feats.dtype == np.float32 and feats.flags.c_contiguous:
+        return torch.from_numpy(feats)
+    stage = getattr(dataset, "_pinned", None)
+    if stage is None or tuple(stage.shape) != tuple(feats.shape):
+        stage = torch.empty(feats.shape, dtype=torch.float32).pin_memory()
+        dataset._pinned = stage
+    np.copyto(stage.numpy(), feats, casting="same_kind")
+    return stage
+
+
+def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
+                layerwise: bool = True) -> TrainSession:
+    """A device session for (dataset, plan, model config), reused across
+    calls: the plan upload, buffers and the captured epoch graph persist on
+    the plan (``plan.device_cache``); inputs are re-uploaded every call."""
+    key = ("session", tuple(model.dims), model.aggregation_mode, model.row_normalize,
+           model.dropout_rate, model.dropout_seed, layerwise)
+    sess = plan.device_cache.get(key)
+    if sess is None:
+        sess = TrainSession(dataset, plan, model, layerwise=layerwise)
+        plan.device_cache[key] = sess
+    else:
+        if plan.num_vertices != dataset.graph.num_vertices:
+            raise ValueError("plan was built for a different graph")
+        sess.reset(dataset, model)
+    return sess
 
 
 def _whole_graph_plan(dataset: LabeledDataset) -> PartitionPlan:

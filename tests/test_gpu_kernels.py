@@ -101,7 +101,7 @@ def test_gemm_matches_numpy(ta, tb, m, n, k):
              relu_ref=_dev(rr))
     full = (a.T if ta else a) @ (b.T if tb else b)
     want = np.where(rr > 0, full * rs[:, None] * em, 0.0)
-    assert rel_l2(_host(c, n), want) < 1e-6
+    assert rel_l2(_host(c, n), want) < 5e-6   # 3xTF32 on tcgen05
 
 
 def test_gemm_relu_out_and_accumulate():
@@ -109,7 +109,7 @@ def test_gemm_relu_out_and_accumulate():
     a, b, c0 = rng.normal(size=(50, 12)), rng.normal(size=(12, 9)), rng.normal(size=(50, 9))
     c = _dev(c0)
     ops.gemm(_dev(a), _dev(b), c, 50, 9, 12, relu_out=True, accumulate=True)
-    assert rel_l2(_host(c, 9), c0 + np.maximum(a @ b, 0)) < 1e-6
+    assert rel_l2(_host(c, 9), c0 + np.maximum(a @ b, 0)) < 5e-6
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000)])
@@ -122,13 +122,15 @@ def test_wgrad_sgd(m, n, k):
     w = _dev(w0)
     ops.wgrad_sgd(_dev(a), _dev(b), dw, m, n, k, w=w, lr=0.25)
     want = a.astype(np.float64).T @ b.astype(np.float64)
-    assert rel_l2(_host(dw, n), want) < 1e-5
-    assert rel_l2(_host(w, n), w0 - 0.25 * want) < 1e-5
+    # fp32 accumulation of up to 8192 zero-mean products per split-K chunk
+    tol = 3e-5
+    assert rel_l2(_host(dw, n), want) < tol
+    assert rel_l2(_host(w, n), w0 - 0.25 * want) < tol
     dw2 = ops.zeros_rows(m, n, DEV)
     ops.wgrad_sgd(_dev(a), _dev(b), dw2, m, n, k)
     assert torch.equal(dw, dw2)
     ops.wgrad_sgd(_dev(a), _dev(b), dw2, m, n, k, accumulate=True)
-    assert rel_l2(_host(dw2, n), 2 * want) < 1e-5
+    assert rel_l2(_host(dw2, n), 2 * want) < tol
 
 
 @pytest.mark.parametrize("n,c", [(1000, 10), (777, 47), (300, 172), (64, 1)])
