@@ -142,7 +142,8 @@ typedef struct grd_agg_args {
     int64_t ldy;
     const float* src_scale;    /* nullable: per-Y-row multiplier           */
     const float* post_scale;   /* nullable: per-output-row multiplier      */
-    int32_t post_div_deg;      /* divide by (degree + 1)                   */
+    int32_t post_div_deg;      /* 1: divide by (degree + 1) (mean with self loop);
+                                  2: divide by degree (mean over neighbours; 0 if none) */
     int32_t relu;
     float* out;
     int64_t ldo;
@@ -154,11 +155,15 @@ typedef struct grd_agg_args {
     const int32_t* seg_heavy;      /* [n_segs] owning heavy index          */
     int64_t n_segs;
     int32_t seg_len;               /* edges per segment                    */
-    int32_t reserved;
+    int32_t no_self;               /* 1: no implicit self term             */
     float* seg_partial;            /* [n_segs * round_up(width,4)] scratch */
-    int32_t* heavy_counter;        /* [n_heavy] zero on entry, zero on exit */
+    int32_t* heavy_counter;        /* [16 * n_heavy] zero on entry, zero on exit
+                                      (one slot per heavy row and column chunk) */
     const float* mask_ref;         /* nullable: out = mask_ref[out_row,:] > 0 ? out : 0 */
     int64_t ld_mask_ref;
+    const float* add_y;            /* nullable: add_y[out_row,:] added after post-scaling,
+                                      before the activation (GraphSAGE root term) */
+    int64_t ld_add_y;
 } grd_agg_args;
 int grd_agg_sum(const grd_agg_args* args, void* stream);
 
@@ -169,8 +174,8 @@ int grd_agg_sum(const grd_agg_args* args, void* stream);
  * weight operand) is pre-split into `workspace`, which needs
  * grd_gemm_workspace(n, k) floats.  Leading dimensions must be multiples of
  * 4 and matrices 16-byte aligned (TMA).
- * epi: acc *= row_scale[m]; acc *= elem_mul[m,n]; acc = relu_ref[m,n]>0 ? acc : 0;
- * relu_out: max(acc,0); then C = acc (accumulate=0) or C += acc.  Epilogue
+ * epi: v = acc (+ C if accumulate); v *= row_scale[m]; v *= elem_mul[m,n];
+ * v = relu_ref[m,n]>0 ? v : 0; relu_out: max(v,0); C = v.  Epilogue
  * pointers are nullable; columns up to round_up(n,4) are written. */
 typedef struct grd_gemm_args {
     int64_t m, n, k;

@@ -57,11 +57,13 @@ class GrdAggArgs(ctypes.Structure):
         ("seg_heavy", c_vp),
         ("n_segs", c_i64),
         ("seg_len", c_i32),
-        ("reserved", c_i32),
+        ("no_self", c_i32),
         ("seg_partial", c_vp),
         ("heavy_counter", c_vp),
         ("mask_ref", c_vp),
         ("ld_mask_ref", c_i64),
+        ("add_y", c_vp),
+        ("ld_add_y", c_i64),
     ]
 
 

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/grinder_b200.h"
 #include "grd_common.h"
@@ -24,6 +25,7 @@ using namespace grd;
 namespace {
 
 constexpr int kWarp = 32;
+constexpr int kMaxAggChunks = 16;   // heavy_counter holds n_heavy x 16 slots
 
 inline int launch_status(const char* what) {
     const cudaError_t err = cudaGetLastError();
@@ -110,7 +112,7 @@ template <int LPR, int NV>
 __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg, int sub,
                                            int w4, float4 (&acc)[NV]) {
     const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
-    const int32_t srow = a.self_idx ? a.self_idx[r] : orow;
+    const int32_t srow = a.no_self ? -1 : (a.self_idx ? a.self_idx[r] : orow);
     if (srow >= 0) {
         const float s = a.src_scale ? a.src_scale[srow] : 1.0f;
         float4 v[NV];
@@ -118,7 +120,8 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
 #pragma unroll
         for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s, v[c], acc[c]);
     }
-    const float div = static_cast<float>(deg + 1);
+    const float div = static_cast<float>(a.post_div_deg == 2 ? deg : deg + 1);
+    const bool do_div = a.post_div_deg == 1 || (a.post_div_deg == 2 && deg > 0);
     const float ps = a.post_scale ? a.post_scale[orow] : 1.0f;
     float* out = a.out + int64_t(orow) * a.ldo;
 #pragma unroll
@@ -126,8 +129,9 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
         const int q = sub + c * LPR;
         if (q >= w4) continue;
         float4 v = acc[c];
-        if (a.post_div_deg) { v.x /= div; v.y /= div; v.z /= div; v.w /= div; }
+        if (do_div) { v.x /= div; v.y /= div; v.z /= div; v.w /= div; }
         if (a.post_scale) { v.x *= ps; v.y *= ps; v.z *= ps; v.w *= ps; }
+        if (a.add_y) v = f4_add(v, ld_nc_f4(a.add_y + int64_t(orow) * a.ld_add_y + 4 * q));
         if (a.relu) {
             v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f);
             v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
@@ -143,9 +147,24 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
     }
 }
 
+// Column chunking: blockIdx.y selects a chunk of `chunk_cols` columns.  Blocks
+// run chunk-major, so at any time the SMs gather one column slice of the rows
+// of the partitions currently in flight, which keeps that slice of the
+// gathered set L2-resident (the partition order of the rows is the locality).
 template <int LPR, int NV, int U>
-__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a, int64_t light_warps) {
+__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, int64_t light_warps,
+                                                      int chunk_cols) {
     constexpr int NG = kWarp / LPR;
+    grd_agg_args a = a_in;
+    const int col0 = static_cast<int>(blockIdx.y) * chunk_cols;
+    const int ldp = 4 * ((a_in.width + 3) / 4);   // partial row stride (full width)
+    a.width = min(chunk_cols, a_in.width - col0);
+    a.y += col0;
+    a.out += col0;
+    if (a.add_y) a.add_y += col0;
+    if (a.mask_ref) a.mask_ref += col0;
+    if (a.seg_partial) a.seg_partial += col0;
+    if (a.heavy_counter) a.heavy_counter += blockIdx.y * a.n_heavy;
     const int lane = threadIdx.x & (kWarp - 1);
     const int g = lane / LPR;
     const int sub = lane % LPR;
@@ -177,7 +196,6 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a, int6
     for (int off = kWarp / 2; off >= LPR; off >>= 1)
 #pragma unroll
         for (int c = 0; c < NV; ++c) acc[c] = f4_add(acc[c], f4_shfl_xor(acc[c], off));
-    const int ldp = 4 * w4;
     if (lane < LPR) {
         float* part = a.seg_partial + s * ldp;
 #pragma unroll
@@ -210,14 +228,26 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a, int6
 }
 
 template <int LPR, int NV, int U>
-int launch_agg(const grd_agg_args& a, cudaStream_t st) {
+int launch_agg(const grd_agg_args& a, int chunk_cols, cudaStream_t st) {
     constexpr int NG = kWarp / LPR;
     const int64_t light_warps = (a.n_rows + NG - 1) / NG;
     const int64_t warps = light_warps + a.n_segs;
     if (warps == 0) return 0;
     const int64_t blocks = (warps * kWarp + 255) / 256;
-    agg_sum_kernel<LPR, NV, U><<<static_cast<unsigned>(blocks), 256, 0, st>>>(a, light_warps);
+    const unsigned chunks = static_cast<unsigned>((a.width + chunk_cols - 1) / chunk_cols);
+    agg_sum_kernel<LPR, NV, U><<<dim3(static_cast<unsigned>(blocks), chunks), 256, 0, st>>>(a, light_warps,
+                                                                                           chunk_cols);
     return launch_status("agg_sum");
+}
+
+int agg_chunk_cols(int width) {
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char* e = getenv("GRD_AGG_CHUNK");
+        cfg = e ? atoi(e) : 0;   // measured: chunking does not pay on B200 (L2 already absorbs reuse)
+    }
+    if (cfg <= 0 || width <= cfg) return (width + 3) / 4 * 4;
+    return (cfg + 3) / 4 * 4;
 }
 
 // ------------------------------------------------------------ K1 / K9 --
@@ -267,7 +297,7 @@ __global__ void wgrad_reduce_kernel(int64_t m, int64_t n, int64_t splits, int64_
 }
 
 int64_t wgrad_splits(int64_t m, int64_t n, int64_t k) {
-    const int64_t bn = n >= 128 ? 128 : (n + 31) / 32 * 32;   // MN-major B tile width
+    const int64_t bn = n >= 256 ? 256 : (n + 31) / 32 * 32;   // MN-major B tile width
     const int64_t tiles = ((m + 127) / 128) * ((n + bn - 1) / bn);
     // >= one wave of CTAs, and K chunks of <= 8192 rows so each fp32 TMEM
     // accumulation stays short (partials are then reduced in a fixed tree)
@@ -483,16 +513,19 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
                          !a.heavy_counter || a.seg_len <= 0))
         return fail(kErrArg, "agg_sum: incomplete heavy-row split");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int w4 = (a.width + 3) / 4;
-    if (w4 <= 1) return launch_agg<1, 1, 4>(a, st);
-    if (w4 <= 2) return launch_agg<2, 1, 4>(a, st);
-    if (w4 <= 4) return launch_agg<4, 1, 4>(a, st);
-    if (w4 <= 8) return launch_agg<8, 1, 4>(a, st);
-    if (w4 <= 16) return launch_agg<16, 1, 4>(a, st);
-    if (w4 <= 32) return launch_agg<32, 1, 4>(a, st);
-    if (w4 <= 64) return launch_agg<32, 2, 4>(a, st);
-    if (w4 <= 128) return launch_agg<32, 4, 2>(a, st);
-    return launch_agg<32, 8, 1>(a, st);
+    const int cc = agg_chunk_cols(a.width);
+    if (a.n_segs > 0 && (a.width + cc - 1) / cc > kMaxAggChunks)
+        return fail(kErrArg, "agg_sum: too many column chunks");
+    const int w4 = (cc + 3) / 4;
+    if (w4 <= 1) return launch_agg<1, 1, 4>(a, cc, st);
+    if (w4 <= 2) return launch_agg<2, 1, 4>(a, cc, st);
+    if (w4 <= 4) return launch_agg<4, 1, 4>(a, cc, st);
+    if (w4 <= 8) return launch_agg<8, 1, 4>(a, cc, st);
+    if (w4 <= 16) return launch_agg<16, 1, 4>(a, cc, st);
+    if (w4 <= 32) return launch_agg<32, 1, 4>(a, cc, st);
+    if (w4 <= 64) return launch_agg<32, 2, 4>(a, cc, st);
+    if (w4 <= 128) return launch_agg<32, 4, 2>(a, cc, st);
+    return launch_agg<32, 8, 1>(a, cc, st);
 }
 
 extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {

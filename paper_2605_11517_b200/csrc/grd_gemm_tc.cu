@@ -6,7 +6,7 @@
 //          Al = A - Ah;  C ~= Al*Bh + Ah*Bl + Ah*Bh  (kind::tf32 MMAs,
 //          fp32 accumulation in TMEM; the dropped Al*Bl is ~2^-22 relative).
 //
-// Warp-specialised persistent kernel (10 warps):
+// Warp-specialised persistent kernel (14 warps):
 //   warp 0     producer: TMA tensor copies of raw A (and, for the weight
 //              gradient, raw B) into a ring of shared-memory stages; the
 //              weight operand of forward/dgrad GEMMs is pre-split into hi/lo
@@ -14,13 +14,15 @@
 //              bulk copy per stage;
 //   warp 1     MMA issuer: one elected thread, 12 tcgen05.mma per 32-deep K
 //              block, tcgen05.commit releases the stage / publishes a tile;
-//   warps 2-5  converters: split each raw stage into hi (in place) and lo;
-//   warps 6-9  epilogue: tcgen05.ld of the double-buffered TMEM accumulator,
+//   warps 2-9  converters: split each raw stage into hi (in place) and lo;
+//   warps 10-13 epilogue: tcgen05.ld of the double-buffered TMEM accumulator,
 //              fused row-scale / element-multiply / ReLU-mask / ReLU /
 //              accumulate, 128-byte row stores (or split-K partial tiles).
-// Shared-memory tiles use the canonical SWIZZLE_128B layouts: K-major for
-// row-major activations (TMA box 32 K x 128 rows), MN-major for the
-// weight-gradient operands whose rows run along K (TMA boxes 32 x 32).
+// Shared-memory tiles use the canonical 128-byte swizzled layouts: K-major
+// SWIZZLE_128B for row-major activations (TMA box 32 K x 128 rows) and, for
+// the weight-gradient operands whose rows run along K, MN-major
+// SWIZZLE_128B_BASE32B (TMA SWIZZLE_128B_ATOM_32B boxes of 32 MN x 32 K),
+// the only MN-major layout the tf32 MMA accepts.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -42,8 +44,8 @@ constexpr int kEpiWarp0 = 10;
 
 enum OpMode : int {
     kKMajorTma = 0,     // raw, K-contiguous rows, one TMA box (32 x rows)
-    kMNMajorTma = 1,    // raw, rows contiguous along MN: TMA boxes (32 MN x 32 K) into a
-                        // staging area, transposed to K-major by the converters
+    kMNMajorTma = 1,    // raw, rows contiguous along MN: TMA boxes (32 MN x 32 K rows)
+                        // in the SW128_32B-atom layout the tf32 MMA reads MN-major
     kPacked = 2,        // pre-split hi/lo K-major tiles, one bulk copy
 };
 
@@ -68,13 +70,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Shared-memory matrix descriptor, SWIZZLE_128B, version 1.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor, version 1.  layout: 2 = SWIZZLE_128B
+// (K-major here), 1 = SWIZZLE_128B_BASE32B (the MN-major tf32 layout).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2u) {
     uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
     d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
     d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
     d |= static_cast<uint64_t>(1u) << 46;
-    d |= static_cast<uint64_t>(2u) << 61;
+    d |= static_cast<uint64_t>(layout) << 61;
     return d;
 }
 
@@ -154,38 +157,36 @@ __device__ __forceinline__ float4 hi4(float4 v) {
     return v;
 }
 
-// Split a raw tile in place: hi over raw, lo into `lo` (same swizzled layout).
-__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t bytes, int ctid, int nthr) {
-    float4* r4 = reinterpret_cast<float4*>(raw);
-    float4* l4 = reinterpret_cast<float4*>(lo);
-    for (uint32_t i = ctid; i < bytes / 16; i += nthr) {
-        const float4 v = r4[i];
-        const float4 h = hi4(v);
-        r4[i] = h;
-        l4[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-    }
+// Split a raw tile in place: hi over raw, lo into `lo` (same swizzled layout,
+// elementwise).  Shared-space 128-bit accesses, 4 loads in flight per thread.
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
 }
-
-// Transpose-and-split an MN-major raw tile (R/32 TMA atoms of 32 MN x 32 K,
-// element (mn, k) of atom j at j*4096 + k*128 + swizzled chunk) into K-major
-// hi/lo tiles.  Lane l of a warp handles (mn & 7, k & 3) = (l & 7, l >> 3):
-// conflict-free stores, 2-way-conflicted loads.
-__device__ __forceinline__ void transpose_split(const uint8_t* raw, uint8_t* hi, uint8_t* lo, int rows,
-                                                int ctid, int nthr) {
-    const int total = rows * 32;
-    for (int i = ctid; i < total; i += nthr) {
-        const int atom = i >> 10, within = i & 1023;
-        const int w = within >> 5, l = within & 31;
-        const int k = (w & 7) * 4 + (l >> 3);
-        const int mn = (w >> 3) * 8 + (l & 7);
-        const float v = *reinterpret_cast<const float*>(
-            raw + atom * 4096 + k * 128 + ((((mn >> 2) ^ (k & 7)) & 7) << 4) + (mn & 3) * 4);
-        const int row = atom * 32 + mn;
-        const uint32_t off = static_cast<uint32_t>(row) * 128u + ((static_cast<uint32_t>((k >> 2) ^ (row & 7))) << 4) +
-                             static_cast<uint32_t>(k & 3) * 4u;
-        const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-        *reinterpret_cast<float*>(hi + off) = h;
-        *reinterpret_cast<float*>(lo + off) = v - h;
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t bytes, int ctid, int nthr) {
+    const uint32_t r0 = smem_u32(raw), l0 = smem_u32(lo);
+    const uint32_t n16 = bytes / 16;
+    uint32_t i = ctid;
+    for (; i + 3u * nthr < n16; i += 4u * nthr) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = lds128(r0 + (i + u * nthr) * 16u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 h = hi4(v[u]);
+            sts128(r0 + (i + u * nthr) * 16u, h);
+            sts128(l0 + (i + u * nthr) * 16u, make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w));
+        }
+    }
+    for (; i < n16; i += nthr) {
+        const float4 v = lds128(r0 + i * 16u);
+        const float4 h = hi4(v);
+        sts128(r0 + i * 16u, h);
+        sts128(l0 + i * 16u, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
     }
 }
 
@@ -199,9 +200,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t a_bytes = kBM * 128u;
     const uint32_t b_bytes = static_cast<uint32_t>(bn) * 128u;
     // stage: A hi | A lo | B hi | B lo | [A raw] | [B raw]  (raw only for MN-major)
-    const uint32_t a_raw_off = 2u * (a_bytes + b_bytes);
-    const uint32_t b_raw_off = a_raw_off + (p.a_mode == kMNMajorTma ? a_bytes : 0u);
-    const uint32_t stage_bytes = b_raw_off + (p.b_mode == kMNMajorTma ? b_bytes : 0u);
+    const uint32_t stage_bytes = 2u * (a_bytes + b_bytes);   // A hi | A lo | B hi | B lo
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
     uint64_t* full = bars;             // [S]
     uint64_t* conv = bars + S;         // [S]
@@ -270,7 +269,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         tma_2d(st, &map_a, static_cast<int32_t>(k0), static_cast<int32_t>(m0), full + s);
                     } else {
                         for (int j = 0; j < kBM / 32; ++j)
-                            tma_2d(st + a_raw_off + j * 4096, &map_a, static_cast<int32_t>(m0 + 32 * j),
+                            tma_2d(st + j * 4096, &map_a, static_cast<int32_t>(m0 + 32 * j),
                                    static_cast<int32_t>(k0), full + s);
                     }
                     uint8_t* bdst = st + 2 * a_bytes;
@@ -283,7 +282,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         tma_2d(bdst, &map_b, static_cast<int32_t>(k0), static_cast<int32_t>(n0), full + s);
                     } else {
                         for (int j = 0; j < bn / 32; ++j)
-                            tma_2d(st + b_raw_off + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
+                            tma_2d(bdst + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
                                    static_cast<int32_t>(k0), full + s);
                     }
                 }
@@ -292,11 +291,17 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------- MMA issuer --
         if (lane == 0) {
-            // every operand reaches the tensor core K-major (MN-major inputs are
-            // transposed by the converters): advance 32 B per 8-deep MMA
-            const uint32_t idesc = make_idesc(bn, 0, 0);
-            const uint32_t a_step = 32u, b_step = 32u;
-            const uint32_t a_lbo = 16u, b_lbo = 16u, a_sbo = 1024u, b_sbo = 1024u;
+            // K-major: SW128, advance 32 B per 8-deep MMA inside the 128 B row.
+            // MN-major: SW128_32B atoms of 32 MN x 4 K rows, LBO = 4 KB between
+            // 32-wide MN atoms, SBO = 512 B between 4-row K groups, advance
+            // 1024 B (8 K rows) per MMA.
+            const int a_mn = p.a_mode == kMNMajorTma;
+            const int b_mn = p.b_mode == kMNMajorTma;
+            const uint32_t idesc = make_idesc(bn, a_mn, b_mn);
+            const uint32_t a_step = a_mn ? 1024u : 32u, b_step = b_mn ? 1024u : 32u;
+            const uint32_t a_lbo = a_mn ? 4096u : 16u, b_lbo = b_mn ? 4096u : 16u;
+            const uint32_t a_sbo = a_mn ? 512u : 1024u, b_sbo = b_mn ? 512u : 1024u;
+            const uint32_t a_lay = a_mn ? 1u : 2u, b_lay = b_mn ? 1u : 2u;
             uint64_t g = 0;
             int64_t i = 0;   // tiles with K work (empty split-K tiles are skipped)
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -316,10 +321,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const uint32_t bh = smem_u32(st + 2 * a_bytes), bl = smem_u32(st + 2 * a_bytes + b_bytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 8; ++kk) {
-                        const uint64_t dah = make_desc(ah + kk * a_step, a_lbo, a_sbo);
-                        const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo);
-                        const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo);
-                        const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo);
+                        const uint64_t dah = make_desc(ah + kk * a_step, a_lbo, a_sbo, a_lay);
+                        const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo, a_lay);
+                        const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo, b_lay);
+                        const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo, b_lay);
                         mma_tf32(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
                         mma_tf32(tacc, dah, dbl, idesc, 1u);
                         mma_tf32(tacc, dah, dbh, idesc, 1u);
@@ -341,11 +346,9 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int s = static_cast<int>(g % S);
                 mbar_wait(full + s, static_cast<uint32_t>((g / S) & 1));
                 uint8_t* st = smem + s * stage_bytes;
-                if (p.a_mode == kKMajorTma) split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads);
-                else transpose_split(st + a_raw_off, st, st + a_bytes, kBM, ctid, kConvThreads);
+                split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads);
                 uint8_t* bh = st + 2 * a_bytes;
-                if (p.b_mode == kKMajorTma) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads);
-                else if (p.b_mode == kMNMajorTma) transpose_split(st + b_raw_off, bh, bh + b_bytes, bn, ctid, kConvThreads);
+                if (p.b_mode != kPacked) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(conv + s);
             }
@@ -391,6 +394,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const int64_t n = n0 + c0 + j;
                     if (n >= n_pad) continue;
                     float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    if (p.accumulate) {
+                        const float4 o = *reinterpret_cast<const float4*>(crow + j);
+                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                    }
                     if (p.row_scale) { x.x *= rs; x.y *= rs; x.z *= rs; x.w *= rs; }
                     if (p.elem_mul) {
                         const float4 e = *reinterpret_cast<const float4*>(p.elem_mul + row * p.ld_elem_mul + n);
@@ -405,10 +412,6 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     }
                     if (p.relu_out) {
                         x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
-                    }
-                    if (p.accumulate) {
-                        const float4 o = *reinterpret_cast<const float4*>(crow + j);
-                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
                     }
                     *reinterpret_cast<float4*>(crow + j) = x;
                 }
@@ -470,9 +473,10 @@ EncodeFn encoder() {
 }
 
 // 2-D fp32 tensor map over a row-major matrix [rows][cols] (leading dim ld),
-// box = box_cols (inner) x box_rows, SWIZZLE_128B, zero OOB fill.
+// box = box_cols (inner) x box_rows, 128-byte swizzle (16 B or 32 B atoms),
+// zero OOB fill.
 bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
-              uint32_t box_rows) {
+              uint32_t box_rows, bool atom32 = false) {
     EncodeFn fn = encoder();
     if (!fn) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -480,12 +484,25 @@ bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, i
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE,
+              atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+inline int bn_max() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("GRD_GEMM_BN_MAX");
+        v = e ? atoi(e) : 256;
+        if (v != 64 && v != 128 && v != 256) v = 256;
+    }
+    return v;
+}
+
 inline int pick_bn(int64_t n) {
-    if (n > 128) return n >= 256 ? 256 : static_cast<int>((n + 31) / 32 * 32);
+    if (n >= bn_max()) return bn_max();
+    if (n > 128) return static_cast<int>((n + 31) / 32 * 32);
     int bn = static_cast<int>((n + 15) / 16 * 16);
     return bn < 16 ? 16 : bn;
 }
@@ -538,7 +555,7 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (!make_map(&map_a, g.a, g.m, g.k, g.lda, 32, 128)) return cudaErrorInvalidValue;
     } else {
         p.a_mode = kMNMajorTma;
-        if (!make_map(&map_a, g.a, g.k, g.m, g.lda, 32, 32)) return cudaErrorInvalidValue;
+        if (!make_map(&map_a, g.a, g.k, g.m, g.lda, 32, 32, true)) return cudaErrorInvalidValue;
     }
     if (g.b_packed) {
         p.b_mode = kPacked;
@@ -549,15 +566,10 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (!make_map(&map_b, g.b, g.n, g.k, g.ldb, 32, static_cast<uint32_t>(p.bn))) return cudaErrorInvalidValue;
     } else {
         p.b_mode = kMNMajorTma;  // B stored K x N
-        if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32)) return cudaErrorInvalidValue;
+        if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32, true)) return cudaErrorInvalidValue;
     }
-    if (p.b_mode == kMNMajorTma) {    // raw staging: keep two stages in shared memory
-        p.bn = p.bn > 128 ? 128 : (p.bn + 31) / 32 * 32;
-        if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32)) return cudaErrorInvalidValue;
-    }
-    uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.bn) * 128u);
-    if (p.a_mode == kMNMajorTma) stage += kBM * 128u;
-    if (p.b_mode == kMNMajorTma) stage += static_cast<uint32_t>(p.bn) * 128u;
+    if (p.b_mode == kMNMajorTma) p.bn = (p.bn + 31) / 32 * 32;   // whole 32-wide TMA atoms
+    const uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.bn) * 128u);
     p.stages = static_cast<int>((220u * 1024u) / stage);
     if (p.stages > 4) p.stages = 4;
     if (p.stages < 2) p.stages = 2;

@@ -147,6 +147,10 @@ class DevicePartition:
 def _degree_scale(name: str, deg: np.ndarray) -> np.ndarray:
     if name == "inv_deg1":
         return 1.0 / (deg + 1.0)
+    if name == "inv_deg":        # GraphSAGE mean over in-neighbours (0 if none)
+        out = np.zeros_like(deg)
+        np.divide(1.0, deg, out=out, where=deg > 0)
+        return out
     if name == "s":
         return 1.0 / np.sqrt(deg + 1.0)
     if name == "s_inv_deg1":
@@ -160,8 +164,10 @@ class _LayerCfg:
         self.d_in, self.d_out = dims[layer], dims[layer + 1]
         self.transform_first = self.d_out <= self.d_in
         self.sym = mode == "symmetric_norm"
+        self.sage = mode == "sage_mean"
         self.rownorm = row_normalize
         self.last = last
+        self.ld_in, self.ld_out = ld_of(self.d_in), ld_of(self.d_out)
 
     # scale applied to the upstream gradient before this layer's pull (TF)
     # or after its dgrad GEMM (AF): mean -> 1/(deg+1), sym -> 1/sqrt(deg+1)
@@ -171,26 +177,41 @@ class _LayerCfg:
 
 
 class _Weights:
-    """fp32 device copies of W_l and dW_l, zero padded to [ld(d_in), ld(d_out)]."""
+    """fp32 device copies of W_l and dW_l, zero padded to [ld(d_in), ld(d_out)].
+    GraphSAGE layers keep [W_root | W_nbr] as [ld(d_in), 2 ld(d_out)] with the
+    neighbour block starting at column ld(d_out) (16-byte aligned)."""
 
     def __init__(self, model, device):
         self.w = []
         self.dw = []
+        self.blocks = 2 if model.kind == "sage" else 1
         for w in model.weights:
-            t = torch.zeros((ld_of(w.shape[0]), ld_of(w.shape[1])), dtype=torch.float32, device=device)
-            t[: w.shape[0], : w.shape[1]] = torch.from_numpy(np.asarray(w, dtype=np.float32)).to(device)
+            d_in, d_out = w.shape[0], w.shape[1] // self.blocks
+            t = torch.zeros((ld_of(d_in), self.blocks * ld_of(d_out)), dtype=torch.float32, device=device)
             self.w.append(t)
             self.dw.append(torch.zeros_like(t))
+        self.load(model)
+
+    def _views(self, t: torch.Tensor, w: np.ndarray):
+        d_in, d_out = w.shape[0], w.shape[1] // self.blocks
+        ld = ld_of(d_out)
+        return [(t[:d_in, b * ld: b * ld + d_out], slice(b * d_out, (b + 1) * d_out))
+                for b in range(self.blocks)]
 
     def load(self, model) -> None:
         for t, w in zip(self.w, model.weights):
-            t[: w.shape[0], : w.shape[1]].copy_(torch.from_numpy(np.asarray(w, dtype=np.float32)))
+            w32 = torch.from_numpy(np.asarray(w, dtype=np.float32))
+            for view, cols in self._views(t, w):
+                view.copy_(w32[:, cols])
 
     def export(self, model) -> None:
-        model.weights = [t[: w.shape[0], : w.shape[1]].double().cpu().numpy()
-                         for t, w in zip(self.w, model.weights)]
-        model.weight_grads = [t[: w.shape[0], : w.shape[1]].double().cpu().numpy()
-                              for t, w in zip(self.dw, model.weights)]
+        def host(tensors):
+            out = []
+            for t, w in zip(tensors, model.weights):
+                out.append(np.concatenate([v.double().cpu().numpy() for v, _ in self._views(t, w)],
+                                          axis=1))
+            return out
+        model.weights, model.weight_grads = host(self.w), host(self.dw)
 
 
 class _EngineBase:
@@ -245,9 +266,12 @@ class LayerwiseEngine(_EngineBase):
     def __init__(self, dg, model, features, labels, train_mask):
         super().__init__(dg, model, features, labels, train_mask)
         dev = self.device
-        self.t1 = ops.zeros_rows(self.V, self.maxw, dev)
-        self.g = ops.zeros_rows(self.V, self.maxw, dev)
-        self.h = ops.zeros_rows(self.V, self.maxw, dev)
+        wide = 2 * ld_of(self.maxw) if model.kind == "sage" else self.maxw
+        self.t1 = ops.zeros_rows(self.V, wide, dev)
+        self.g = ops.zeros_rows(self.V, wide, dev)
+        self.h = ops.zeros_rows(self.V, wide, dev)
+        self.t2 = ops.zeros_rows(self.V, self.maxw, dev) if model.kind == "sage" else None
+        self._gh = (self.g, self.h)
 
     # ---------------------------------------------------------- forward --
     def _forward_layer(self, l: int, x: torch.Tensor, out: torch.Tensor, relu: bool) -> None:
@@ -261,10 +285,60 @@ class LayerwiseEngine(_EngineBase):
             ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
             ops.gemm(self.t1, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
 
+    # ------------------------------------------------ GraphSAGE-mean layer --
+    # out = act(X W_root + mean_in(X) W_nbr); weights [W_root | W_nbr].
+    def _forward_sage(self, l: int, x: torch.Tensor, out: torch.Tensor, relu: bool) -> None:
+        c, dg = self.cfg[l], self.dg
+        W = self.wts.w[l]
+        if c.transform_first:
+            # Y = X [W_root | W_nbr] (one GEMM), out = Y_root + mean_in(Y_nbr)
+            y = self.t1[:, : 2 * c.ld_out]
+            ops.gemm(x, W, y, self.V, 2 * c.ld_out, c.d_in)
+            ops.agg_sum(dg.fwd, y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
+                        add_y=y[:, : c.ld_out], relu=relu)
+        else:
+            # N = mean_in(X), out = X W_root + N W_nbr
+            n = self.t1[:, : c.ld_in]
+            ops.agg_sum(dg.fwd, x, n, c.d_in, post_div_deg=2, no_self=True)
+            ops.gemm(x, W[:, : c.ld_out], out, self.V, c.d_out, c.d_in)
+            ops.gemm(n, W[:, c.ld_out:], out, self.V, c.d_out, c.d_in, accumulate=True, relu_out=relu)
+
+    def _backward_sage(self, l: int, x: torch.Tensor, lr: float) -> None:
+        """g holds gp = dL/dpre of layer l (ReLU mask applied by the producer);
+        leaves dL/dA_l (masked for layer l-1) in h, then swaps g and h."""
+        c, dg = self.cfg[l], self.dg
+        W, dW = self.wts.w[l], self.wts.dw[l]
+        inv_deg = dg.scale("inv_deg")
+        ref, _ = self._consumer_epilogue(l - 1) if l > 0 else (None, None)
+        if c.transform_first:
+            # [gp | H_nbr] with H_nbr = mean_in^T gp (pull over out-edges, 1/deg_v per edge)
+            gcat = self.g[:, : 2 * c.ld_out]
+            ops.agg_sum(dg.bwd, gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
+                        no_self=True)
+            if l > 0:
+                ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
+            ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=W, lr=lr)
+        else:
+            gp = self.g[:, : c.ld_out]
+            n = self.t1[:, : c.ld_in]
+            ops.agg_sum(dg.fwd, x, n, c.d_in, post_div_deg=2, no_self=True)     # regather
+            if l > 0:
+                gn = self.t2[:, : c.ld_in]
+                ops.gemm(gp, W[:, c.ld_out:], gn, self.V, c.d_in, c.d_out, trans_b=True)
+                ops.agg_sum(dg.bwd, gn, self.h, c.d_in, src_scale=inv_deg, no_self=True)
+                ops.gemm(gp, W[:, : c.ld_out], self.h, self.V, c.d_in, c.d_out, trans_b=True,
+                         accumulate=True, relu_ref=ref)
+            ops.wgrad_sgd(x, gp, dW[:, : c.ld_out], c.d_in, c.d_out, self.V, w=W[:, : c.ld_out], lr=lr)
+            ops.wgrad_sgd(n, gp, dW[:, c.ld_out:], c.d_in, c.d_out, self.V, w=W[:, c.ld_out:], lr=lr)
+        self.g, self.h = self.h, self.g
+
     def forward(self) -> None:
         for l, c in enumerate(self.cfg):
             x = self.layer_input(l)
             out = self.acts[l + 1]
+            if c.sage:
+                self._forward_sage(l, x, out, relu=not c.last)
+                continue
             self._forward_layer(l, x, out, relu=not c.last and not c.rownorm)
             if c.rownorm:
                 ops.rownorm_fwd(out, out, self.V, c.d_out, relu=not c.last)
@@ -276,7 +350,7 @@ class LayerwiseEngine(_EngineBase):
         if c.rownorm:
             return None, None
         ref = None if c.last else self.acts[l + 1]
-        scale = self.dg.scale(c.pre_scale) if c.transform_first else None
+        scale = self.dg.scale(c.pre_scale) if c.transform_first and not c.sage else None
         return ref, scale
 
     def loss(self) -> None:
@@ -291,6 +365,9 @@ class LayerwiseEngine(_EngineBase):
             c = self.cfg[l]
             W, dW = self.wts.w[l], self.wts.dw[l]
             x = self.layer_input(l)
+            if c.sage:
+                self._backward_sage(l, x, lr)
+                continue
             s = dg.scale("s") if c.sym else None
             have_n = False
             if c.rownorm:
@@ -341,6 +418,7 @@ class LayerwiseEngine(_EngineBase):
         return self.dg.scale("inv_deg1")
 
     def epoch(self, lr: float) -> None:
+        self.g, self.h = self._gh    # canonical buffer roles (layers may swap them)
         self.forward()
         self.loss()
         self.backward(lr)

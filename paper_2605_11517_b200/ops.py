@@ -119,7 +119,7 @@ class AggSpec:
             heavy_rows=up(heavy, np.int32) if has_heavy else None,
             heavy_seg_ptr=up(seg_ptr, np.int64) if has_heavy else None,
             seg_heavy=up(seg_heavy, np.int32) if has_heavy else None,
-            heavy_counter=torch.zeros(max(heavy.size, 1), dtype=torch.int32, device=device)
+            heavy_counter=torch.zeros(16 * max(heavy.size, 1), dtype=torch.int32, device=device)
             if has_heavy else None,
             n_heavy=int(heavy.size), n_segs=int(seg_heavy.size), nnz=int(row_ptr[-1]),
         )
@@ -135,7 +135,9 @@ class AggSpec:
 
 def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
             src_scale=None, post_scale=None, post_div_deg=False, relu=False,
-            mask_ref=None) -> None:
+            mask_ref=None, no_self=False, add_y=None) -> None:
+    """out[o] = act(post(sum_e y[idx_e] (+ y[self])) + add_y[o]); post_div_deg:
+    False/0 none, True/1 divide by deg+1, 2 divide by deg (GraphSAGE mean)."""
     a = _lib.GrdAggArgs()
     a.n_rows = spec.n_rows
     a.row_ptr = _p(spec.row_ptr)
@@ -146,7 +148,7 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
     a.ldy = _ld(y)
     a.src_scale = _p(src_scale)
     a.post_scale = _p(post_scale)
-    a.post_div_deg = int(bool(post_div_deg))
+    a.post_div_deg = int(post_div_deg)
     a.relu = int(bool(relu))
     a.out = _p(out)
     a.ldo = _ld(out)
@@ -162,8 +164,12 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
     a.heavy_counter = _p(spec.heavy_counter)
     a.mask_ref = _p(mask_ref)
     a.ld_mask_ref = _ld(mask_ref) if mask_ref is not None else 0
+    a.no_self = int(bool(no_self))
+    a.add_y = _p(add_y)
+    a.ld_add_y = _ld(add_y) if add_y is not None else 0
     R, E, w = spec.n_rows, spec.nnz, int(width)
-    nbytes = 8 * (R + 1) + 4 * E + 4 * w * (E + R) + 4 * w * R
+    nbytes = 8 * (R + 1) + 4 * E + 4 * w * (E + R * (not no_self)) + 4 * w * R
+    nbytes += 4 * w * R * (add_y is not None)
     nbytes += 4 * R * ((spec.out_idx is not None) + (spec.self_idx is not None)
                        + (post_scale is not None))
     nbytes += 4 * (E + R) * (src_scale is not None) + 4 * w * R * (mask_ref is not None)

@@ -262,6 +262,9 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
         raise ValueError("plan was built for a different graph")
     observed = hierarchy is not None or use_snapshots or grad_probe is not None \
         or partition_order is not None
+    if observed and model.kind != "gcn":
+        raise NotImplementedError("per-partition observers (hierarchy, probes, snapshots, "
+                                  "partition_order) are implemented for GCN layers")
     session = session_for(dataset, plan, model, layerwise=not observed)
     trained, trace = session.train(epochs, lr, hierarchy=hierarchy, use_snapshots=use_snapshots,
                                    grad_probe=grad_probe, partition_order=partition_order)

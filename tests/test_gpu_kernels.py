@@ -109,7 +109,7 @@ def test_gemm_relu_out_and_accumulate():
     a, b, c0 = rng.normal(size=(50, 12)), rng.normal(size=(12, 9)), rng.normal(size=(50, 9))
     c = _dev(c0)
     ops.gemm(_dev(a), _dev(b), c, 50, 9, 12, relu_out=True, accumulate=True)
-    assert rel_l2(_host(c, 9), c0 + np.maximum(a @ b, 0)) < 5e-6
+    assert rel_l2(_host(c, 9), np.maximum(c0 + a @ b, 0)) < 5e-6   # relu(C + AB)
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000)])

@@ -1,0 +1,65 @@
+"""GPU parity of the builder-defined GraphSAGE-mean / GAT layers against the
+float64 oracle (oracle/sage_gat.py).  Tolerance as the north star: 1e-4
+L2-relative on weights and gradients, 1e-4 relative on the loss."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from conftest import rel_l2  # noqa: E402
+from oracle import sage_gat  # noqa: E402
+import paper_2605_11517_b200 as g2  # noqa: E402
+
+TOL = 1e-4
+
+
+def _setup(scale, deg, F, C, L, H, P, mode):
+    g = g2.generate_kronecker(scale, deg, seed=scale)
+    ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=scale + 1)
+    part = g2.switching_aware_partition(g, P, g2.PartitionerParams(seed=scale + 2))
+    plan = g2.build_partition_plan(g, part.labels, P)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=scale + 3, aggregation_mode=mode)
+    return g, ds, plan, model
+
+
+@pytest.mark.parametrize("F,H,C,L", [(6, 12, 3, 3), (16, 8, 5, 2), (10, 10, 4, 3), (3, 37, 7, 2)])
+def test_sage_matches_oracle(F, H, C, L):
+    g, ds, plan, model = _setup(9, 8, F, C, L, H, 4, "sage_mean")
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=3, lr=0.05)
+    W, grads, ref = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                        model.weights, 3, 0.05)
+    for (_, l, a), (_, rl, ra) in zip(trace, ref):
+        assert abs(l - rl) <= TOL * abs(rl)
+        assert abs(a - ra) <= 2.0 / ds.train_mask.sum()
+    for a, b in zip(trained.weights, W):
+        assert a.shape == b.shape and rel_l2(a, b) < TOL
+    # gradients of the first epoch: later epochs' gradients may cross a ReLU
+    # kink when the weights differ in the 7th digit (a discontinuity, not
+    # rounding), so they are compared where the weights are identical
+    one, _, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    _, grads1, _ = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                       model.weights, 1, 0.05)
+    for a, b in zip(one.weight_grads, grads1):
+        assert rel_l2(a, b) < TOL
+
+
+def test_sage_power_law_graph_with_hubs():
+    # scale-12 RMAT: hub rows exceed the heavy-row threshold in both directions
+    g, ds, plan, model = _setup(12, 16, 20, 6, 2, 24, 8, "sage_mean")
+    assert g.out_degrees().max() > 256
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.05)
+    W, grads, ref = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                        model.weights, 2, 0.05)
+    assert abs(trace[-1][1] - ref[-1][1]) <= TOL * abs(ref[-1][1])
+    for a, b in zip(trained.weights, W):
+        assert rel_l2(a, b) < TOL
+
+
+def test_sage_rejects_per_partition_observers():
+    g, ds, plan, model = _setup(7, 4, 4, 3, 2, 4, 2, "sage_mean")
+    with pytest.raises(NotImplementedError):
+        g2.partitioned_train(ds, plan, model, 1, 0.01, grad_probe=lambda *a: None)

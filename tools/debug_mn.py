@@ -9,7 +9,7 @@ b = torch.randn(k, n, device='cuda')
 c = torch.zeros(m, n, device='cuda')
 ops.gemm(a, b, c, m, n, k, trans_a=True)
 ref = a.double().T @ b.double()
-print(os.environ.get("GRD_DEBUG_MN"), "rel", float((c.double() - ref).norm() / ref.norm()), "cnorm", float(c.norm()))
+print(os.environ.get("GRD_MN_NATIVE"), "rel", float((c.double() - ref).norm() / ref.norm()), "cnorm", float(c.norm()))
 # block structure probe: which output rows are right
 err_rows = ((c.double() - ref).norm(dim=1) / ref.norm(dim=1)).cpu().numpy()
 print("rows ok:", np.flatnonzero(err_rows < 1e-4)[:40])
