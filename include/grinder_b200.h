@@ -209,7 +209,8 @@ int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a,
 
 /* K4 — masked softmax cross-entropy (model.py:102-129): per masked row,
  * loss -= log softmax(logits)[label]; grad = (softmax - onehot) / count *
- * grad_scale[row] (grad_scale nullable); unmasked rows get zero gradient.
+ * grad_scale[row] (grad_scale nullable); unmasked rows get zero gradient and
+ * the padding columns [n_classes, round_up(n_classes,4)) are zeroed.
  * stats_out (device, 4 doubles): {loss, accuracy, loss_sum, correct}.
  * `partials` needs grd_loss_partials(n_rows) doubles of scratch. */
 int64_t grd_loss_partials(int64_t n_rows);

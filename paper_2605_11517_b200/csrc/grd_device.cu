@@ -320,12 +320,16 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
                                                    const float* __restrict__ gscale, double* partials) {
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x / kWarp;
+    const int c4 = (c + 3) / 4 * 4;
     double loss_acc = 0.0;
     double correct = 0.0;
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / kWarp);
     for (int64_t r = int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows; r += nwarps) {
         const float* row = logits + r * ldl;
         float* grow = grad + r * ldg;
+        // padding columns [c, round_up(c, 4)) are part of the 16-byte rows the
+        // aggregation kernels read: keep them zero
+        if (lane < c4 - c) grow[c + lane] = 0.f;
         if (!mask[r]) {
             for (int j = lane; j < c; j += kWarp) grow[j] = 0.f;
             continue;

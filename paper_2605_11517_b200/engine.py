@@ -37,7 +37,7 @@ from . import ops
 from .ops import AggSpec, ld_of
 
 __all__ = ["DeviceGraph", "DevicePartition", "LayerOps", "LayerwiseEngine", "PartitionEngine",
-           "dropout_mask"]
+           "ShardDeviceGraph", "dropout_mask"]
 
 
 def dropout_mask(dropout_rate: float, dropout_seed: int, epoch: int, layer: int,
@@ -61,6 +61,10 @@ class DeviceGraph:
         self.num_edges = int(f.in_ptr[-1])
         self.num_partitions = plan.num_partitions
         self.part_ptr = f.part_ptr.copy()
+        # rows computed on this device / rows held (owned + halo); one device
+        # owns every vertex and holds no halo
+        self.n_own = self.n_local = plan.num_vertices
+        self.comm = None
         # forward: rows = perm order, output row = vertex, self = vertex
         self.fwd = AggSpec.build(f.in_ptr, f.in_src, device, out_idx=f.perm)
         # transposed pull: rows = vertices, neighbours = out-edges (u -> v)
@@ -69,6 +73,14 @@ class DeviceGraph:
         self._scales: dict[str, torch.Tensor] = {}
         self._partitions: dict[int, "DevicePartition"] = {}
         self.plan = plan
+
+    def exchange(self, buf: torch.Tensor, width: int) -> None:
+        """Fill the halo rows of ``buf`` from their owners (no-op on one device)."""
+        return None
+
+    def local_rows(self, arr: np.ndarray) -> np.ndarray:
+        """Rows of a per-vertex host array in this device's row order."""
+        return arr
 
     def scale(self, name: str | None) -> torch.Tensor | None:
         if name is None:
@@ -85,6 +97,55 @@ class DeviceGraph:
             part = DevicePartition.from_plan(self.plan, q, self.device)
             self._partitions[q] = part
         return part
+
+
+class ShardDeviceGraph(DeviceGraph):
+    """One rank's shard (distributed.ShardPlan) on its GPU: local rows are
+    [owned | halo]; aggregations run over the owned rows only and read halo
+    rows filled by ``exchange`` (one all-to-all per call)."""
+
+    def __init__(self, graph, plan, shard, comm, device):
+        self.device = device
+        self.num_vertices = plan.num_vertices
+        self.num_edges = int(shard.in_ptr[-1])
+        self.num_partitions = plan.num_partitions
+        self.plan = plan
+        self.shard = shard
+        self.comm = comm
+        self.n_own, self.n_local = shard.n_own, shard.n_local
+        self.fwd = AggSpec.build(shard.in_ptr, shard.in_idx, device)
+        self.bwd = AggSpec.build(shard.out_ptr, shard.out_idx, device)
+        self._deg = plan.flat.in_degree[shard.local_ids].astype(np.float64)
+        self._scales = {}
+        self._partitions = {}
+        self.send_idx = torch.from_numpy(shard.send_idx.astype(np.int32)).to(device)
+        self.n_send = int(shard.send_idx.size)
+        self.n_recv = int(shard.halo.size)
+        self.recv_ident = torch.arange(self.n_recv, dtype=torch.int32, device=device)
+        self._bufs: dict = {}
+
+    def _buf(self, key: str, rows: int, ld: int) -> torch.Tensor:
+        t = self._bufs.get(key)
+        if t is None or t.numel() < max(rows * ld, 1):
+            t = torch.empty(max(rows * ld, 1), dtype=torch.float32, device=self.device)
+            self._bufs[key] = t
+        return t[: rows * ld].view(rows, ld)
+
+    def exchange(self, buf: torch.Tensor, width: int) -> None:
+        ld = ld_of(width)
+        send = self._buf("send", self.n_send, ld)
+        recv = self._buf("recv", self.n_recv, ld)
+        if self.n_send:
+            ops.gather_rows(buf, self.send_idx, send, width)
+        self.comm.all_to_all_rows(recv, send, self.shard.recv_counts, self.shard.send_counts)
+        if self.n_recv:
+            ops.gather_rows(recv, self.recv_ident, buf[self.n_own:], width)
+
+    def local_rows(self, arr: np.ndarray) -> np.ndarray:
+        return arr[self.shard.local_ids]
+
+    def partition(self, q: int):
+        raise NotImplementedError("per-partition operators run on one device")
 
 
 class DevicePartition:
@@ -216,11 +277,13 @@ class _Weights:
 
 class _EngineBase:
     def __init__(self, dg: DeviceGraph, model, features: torch.Tensor, labels: np.ndarray,
-                 train_mask: np.ndarray):
+                 train_mask: np.ndarray, mask_count: int | None = None):
         self.dg = dg
         dev = dg.device
         self.device = dev
-        self.V = dg.num_vertices
+        self.V = dg.n_own            # rows computed here
+        self.NL = dg.n_local         # rows held (owned + halo)
+        self.comm = dg.comm
         self.dims = model.dims
         self.L = model.num_layers
         self.mode = model.aggregation_mode
@@ -228,10 +291,10 @@ class _EngineBase:
         self.cfg = [_LayerCfg(l, self.dims, self.mode, model.row_normalize, l == self.L - 1)
                     for l in range(self.L)]
         self.wts = _Weights(model, dev)
-        self.acts = [features] + [ops.zeros_rows(self.V, d, dev) for d in self.dims[1:]]
+        self.acts = [features] + [ops.zeros_rows(self.NL, d, dev) for d in self.dims[1:]]
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
         self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
-        self.mask_count = int(np.count_nonzero(train_mask))
+        self.mask_count = int(np.count_nonzero(train_mask)) if mask_count is None else int(mask_count)
         if self.mask_count == 0:
             raise ValueError("loss mask selects no vertices")
         self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
@@ -240,7 +303,9 @@ class _EngineBase:
         self.dropout_rate = model.dropout_rate
         self.dropout_seed = model.dropout_seed
         self.dmask = [None] * self.L
-        self.xd = ops.zeros_rows(self.V, self.maxw, dev) if self.dropout_rate > 0 else None
+        self.xd = ops.zeros_rows(self.NL, self.maxw, dev) if self.dropout_rate > 0 else None
+        if self.comm is not None and (self.dropout_rate > 0 or model.row_normalize):
+            raise NotImplementedError("dropout / row_normalize run on one device")
 
     def set_dropout(self, epoch: int) -> None:
         if self.dropout_rate == 0.0:
@@ -263,14 +328,17 @@ class _EngineBase:
 class LayerwiseEngine(_EngineBase):
     """Fused layer-wide epoch over an HBM-resident graph (module docstring)."""
 
-    def __init__(self, dg, model, features, labels, train_mask):
-        super().__init__(dg, model, features, labels, train_mask)
+    def __init__(self, dg, model, features, labels, train_mask, mask_count=None):
+        super().__init__(dg, model, features, labels, train_mask, mask_count)
         dev = self.device
         wide = 2 * ld_of(self.maxw) if model.kind == "sage" else self.maxw
-        self.t1 = ops.zeros_rows(self.V, wide, dev)
-        self.g = ops.zeros_rows(self.V, wide, dev)
-        self.h = ops.zeros_rows(self.V, wide, dev)
-        self.t2 = ops.zeros_rows(self.V, self.maxw, dev) if model.kind == "sage" else None
+        self.t1 = ops.zeros_rows(self.NL, wide, dev)
+        self.g = ops.zeros_rows(self.NL, wide, dev)
+        self.h = ops.zeros_rows(self.NL, wide, dev)
+        self.t2 = ops.zeros_rows(self.NL, self.maxw, dev) if model.kind == "sage" else None
+        # one device: SGD fused into the weight-gradient reduction; sharded:
+        # local weight gradients are all-reduced first, SGD at epoch end
+        self.defer_sgd = self.comm is not None
         self._gh = (self.g, self.h)
 
     # ---------------------------------------------------------- forward --
@@ -280,10 +348,22 @@ class LayerwiseEngine(_EngineBase):
         s = dg.scale("s") if c.sym else None
         if c.transform_first:
             ops.gemm(x, W, self.t1, self.V, c.d_out, c.d_in, row_scale=s)
+            dg.exchange(self.t1, c.d_out)          # halo rows of P = X W
             ops.agg_sum(dg.fwd, self.t1, out, c.d_out, post_div_deg=not c.sym, post_scale=s, relu=relu)
         else:
+            self._input_halo(l, x)
             ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
             ops.gemm(self.t1, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
+
+    def _input_halo(self, l: int, x: torch.Tensor) -> None:
+        """Aggregate-first layers read the layer input's halo rows (the
+        features' halo is filled once at upload)."""
+        if l > 0:
+            self.dg.exchange(x, self.cfg[l].d_in)
+
+    def _w(self, W):
+        """SGD target of a weight-gradient call (None: deferred past the all-reduce)."""
+        return None if self.defer_sgd else W
 
     # ------------------------------------------------ GraphSAGE-mean layer --
     # out = act(X W_root + mean_in(X) W_nbr); weights [W_root | W_nbr].
@@ -294,11 +374,13 @@ class LayerwiseEngine(_EngineBase):
             # Y = X [W_root | W_nbr] (one GEMM), out = Y_root + mean_in(Y_nbr)
             y = self.t1[:, : 2 * c.ld_out]
             ops.gemm(x, W, y, self.V, 2 * c.ld_out, c.d_in)
+            dg.exchange(y[:, c.ld_out:], c.d_out)   # halo rows of X W_nbr
             ops.agg_sum(dg.fwd, y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
                         add_y=y[:, : c.ld_out], relu=relu)
         else:
             # N = mean_in(X), out = X W_root + N W_nbr
             n = self.t1[:, : c.ld_in]
+            self._input_halo(l, x)
             ops.agg_sum(dg.fwd, x, n, c.d_in, post_div_deg=2, no_self=True)
             ops.gemm(x, W[:, : c.ld_out], out, self.V, c.d_out, c.d_in)
             ops.gemm(n, W[:, c.ld_out:], out, self.V, c.d_out, c.d_in, accumulate=True, relu_out=relu)
@@ -313,11 +395,12 @@ class LayerwiseEngine(_EngineBase):
         if c.transform_first:
             # [gp | H_nbr] with H_nbr = mean_in^T gp (pull over out-edges, 1/deg_v per edge)
             gcat = self.g[:, : 2 * c.ld_out]
+            dg.exchange(gcat[:, : c.ld_out], c.d_out)   # halo rows of gp
             ops.agg_sum(dg.bwd, gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
                         no_self=True)
             if l > 0:
                 ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
-            ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=W, lr=lr)
+            ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=self._w(W), lr=lr)
         else:
             gp = self.g[:, : c.ld_out]
             n = self.t1[:, : c.ld_in]
@@ -325,11 +408,14 @@ class LayerwiseEngine(_EngineBase):
             if l > 0:
                 gn = self.t2[:, : c.ld_in]
                 ops.gemm(gp, W[:, c.ld_out:], gn, self.V, c.d_in, c.d_out, trans_b=True)
+                dg.exchange(gn, c.d_in)                  # halo rows of gp W_nbr^T
                 ops.agg_sum(dg.bwd, gn, self.h, c.d_in, src_scale=inv_deg, no_self=True)
                 ops.gemm(gp, W[:, : c.ld_out], self.h, self.V, c.d_in, c.d_out, trans_b=True,
                          accumulate=True, relu_ref=ref)
-            ops.wgrad_sgd(x, gp, dW[:, : c.ld_out], c.d_in, c.d_out, self.V, w=W[:, : c.ld_out], lr=lr)
-            ops.wgrad_sgd(n, gp, dW[:, c.ld_out:], c.d_in, c.d_out, self.V, w=W[:, c.ld_out:], lr=lr)
+            ops.wgrad_sgd(x, gp, dW[:, : c.ld_out], c.d_in, c.d_out, self.V, w=self._w(W[:, : c.ld_out]),
+                          lr=lr)
+            ops.wgrad_sgd(n, gp, dW[:, c.ld_out:], c.d_in, c.d_out, self.V, w=self._w(W[:, c.ld_out:]),
+                          lr=lr)
         self.g, self.h = self.h, self.g
 
     def forward(self) -> None:
@@ -358,6 +444,8 @@ class LayerwiseEngine(_EngineBase):
         _, scale = self._consumer_epilogue(self.L - 1)
         ops.softmax_xent(self.acts[-1], self.V, c.d_out, self.labels, self.mask, self.mask_count,
                          self.g, self.stats, self.partials, grad_scale=scale)
+        if self.comm is not None:
+            self.comm.all_reduce_sum(self.stats)   # {loss, acc, sums}: partial / global count
 
     def backward(self, lr: float) -> None:
         dg = self.dg
@@ -387,19 +475,21 @@ class LayerwiseEngine(_EngineBase):
             dmask = self.dmask[l]
             if c.transform_first:
                 # H = A_hat^T (gp * pre_scale)
+                dg.exchange(self.g, c.d_out)
                 ops.agg_sum(dg.bwd, self.g, self.h, c.d_out, post_scale=s)
                 if l > 0:
                     ops.gemm(self.h, W, self.g, self.V, c.d_in, c.d_out, trans_b=True,
                              row_scale=prev[1], elem_mul=dmask, relu_ref=prev[0])
-                ops.wgrad_sgd(x, self.h, dW, c.d_in, c.d_out, self.V, w=W, lr=lr)
+                ops.wgrad_sgd(x, self.h, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
             else:
                 if not have_n:   # regather: recompute the normalised aggregate
                     ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym,
                                 post_scale=s)
                 ops.gemm(self.g, W, self.h, self.V, c.d_in, c.d_out, trans_b=True,
                          row_scale=dg.scale(c.pre_scale))
-                ops.wgrad_sgd(self.t1, self.g, dW, c.d_in, c.d_out, self.V, w=W, lr=lr)
+                ops.wgrad_sgd(self.t1, self.g, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
                 if l > 0:
+                    dg.exchange(self.h, c.d_in)
                     post = self._combine(s is not None, prev[1])
                     ops.agg_sum(dg.bwd, self.h, self.g, c.d_in, post_scale=post,
                                 mask_ref=None if dmask is not None else prev[0])
@@ -417,11 +507,20 @@ class LayerwiseEngine(_EngineBase):
         # here: one model has one mode), so the consumer's scale is s.
         return self.dg.scale("inv_deg1")
 
+    def sgd_after_allreduce(self, lr: float) -> None:
+        """Sharded runs: sum the local weight gradients over ranks, then the
+        replicated SGD step (training.py:343,352-354)."""
+        for W, dW in zip(self.wts.w, self.wts.dw):
+            self.comm.all_reduce_sum(dW)
+            ops.wgrad_sgd(W, W, dW, dW.shape[0], dW.shape[1], 0, accumulate=True, w=W, lr=lr)
+
     def epoch(self, lr: float) -> None:
         self.g, self.h = self._gh    # canonical buffer roles (layers may swap them)
         self.forward()
         self.loss()
         self.backward(lr)
+        if self.defer_sgd:
+            self.sgd_after_allreduce(lr)
 
 
 class LayerOps:
@@ -510,8 +609,8 @@ class LayerOps:
 class PartitionEngine(_EngineBase):
     """Per-(layer, partition) execution, literally following training.py:259-358."""
 
-    def __init__(self, dg, model, features, labels, train_mask):
-        super().__init__(dg, model, features, labels, train_mask)
+    def __init__(self, dg, model, features, labels, train_mask, mask_count=None):
+        super().__init__(dg, model, features, labels, train_mask, mask_count)
         self.grad_cur = ops.zeros_rows(self.V, self.maxw, self.device)
         self.grad_prev = ops.zeros_rows(self.V, self.maxw, self.device)
         self.ops = LayerOps(model, self.device, self.wts)

@@ -28,7 +28,8 @@ import torch
 
 from . import ops
 from .dataset import LabeledDataset
-from .engine import DeviceGraph, DevicePartition, LayerOps, LayerwiseEngine, PartitionEngine
+from .engine import (DeviceGraph, DevicePartition, LayerOps, LayerwiseEngine, PartitionEngine,
+                     ShardDeviceGraph)
 from .model import ModelState, copy_model
 from .plan import PartitionPlan, PartitionTopology, build_partition_plan
 
@@ -135,21 +136,36 @@ class TrainSession:
     """
 
     def __init__(self, dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
-                 layerwise: bool = True):
+                 layerwise: bool = True, comm=None):
         if plan.num_vertices != dataset.graph.num_vertices:
             raise ValueError("plan was built for a different graph")
         self.dev = _device()
-        key = ("device_graph", str(self.dev))
-        dg = plan.device_cache.get(key)
-        if dg is None:
-            dg = DeviceGraph(dataset.graph, plan, self.dev)
-            plan.device_cache[key] = dg
+        self.comm = comm
+        if comm is None:
+            key = ("device_graph", str(self.dev))
+            dg = plan.device_cache.get(key)
+            if dg is None:
+                dg = DeviceGraph(dataset.graph, plan, self.dev)
+                plan.device_cache[key] = dg
+        else:
+            if not layerwise:
+                raise NotImplementedError("per-partition observers run on one device")
+            from .distributed import build_shard_plan
+            key = ("shard", comm.rank, comm.world, str(self.dev))
+            dg = plan.device_cache.get(key)
+            if dg is None:
+                shard = build_shard_plan(dataset.graph, plan, comm.rank, comm.world, comm)
+                dg = ShardDeviceGraph(dataset.graph, plan, shard, comm, self.dev)
+                plan.device_cache[key] = dg
         self.dg = dg
         self.model = copy_model(model)
         self.dataset = dataset
-        features = ops.zeros_rows(dataset.graph.num_vertices, dataset.feature_dim, self.dev)
+        features = ops.zeros_rows(dg.n_local, dataset.feature_dim, self.dev)
         cls = LayerwiseEngine if layerwise else PartitionEngine
-        self.engine = cls(dg, self.model, features, dataset.labels, dataset.train_mask)
+        own = slice(None) if comm is None else dg.shard.owned
+        self.engine = cls(dg, self.model, features, np.asarray(dataset.labels)[own],
+                          np.asarray(dataset.train_mask)[own],
+                          mask_count=int(np.count_nonzero(dataset.train_mask)))
         self.upload_features(dataset)
         self.layerwise = layerwise
         self._graph = None
@@ -162,8 +178,11 @@ class TrainSession:
                 m.dropout_seed, self.layerwise)
 
     def upload_features(self, dataset: LabeledDataset) -> int:
-        """H2D of the features from pinned host memory; returns bytes moved."""
+        """H2D of the features (this device's rows) from pinned host memory;
+        returns bytes moved."""
         src = pinned_features(dataset)
+        if self.comm is not None:
+            src = src[torch.from_numpy(self.dg.shard.local_ids)]
         dst = self.engine.acts[0]
         f = src.shape[1]
         if dst.shape[1] == f:
@@ -178,8 +197,9 @@ class TrainSession:
         stays valid).  Returns the H2D bytes."""
         eng = self.engine
         moved = self.upload_features(dataset)
-        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)))
-        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)))
+        own = slice(None) if self.comm is None else self.dg.shard.owned
+        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)[own]))
+        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)[own]))
         eng.mask_count = int(np.count_nonzero(dataset.train_mask))
         self.model = copy_model(model)
         eng.wts.load(self.model)
@@ -208,6 +228,8 @@ class TrainSession:
     def run_epoch(self, epoch: int, lr: float, use_graph: bool = True) -> None:
         """Enqueue one fused epoch (loss stats land in engine.stats)."""
         eng = self.engine
+        if self.comm is not None:
+            use_graph = False   # collectives stay outside CUDA graphs
         if eng.dropout_rate > 0.0:
             eng.set_dropout(epoch)
             use_graph = False   # fresh masks every epoch
@@ -289,16 +311,28 @@ def pinned_features(dataset: LabeledDataset) -> torch.Tensor:
     return stage
 
 
+def _communicator():
+    """A Communicator when this process is one rank of a multi-rank job."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        from .distributed import Communicator
+        return Communicator()
+    return None
+
+
 def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
                 layerwise: bool = True) -> TrainSession:
     """A device session for (dataset, plan, model config), reused across
     calls: the plan upload, buffers and the captured epoch graph persist on
-    the plan (``plan.device_cache``); inputs are re-uploaded every call."""
+    the plan (``plan.device_cache``); inputs are re-uploaded every call.
+    Inside an initialised torch.distributed job with several ranks the
+    session is this rank's shard of the partitions (distributed.py)."""
+    comm = _communicator()
     key = ("session", tuple(model.dims), model.aggregation_mode, model.row_normalize,
-           model.dropout_rate, model.dropout_seed, layerwise)
+           model.dropout_rate, model.dropout_seed, layerwise, comm is not None)
     sess = plan.device_cache.get(key)
     if sess is None:
-        sess = TrainSession(dataset, plan, model, layerwise=layerwise)
+        sess = TrainSession(dataset, plan, model, layerwise=layerwise, comm=comm)
         plan.device_cache[key] = sess
     else:
         if plan.num_vertices != dataset.graph.num_vertices:

@@ -63,3 +63,14 @@ def test_sage_rejects_per_partition_observers():
     g, ds, plan, model = _setup(7, 4, 4, 3, 2, 4, 2, "sage_mean")
     with pytest.raises(NotImplementedError):
         g2.partitioned_train(ds, plan, model, 1, 0.01, grad_probe=lambda *a: None)
+
+
+def test_sage_cached_session_is_bitwise_identical():
+    # regression: padding columns of the loss gradient must stay zero across
+    # epochs of a reused session (GraphSAGE GEMMs run over padded widths)
+    g, ds, plan, model = _setup(9, 8, 6, 3, 3, 12, 4, "sage_mean")
+    a, ta, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    g2.partitioned_train(ds, plan, model, epochs=3, lr=0.05)
+    b, tb, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    assert ta == tb
+    assert all(np.array_equal(x, y) for x, y in zip(a.weight_grads, b.weight_grads))
