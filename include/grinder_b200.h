@@ -105,6 +105,20 @@ int grd_plan_export(const grd_plan* plan, int64_t* part_ptr, int32_t* perm,
                     int32_t* self_pos, int32_t* in_degree);
 void grd_plan_destroy(grd_plan* plan);
 
+/* Host-tier row movement for the structured-storage-offloading (SSO) path
+ * (hierarchy.py:549-583 charges these bytes):
+ *   gather      dst[i,:] = src[idx[i],:]     (regather of GA_p from the host cache)
+ *   scatter-add dst[idx[i],:] += src[i,:]   (host gradient write-back buffer;
+ *                                            idx duplicate-free, training.py:166-175)
+ * OpenMP over rows; row-major fp32 with leading dimensions. */
+int grd_host_gather_rows(const float* src, int64_t ld_src, const int64_t* idx,
+                         int64_t n_rows, int32_t width, float* dst,
+                         int64_t ld_dst, int32_t num_threads);
+int grd_host_scatter_add_rows(const float* src, int64_t ld_src,
+                              const int64_t* idx, int64_t n_rows,
+                              int32_t width, float* dst, int64_t ld_dst,
+                              int32_t num_threads);
+
 /* ------------------------------------------------------------------------
  * Device kernels (sm_100a).  All take `stream` = cudaStream_t.
  * --------------------------------------------------------------------- */

@@ -548,3 +548,35 @@ extern "C" int grd_plan_export(const grd_plan* plan, int64_t* part_ptr, int32_t*
 }
 
 extern "C" void grd_plan_destroy(grd_plan* plan) { delete plan; }
+
+// --------------------------------------------------------------------------
+// Host-tier row gather / scatter-add for the SSO path.
+// --------------------------------------------------------------------------
+extern "C" int grd_host_gather_rows(const float* src, int64_t ld_src, const int64_t* idx, int64_t n_rows,
+                                    int32_t width, float* dst, int64_t ld_dst, int32_t num_threads) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!src || !idx || !dst || width <= 0 || ld_src < width || ld_dst < width)
+        return fail(kErrArg, "host_gather_rows: bad arguments");
+    const int nt = threads_or_default(num_threads);
+#pragma omp parallel for num_threads(nt) schedule(static, 256)
+    for (int64_t i = 0; i < n_rows; ++i)
+        std::memcpy(dst + i * ld_dst, src + idx[i] * ld_src, sizeof(float) * static_cast<size_t>(width));
+    return 0;
+}
+
+extern "C" int grd_host_scatter_add_rows(const float* src, int64_t ld_src, const int64_t* idx, int64_t n_rows,
+                                         int32_t width, float* dst, int64_t ld_dst, int32_t num_threads) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!src || !idx || !dst || width <= 0 || ld_src < width || ld_dst < width)
+        return fail(kErrArg, "host_scatter_add_rows: bad arguments");
+    const int nt = threads_or_default(num_threads);
+#pragma omp parallel for num_threads(nt) schedule(static, 256)
+    for (int64_t i = 0; i < n_rows; ++i) {
+        float* d = dst + idx[i] * ld_dst;
+        const float* s = src + i * ld_src;
+        for (int32_t j = 0; j < width; ++j) d[j] += s[j];
+    }
+    return 0;
+}

@@ -287,6 +287,12 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
     if observed and model.kind != "gcn":
         raise NotImplementedError("per-partition observers (hierarchy, probes, snapshots, "
                                   "partition_order) are implemented for GCN layers")
+    from .hierarchy import TierSession
+    if isinstance(hierarchy, TierSession) and hierarchy.execute:
+        if use_snapshots:
+            raise NotImplementedError("the offloaded path regathers; snapshots stay in HBM only")
+        return _offloaded_train(dataset, plan, model, epochs, lr, hierarchy, grad_probe,
+                                partition_order)
     session = session_for(dataset, plan, model, layerwise=not observed)
     trained, trace = session.train(epochs, lr, hierarchy=hierarchy, use_snapshots=use_snapshots,
                                    grad_probe=grad_probe, partition_order=partition_order)
@@ -339,6 +345,28 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
             raise ValueError("plan was built for a different graph")
         sess.reset(dataset, model)
     return sess
+
+
+def _offloaded_train(dataset, plan, model, epochs, lr, hierarchy, grad_probe, partition_order):
+    """Structured storage offloading: layers live in the host tier (sso.py)."""
+    from .sso import OffloadedTrainer
+    trained = copy_model(model)
+    if epochs == 0:
+        return trained, [], hierarchy.ledger
+    trainer = OffloadedTrainer(dataset, plan, trained, hierarchy, _device())
+
+    def order_of(layer: int, phase: str) -> list[int]:
+        if partition_order is not None:
+            return list(partition_order(layer, phase))
+        return list(hierarchy.partition_order(layer, phase))
+
+    trace = []
+    for epoch in range(epochs):
+        trainer.epoch(epoch, lr, order_of, grad_probe=grad_probe, to_host=_to_host)
+        loss, acc = trainer.read_stats()
+        trace.append((epoch, loss, acc))
+    trainer.lops.wts.export(trained)
+    return trained, trace, hierarchy.ledger
 
 
 def _whole_graph_plan(dataset: LabeledDataset) -> PartitionPlan:

@@ -135,5 +135,41 @@ def main() -> None:
         print(f, (OUT / f).stat().st_size, "bytes")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--ledger" not in sys.argv:
     main()
+
+
+def ledger_cases() -> dict:
+    """Ledgers of the reference's simulate_epoch (GRINNDER) for the tier
+    manager's parity test: host capacities that keep whole layers, force
+    per-partition slabs, or force page-granular vertex reads; bypass on/off."""
+    import json
+    from grinder.hierarchy import HierarchyConfig
+    from grinder.simulate import ledger_summary, simulate_epoch
+    g = generate_kronecker(7, 6, seed=3)
+    labels = random_partition(g.num_vertices, 4, seed=1)
+    plan = build_partition_plan(g, labels, 4)
+    dims = [6, 5, 5, 3]
+    out = {"labels": labels, "graph_digest": np.array(digest(g.src_ptr, g.dst_idx))}
+    n = g.num_vertices
+    cases = {
+        "layer_lru": dict(host_capacity=3 * n * 6 * 4, bytes_per_value=4),
+        "partition_lru": dict(host_capacity=n * 6 * 4 // 2, bytes_per_value=4),
+        "vertex": dict(host_capacity=64, bytes_per_value=4, page_size=64),
+        "no_bypass": dict(host_capacity=3 * n * 6 * 8, bytes_per_value=8),
+        "tight": dict(host_capacity=n * 6 * 8 + 100, bytes_per_value=8),
+    }
+    for name, kw in cases.items():
+        bypass = name != "no_bypass"
+        from grinder.hierarchy import PolicySpec
+        pol = PolicySpec("GRINNDER", bypass_enabled=bypass)
+        led = simulate_epoch(plan, dims, pol, HierarchyConfig(**kw), epochs=2)
+        out[f"{name}/events"] = np.array(json.dumps(led.events))
+        out[f"{name}/summary"] = np.array(json.dumps(ledger_summary(led), sort_keys=True))
+        out[f"{name}/stage_table"] = np.array(json.dumps(led.stage_table(1), sort_keys=True))
+        out[f"{name}/config"] = np.array(json.dumps(kw, sort_keys=True))
+    return out
+
+
+if __name__ == "__main__" and "--ledger" in sys.argv:
+    np.savez_compressed(OUT / "ledger_cases.npz", **ledger_cases())
