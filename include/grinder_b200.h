@@ -178,7 +178,61 @@ typedef struct grd_agg_args {
     const float* add_y;            /* nullable: add_y[out_row,:] added after post-scaling,
                                       before the activation (GraphSAGE root term) */
     int64_t ld_add_y;
+    const float* edge_w;           /* nullable: per-edge, per-head weights [E, heads]
+                                      replacing src_scale (GAT attention) */
+    const int32_t* edge_w_perm;    /* nullable: weight row of edge e is edge_w_perm[e] */
+    const float* self_w;           /* self-term weights [out rows, heads] (with edge_w) */
+    int32_t heads;
+    int32_t head_ld;               /* columns per head (multiple of 4) */
 } grd_agg_args;
+
+/* GAT edge softmax (builder-defined layer).  Rows are
+ * aggregation targets (row_ptr/idx = in-edges, out_idx = vertex of a row);
+ * p_ext rows hold [P (heads x dhp) | s (heads) | t (heads)].
+ *   grd_gat_softmax:     alpha[e,h] = softmax over in(v) U {v} of
+ *                        LeakyReLU(s_u + t_v); self loop in alpha_self[v,h]
+ *   grd_gat_softmax_bwd: dalpha = gO_h[v] . P_h[u]; delta = alpha (dalpha -
+ *                        sum alpha dalpha) lrelu'(z); dt_v -> grad_ext
+ *   grd_gat_src_grad:    rows = sources over out-edges (edge_perm maps to the
+ *                        in-edge order): ds_u = sum delta (+ self) -> grad_ext */
+typedef struct grd_gat_args {
+    int64_t n_rows;
+    const int64_t* row_ptr;
+    const int32_t* idx;
+    const int32_t* out_idx;
+    const int32_t* edge_perm;
+    const float* p_ext;
+    int64_t ld_ext;
+    int32_t heads;
+    int32_t hdp;                   /* heads * dhp (<= 256 for the backward) */
+    int32_t dhp;                   /* padded per-head width, multiple of 4 */
+    float slope;                   /* LeakyReLU negative slope (0.2) */
+    float* alpha;
+    float* alpha_self;
+    const float* grad_o;           /* dL/dO [rows, hdp] (ld_go) */
+    int64_t ld_go;
+    float* dalpha;
+    float* dalpha_self;
+    float* delta;
+    float* delta_self;
+    float* grad_ext;               /* dL/dP_ext: s and t columns written here */
+    int64_t ld_gext;
+} grd_gat_args;
+int grd_gat_softmax(const grd_gat_args* args, void* stream);
+int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream);
+int grd_gat_src_grad(const grd_gat_args* args, void* stream);
+/* W_ext = [W | W a_src | W a_dst] (att = [a_src; a_dst], each heads x dhp). */
+int grd_gat_build_wext(const float* w, int64_t ldw, const float* att, int64_t d_in,
+                       int32_t heads, int32_t dh, int32_t dhp, float* wext,
+                       int64_t ld_ext, void* stream);
+/* dW, datt from dW_ext, then W -= lr dW, att -= lr datt (lr = 0: no step). */
+int grd_gat_param_grads(const float* dwext, int64_t ld_ext, float* w, int64_t ldw,
+                        float* att, int64_t d_in, int32_t heads, int32_t dh,
+                        int32_t dhp, float* dw, float* datt, float lr, void* stream);
+/* Last GAT layer: out = mean over heads (backward = 1: spread dL/dout / heads). */
+int grd_head_mean(const float* o, int64_t ldo, int64_t n_rows, int32_t heads,
+                  int32_t dh, int32_t dhp, float* out, int64_t ld_out,
+                  int32_t backward, void* stream);
 int grd_agg_sum(const grd_agg_args* args, void* stream);
 
 /* K3/K6/K7 — dense fp32 GEMM on tcgen05 tensor cores, 3xTF32 split

@@ -64,6 +64,37 @@ class GrdAggArgs(ctypes.Structure):
         ("ld_mask_ref", c_i64),
         ("add_y", c_vp),
         ("ld_add_y", c_i64),
+        ("edge_w", c_vp),
+        ("edge_w_perm", c_vp),
+        ("self_w", c_vp),
+        ("heads", c_i32),
+        ("head_ld", c_i32),
+    ]
+
+
+class GrdGatArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", c_i64),
+        ("row_ptr", c_vp),
+        ("idx", c_vp),
+        ("out_idx", c_vp),
+        ("edge_perm", c_vp),
+        ("p_ext", c_vp),
+        ("ld_ext", c_i64),
+        ("heads", c_i32),
+        ("hdp", c_i32),
+        ("dhp", c_i32),
+        ("slope", c_f32),
+        ("alpha", c_vp),
+        ("alpha_self", c_vp),
+        ("grad_o", c_vp),
+        ("ld_go", c_i64),
+        ("dalpha", c_vp),
+        ("dalpha_self", c_vp),
+        ("delta", c_vp),
+        ("delta_self", c_vp),
+        ("grad_ext", c_vp),
+        ("ld_gext", c_i64),
     ]
 
 
@@ -110,6 +141,13 @@ SIGNATURES = {
     "grd_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_agg_sum": (c_i32, [ctypes.POINTER(GrdAggArgs), c_vp]),
     "grd_gemm": (c_i32, [ctypes.POINTER(GrdGemmArgs), c_vp]),
+    "grd_gat_softmax": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_softmax_bwd": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_src_grad": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_build_wext": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp]),
+    "grd_gat_param_grads": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp,
+                                    c_vp, c_f32, c_vp]),
+    "grd_head_mean": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_i32, c_vp]),
     "grd_gemm_workspace": (c_i64, [c_i64, c_i64]),
     "grd_wgrad_workspace": (c_i64, [c_i64, c_i64, c_i64]),
     "grd_wgrad_sgd": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32,

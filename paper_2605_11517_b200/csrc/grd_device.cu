@@ -74,51 +74,76 @@ __device__ __forceinline__ void load_row(const float* row, int sub, int w4, floa
 }
 
 // acc += sum over edges e = beg + first, beg + first + stride, ... < end
-template <int LPR, int NV, int U>
+// Edge weight of chunk c: per-source scale, or (WE) the per-edge per-head
+// weight edge_w[e, head(c)] (GAT attention), e optionally permuted.
+template <int NV, bool WE>
+__device__ __forceinline__ void edge_weights(const grd_agg_args& a, int64_t e, int32_t j,
+                                             const int (&hd)[NV], float (&w)[NV]) {
+    if constexpr (WE) {
+        const int64_t eid = a.edge_w_perm ? a.edge_w_perm[e] : e;
+        const float* we = a.edge_w + eid * a.heads;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) w[c] = __ldg(we + hd[c]);
+    } else {
+        const float s = a.src_scale ? __ldg(a.src_scale + j) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) w[c] = s;
+    }
+}
+
+template <int LPR, int NV, int U, bool WE>
 __device__ __forceinline__ void agg_edges(const grd_agg_args& a, int64_t beg, int64_t end, int stride,
-                                          int sub, int w4, float4 (&acc)[NV]) {
+                                          int sub, int w4, const int (&hd)[NV], float4 (&acc)[NV]) {
     const float* __restrict__ y = a.y;
     const int32_t* __restrict__ idx = a.idx;
-    const float* __restrict__ ss = a.src_scale;
     int64_t e = beg;
     for (; e + int64_t(U - 1) * stride < end; e += int64_t(U) * stride) {
         int32_t j[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) j[u] = __ldg(idx + e + int64_t(u) * stride);
         float4 v[U][NV];
-        float s[U];
+        float s[U][NV];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            s[u] = ss ? __ldg(ss + j[u]) : 1.0f;
+            edge_weights<NV, WE>(a, e + int64_t(u) * stride, j[u], hd, s[u]);
             load_row<LPR, NV>(y + int64_t(j[u]) * a.ldy, sub, w4, v[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[u], v[u][c], acc[c]);
+            for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[u][c], v[u][c], acc[c]);
     }
     for (; e < end; e += stride) {
         const int32_t jj = __ldg(idx + e);
-        const float s = ss ? __ldg(ss + jj) : 1.0f;
+        float s[NV];
+        edge_weights<NV, WE>(a, e, jj, hd, s);
         float4 v[NV];
         load_row<LPR, NV>(y + int64_t(jj) * a.ldy, sub, w4, v);
 #pragma unroll
-        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s, v[c], acc[c]);
+        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[c], v[c], acc[c]);
     }
 }
 
 // self term, post-scale, activation, mask, store — by the LPR lanes of a group
-template <int LPR, int NV>
+template <int LPR, int NV, bool WE>
 __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg, int sub,
-                                           int w4, float4 (&acc)[NV]) {
+                                           int w4, const int (&hd)[NV], float4 (&acc)[NV]) {
     const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
     const int32_t srow = a.no_self ? -1 : (a.self_idx ? a.self_idx[r] : orow);
     if (srow >= 0) {
-        const float s = a.src_scale ? a.src_scale[srow] : 1.0f;
+        float s[NV];
+        if constexpr (WE) {
+#pragma unroll
+            for (int c = 0; c < NV; ++c) s[c] = a.self_w[int64_t(orow) * a.heads + hd[c]];
+        } else {
+            const float sc = a.src_scale ? a.src_scale[srow] : 1.0f;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) s[c] = sc;
+        }
         float4 v[NV];
         load_row<LPR, NV>(a.y + int64_t(srow) * a.ldy, sub, w4, v);
 #pragma unroll
-        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s, v[c], acc[c]);
+        for (int c = 0; c < NV; ++c) acc[c] = f4_fma(s[c], v[c], acc[c]);
     }
     const float div = static_cast<float>(a.post_div_deg == 2 ? deg : deg + 1);
     const bool do_div = a.post_div_deg == 1 || (a.post_div_deg == 2 && deg > 0);
@@ -151,7 +176,7 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
 // run chunk-major, so at any time the SMs gather one column slice of the rows
 // of the partitions currently in flight, which keeps that slice of the
 // gathered set L2-resident (the partition order of the rows is the locality).
-template <int LPR, int NV, int U>
+template <int LPR, int NV, int U, bool WE>
 __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, int64_t light_warps,
                                                       int chunk_cols) {
     constexpr int NG = kWarp / LPR;
@@ -171,16 +196,20 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, i
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const int w4 = (a.width + 3) / 4;
     float4 acc[NV];
+    int hd[NV];                           // head of each column chunk (WE)
 #pragma unroll
-    for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < NV; ++c) {
+        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        hd[c] = WE ? min((col0 + 4 * (sub + c * LPR)) / a.head_ld, a.heads - 1) : 0;
+    }
 
     if (warp < light_warps) {
         const int64_t r = warp * NG + g;
         if (r >= a.n_rows) return;
         const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
         if (a.heavy_threshold > 0 && end - beg > a.heavy_threshold) return;  // segmented
-        agg_edges<LPR, NV, U>(a, beg, end, 1, sub, w4, acc);
-        agg_finish<LPR, NV>(a, r, end - beg, sub, w4, acc);
+        agg_edges<LPR, NV, U, WE>(a, beg, end, 1, sub, w4, hd, acc);
+        agg_finish<LPR, NV, WE>(a, r, end - beg, sub, w4, hd, acc);
         return;
     }
     const int64_t s = warp - light_warps;
@@ -191,7 +220,7 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, i
     const int64_t rb = a.row_ptr[r], re = a.row_ptr[r + 1];
     const int64_t beg = rb + (s - seg0) * a.seg_len;
     const int64_t end = min(beg + int64_t(a.seg_len), re);
-    agg_edges<LPR, NV, 4>(a, beg + g, end, NG, sub, w4, acc);
+    agg_edges<LPR, NV, 4, WE>(a, beg + g, end, NG, sub, w4, hd, acc);
 #pragma unroll
     for (int off = kWarp / 2; off >= LPR; off >>= 1)
 #pragma unroll
@@ -223,21 +252,27 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, i
             if (q < w4) acc[c] = f4_add(acc[c], __ldcg(reinterpret_cast<const float4*>(part + 4 * q)));
         }
     }
-    agg_finish<LPR, NV>(a, r, re - rb, sub, w4, acc);
+    agg_finish<LPR, NV, WE>(a, r, re - rb, sub, w4, hd, acc);
     if (lane == 0) a.heavy_counter[h] = 0;
 }
 
-template <int LPR, int NV, int U>
-int launch_agg(const grd_agg_args& a, int chunk_cols, cudaStream_t st) {
+template <int LPR, int NV, int U, bool WE>
+int launch_agg_t(const grd_agg_args& a, int chunk_cols, cudaStream_t st) {
     constexpr int NG = kWarp / LPR;
     const int64_t light_warps = (a.n_rows + NG - 1) / NG;
     const int64_t warps = light_warps + a.n_segs;
     if (warps == 0) return 0;
     const int64_t blocks = (warps * kWarp + 255) / 256;
     const unsigned chunks = static_cast<unsigned>((a.width + chunk_cols - 1) / chunk_cols);
-    agg_sum_kernel<LPR, NV, U><<<dim3(static_cast<unsigned>(blocks), chunks), 256, 0, st>>>(a, light_warps,
-                                                                                           chunk_cols);
+    agg_sum_kernel<LPR, NV, U, WE><<<dim3(static_cast<unsigned>(blocks), chunks), 256, 0, st>>>(a, light_warps,
+                                                                                               chunk_cols);
     return launch_status("agg_sum");
+}
+
+template <int LPR, int NV, int U>
+int launch_agg(const grd_agg_args& a, int chunk_cols, cudaStream_t st) {
+    if (a.edge_w) return launch_agg_t<LPR, NV, U, true>(a, chunk_cols, st);
+    return launch_agg_t<LPR, NV, U, false>(a, chunk_cols, st);
 }
 
 int agg_chunk_cols(int width) {

@@ -73,10 +73,26 @@ class DeviceGraph:
         self._scales: dict[str, torch.Tensor] = {}
         self._partitions: dict[int, "DevicePartition"] = {}
         self.plan = plan
+        self.graph = graph
 
     def exchange(self, buf: torch.Tensor, width: int) -> None:
         """Fill the halo rows of ``buf`` from their owners (no-op on one device)."""
         return None
+
+    def out_to_in_perm(self) -> torch.Tensor:
+        """For every out-edge (graph CSR order) its position in the forward
+        in-CSR (GAT reads per-edge attention in the transposed pull)."""
+        if getattr(self, "_o2i", None) is None:
+            f, g = self.plan.flat, self.graph
+            n = np.int64(self.num_vertices)
+            tgt = np.repeat(f.perm.astype(np.int64), np.diff(f.in_ptr))
+            key_in = f.in_src.astype(np.int64) * n + tgt
+            order = np.argsort(key_in, kind="stable")
+            src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(g.src_ptr))
+            key_out = src * n + g.dst_idx.astype(np.int64)
+            pos = order[np.searchsorted(key_in[order], key_out)]
+            self._o2i = torch.from_numpy(pos.astype(np.int32)).to(self.device)
+        return self._o2i
 
     def local_rows(self, arr: np.ndarray) -> np.ndarray:
         """Rows of a per-vertex host array in this device's row order."""
@@ -220,15 +236,26 @@ def _degree_scale(name: str, deg: np.ndarray) -> np.ndarray:
 
 
 class _LayerCfg:
-    def __init__(self, layer: int, dims: list[int], mode: str, row_normalize: bool, last: bool):
+    def __init__(self, layer: int, dims: list[int], mode: str, row_normalize: bool, last: bool,
+                 heads: int = 1):
         self.layer = layer
         self.d_in, self.d_out = dims[layer], dims[layer + 1]
         self.transform_first = self.d_out <= self.d_in
         self.sym = mode == "symmetric_norm"
         self.sage = mode == "sage_mean"
+        self.gat = mode == "gat"
         self.rownorm = row_normalize
         self.last = last
         self.ld_in, self.ld_out = ld_of(self.d_in), ld_of(self.d_out)
+        if self.gat:
+            self.heads = heads
+            self.dh = self.d_out if last else self.d_out // heads
+            self.dhp = ld_of(self.dh)
+            if not last and self.dhp != self.dh:
+                raise ValueError("GAT hidden head width must be a multiple of 4")
+            self.hdp = heads * self.dhp
+            self.n_ext = self.hdp + 2 * heads        # [P | s | t] columns
+            self.ld_ext = ld_of(self.n_ext)
 
     # scale applied to the upstream gradient before this layer's pull (TF)
     # or after its dgrad GEMM (AF): mean -> 1/(deg+1), sym -> 1/sqrt(deg+1)
@@ -246,12 +273,65 @@ class _Weights:
         self.w = []
         self.dw = []
         self.blocks = 2 if model.kind == "sage" else 1
+        self.gat = model.kind == "gat"
+        if self.gat:
+            self._init_gat(model, device)
+            return
         for w in model.weights:
             d_in, d_out = w.shape[0], w.shape[1] // self.blocks
             t = torch.zeros((ld_of(d_in), self.blocks * ld_of(d_out)), dtype=torch.float32, device=device)
             self.w.append(t)
             self.dw.append(torch.zeros_like(t))
         self.load(model)
+
+    # GAT: W per head padded to dhp columns [ld(d_in), H*dhp]; att = [a_src; a_dst]
+    # as [2, H, dhp]; the fused transform matrix W_ext [ld(d_in), ld_ext] is
+    # rebuilt from them before every use.
+    def _init_gat(self, model, device):
+        H = model.heads
+        self.heads = H
+        self.att, self.datt, self.wext, self.dwext, self.shape = [], [], [], [], []
+        L = len(model.weights)
+        for l, wp in enumerate(model.weights):
+            d_in = wp.shape[0] - 2
+            dh = wp.shape[1] // H
+            dhp = ld_of(dh)
+            n_ext = H * dhp + 2 * H
+            self.shape.append((d_in, dh, dhp))
+            self.w.append(torch.zeros((ld_of(d_in), H * dhp), dtype=torch.float32, device=device))
+            self.dw.append(torch.zeros_like(self.w[-1]))
+            self.att.append(torch.zeros((2, H, dhp), dtype=torch.float32, device=device))
+            self.datt.append(torch.zeros_like(self.att[-1]))
+            self.wext.append(torch.zeros((ld_of(d_in), ld_of(n_ext)), dtype=torch.float32, device=device))
+            self.dwext.append(torch.zeros_like(self.wext[-1]))
+        self.load(model)
+
+    def _gat_load(self, model) -> None:
+        for l, wp in enumerate(model.weights):
+            d_in, dh, dhp = self.shape[l]
+            H = self.heads
+            w32 = np.asarray(wp, dtype=np.float32)
+            w = np.zeros((d_in, H, dhp), np.float32)
+            w[:, :, :dh] = w32[:d_in].reshape(d_in, H, dh)
+            self.w[l][:d_in].copy_(torch.from_numpy(w.reshape(d_in, H * dhp)))
+            att = np.zeros((2, H, dhp), np.float32)
+            att[:, :, :dh] = w32[d_in:].reshape(2, H, dh)
+            self.att[l].copy_(torch.from_numpy(att))
+
+    def _gat_export(self, model) -> None:
+        ws, gs = [], []
+        for l in range(len(self.w)):
+            d_in, dh, dhp = self.shape[l]
+            H = self.heads
+            for src, att, out in ((self.w[l], self.att[l], ws), (self.dw[l], self.datt[l], gs)):
+                w = src[:d_in].double().cpu().numpy().reshape(d_in, H, dhp)[:, :, :dh]
+                a = att.double().cpu().numpy()[:, :, :dh]
+                out.append(np.concatenate([w.reshape(d_in, H * dh), a.reshape(2, H * dh)], axis=0))
+        model.weights, model.weight_grads = ws, gs
+
+    def params(self) -> list[torch.Tensor]:
+        """Every trained device tensor (what an SGD step modifies)."""
+        return self.w + (self.att if self.gat else [])
 
     def _views(self, t: torch.Tensor, w: np.ndarray):
         d_in, d_out = w.shape[0], w.shape[1] // self.blocks
@@ -260,12 +340,19 @@ class _Weights:
                 for b in range(self.blocks)]
 
     def load(self, model) -> None:
+        if self.gat:
+            self._gat_load(model)
+            return
         for t, w in zip(self.w, model.weights):
             w32 = torch.from_numpy(np.asarray(w, dtype=np.float32))
             for view, cols in self._views(t, w):
                 view.copy_(w32[:, cols])
 
     def export(self, model) -> None:
+        if self.gat:
+            self._gat_export(model)
+            return
+
         def host(tensors):
             out = []
             for t, w in zip(tensors, model.weights):
@@ -288,8 +375,8 @@ class _EngineBase:
         self.L = model.num_layers
         self.mode = model.aggregation_mode
         self.model = model
-        self.cfg = [_LayerCfg(l, self.dims, self.mode, model.row_normalize, l == self.L - 1)
-                    for l in range(self.L)]
+        self.cfg = [_LayerCfg(l, self.dims, self.mode, model.row_normalize, l == self.L - 1,
+                              model.heads) for l in range(self.L)]
         self.wts = _Weights(model, dev)
         self.acts = [features] + [ops.zeros_rows(self.NL, d, dev) for d in self.dims[1:]]
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
@@ -332,10 +419,18 @@ class LayerwiseEngine(_EngineBase):
         super().__init__(dg, model, features, labels, train_mask, mask_count)
         dev = self.device
         wide = 2 * ld_of(self.maxw) if model.kind == "sage" else self.maxw
+        if model.kind == "gat":
+            if self.comm is not None:
+                raise NotImplementedError("GAT layers run on one device")
+            wide = max([self.maxw] + [c.ld_ext for c in self.cfg])
+            self._gat_buffers(dg, model)
         self.t1 = ops.zeros_rows(self.NL, wide, dev)
         self.g = ops.zeros_rows(self.NL, wide, dev)
         self.h = ops.zeros_rows(self.NL, wide, dev)
-        self.t2 = ops.zeros_rows(self.NL, self.maxw, dev) if model.kind == "sage" else None
+        if model.kind == "sage":
+            self.t2 = ops.zeros_rows(self.NL, self.maxw, dev)
+        elif model.kind != "gat":
+            self.t2 = None
         # one device: SGD fused into the weight-gradient reduction; sharded:
         # local weight gradients are all-reduced first, SGD at epoch end
         self.defer_sgd = self.comm is not None
@@ -418,12 +513,73 @@ class LayerwiseEngine(_EngineBase):
                           lr=lr)
         self.g, self.h = self.h, self.g
 
+    # ---------------------------------------------------------------- GAT --
+    def _gat_buffers(self, dg, model) -> None:
+        dev = self.device
+        H = model.heads
+        E = dg.fwd.nnz
+        self.alpha = torch.zeros(max(E * H, 1), dtype=torch.float32, device=dev)
+        self.dalpha = torch.zeros_like(self.alpha)
+        self.delta = torch.zeros_like(self.alpha)
+        self.alpha_self = torch.zeros(self.NL * H, dtype=torch.float32, device=dev)
+        self.dalpha_self = torch.zeros_like(self.alpha_self)
+        self.delta_self = torch.zeros_like(self.alpha_self)
+        self.edge_perm = dg.out_to_in_perm()
+        self.t2 = ops.zeros_rows(self.NL, max(c.hdp for c in self.cfg), dev)
+
+    def _gat_transform(self, l: int, x: torch.Tensor) -> torch.Tensor:
+        """P_ext = X [W | W a_src | W a_dst] and the attention (forward, and
+        recomputed in backward: the regather)."""
+        c, dg = self.cfg[l], self.dg
+        wt = self.wts
+        d_in, dh, dhp = wt.shape[l]
+        ops.gat_build_wext(wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.wext[l])
+        pext = self.t1[:, : c.ld_ext]
+        ops.gemm(x, wt.wext[l], pext, self.V, c.n_ext, c.d_in)
+        ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self)
+        return pext
+
+    def _forward_gat(self, l: int, x: torch.Tensor, out: torch.Tensor) -> None:
+        c, dg = self.cfg[l], self.dg
+        pext = self._gat_transform(l, x)
+        dst = self.t2[:, : c.hdp] if c.last else out
+        ops.agg_sum(dg.fwd, pext[:, : c.hdp], dst, c.hdp, edge_w=self.alpha, self_w=self.alpha_self,
+                    heads=c.heads, head_ld=c.dhp, relu=not c.last)
+        if c.last:
+            ops.head_mean(dst, self.V, c.heads, c.dh, c.dhp, out)
+
+    def _backward_gat(self, l: int, x: torch.Tensor, lr: float) -> None:
+        c, dg = self.cfg[l], self.dg
+        wt = self.wts
+        d_in, dh, dhp = wt.shape[l]
+        if c.last:
+            go = self.t2[:, : c.hdp]
+            ops.head_mean(self.g, self.V, c.heads, c.dh, c.dhp, go, backward=True)
+        else:
+            go = self.g[:, : c.hdp]                  # ReLU mask applied by the producer
+        pext = self._gat_transform(l, x)
+        gext = self.h[:, : c.ld_ext]
+        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go,
+                            self.dalpha, self.dalpha_self, self.delta, self.delta_self, gext)
+        ops.agg_sum(dg.bwd, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha, edge_w_perm=self.edge_perm,
+                    self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+        ops.gat_src_grad(dg.bwd, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
+        ops.wgrad_sgd(x, gext, wt.dwext[l], c.d_in, c.n_ext, self.V)
+        if l > 0:
+            ref, _ = self._consumer_epilogue(l - 1)
+            ops.gemm(gext, wt.wext[l], self.g, self.V, c.d_in, c.n_ext, trans_b=True, relu_ref=ref)
+        ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.dw[l],
+                            wt.datt[l], lr)
+
     def forward(self) -> None:
         for l, c in enumerate(self.cfg):
             x = self.layer_input(l)
             out = self.acts[l + 1]
             if c.sage:
                 self._forward_sage(l, x, out, relu=not c.last)
+                continue
+            if c.gat:
+                self._forward_gat(l, x, out)
                 continue
             self._forward_layer(l, x, out, relu=not c.last and not c.rownorm)
             if c.rownorm:
@@ -436,7 +592,7 @@ class LayerwiseEngine(_EngineBase):
         if c.rownorm:
             return None, None
         ref = None if c.last else self.acts[l + 1]
-        scale = self.dg.scale(c.pre_scale) if c.transform_first and not c.sage else None
+        scale = self.dg.scale(c.pre_scale) if c.transform_first and not (c.sage or c.gat) else None
         return ref, scale
 
     def loss(self) -> None:
@@ -455,6 +611,9 @@ class LayerwiseEngine(_EngineBase):
             x = self.layer_input(l)
             if c.sage:
                 self._backward_sage(l, x, lr)
+                continue
+            if c.gat:
+                self._backward_gat(l, x, lr)
                 continue
             s = dg.scale("s") if c.sym else None
             have_n = False

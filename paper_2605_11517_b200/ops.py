@@ -135,7 +135,8 @@ class AggSpec:
 
 def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
             src_scale=None, post_scale=None, post_div_deg=False, relu=False,
-            mask_ref=None, no_self=False, add_y=None) -> None:
+            mask_ref=None, no_self=False, add_y=None, edge_w=None, edge_w_perm=None,
+            self_w=None, heads=1, head_ld=4) -> None:
     """out[o] = act(post(sum_e y[idx_e] (+ y[self])) + add_y[o]); post_div_deg:
     False/0 none, True/1 divide by deg+1, 2 divide by deg (GraphSAGE mean)."""
     a = _lib.GrdAggArgs()
@@ -167,9 +168,14 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
     a.no_self = int(bool(no_self))
     a.add_y = _p(add_y)
     a.ld_add_y = _ld(add_y) if add_y is not None else 0
+    a.edge_w = _p(edge_w)
+    a.edge_w_perm = _p(edge_w_perm)
+    a.self_w = _p(self_w)
+    a.heads = int(heads)
+    a.head_ld = int(head_ld)
     R, E, w = spec.n_rows, spec.nnz, int(width)
     nbytes = 8 * (R + 1) + 4 * E + 4 * w * (E + R * (not no_self)) + 4 * w * R
-    nbytes += 4 * w * R * (add_y is not None)
+    nbytes += 4 * w * R * (add_y is not None) + 4 * int(heads) * (E + R) * (edge_w is not None)
     nbytes += 4 * R * ((spec.out_idx is not None) + (spec.self_idx is not None)
                        + (post_scale is not None))
     nbytes += 4 * (E + R) * (src_scale is not None) + 4 * w * R * (mask_ref is not None)
@@ -292,3 +298,70 @@ def softmax_xent(logits: torch.Tensor, n_rows: int, n_classes: int, labels: torc
 def loss_partials(n_rows: int, device) -> torch.Tensor:
     return torch.empty(int(_lib.lib().grd_loss_partials(int(n_rows))), dtype=torch.float64,
                        device=device)
+
+
+# ---------------------------------------------------------------- GAT ops --
+def _gat_args(spec: AggSpec, p_ext, heads, dhp, **kw):
+    a = _lib.GrdGatArgs()
+    a.n_rows = spec.n_rows
+    a.row_ptr = _p(spec.row_ptr)
+    a.idx = _p(spec.idx)
+    a.out_idx = _p(spec.out_idx)
+    a.p_ext = _p(p_ext)
+    a.ld_ext = _ld(p_ext)
+    a.heads, a.dhp, a.hdp = int(heads), int(dhp), int(heads) * int(dhp)
+    a.slope = 0.2
+    for k, v in kw.items():
+        if k.startswith("ld_"):
+            setattr(a, k, int(v))
+        else:
+            setattr(a, k, _p(v))
+    return a
+
+
+def gat_softmax(spec, p_ext, heads, dhp, alpha, alpha_self) -> None:
+    a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self)
+    E, R = spec.nnz, spec.n_rows
+    _launch("gat_softmax", 1, 3 * 4 * heads * (E + R) + 8 * (R + 1) + 4 * E + 4 * heads * (E + R),
+            8.0 * heads * (E + R),
+            lambda: _lib.check(_lib.lib().grd_gat_softmax(ctypes.byref(a), stream_ptr()), "gat_softmax"))
+
+
+def gat_softmax_bwd(spec, p_ext, heads, dhp, alpha, alpha_self, grad_o, dalpha, dalpha_self, delta,
+                    delta_self, grad_ext) -> None:
+    a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self, grad_o=grad_o,
+                  ld_go=_ld(grad_o), dalpha=dalpha, dalpha_self=dalpha_self, delta=delta,
+                  delta_self=delta_self, grad_ext=grad_ext, ld_gext=_ld(grad_ext))
+    E, R, hdp = spec.nnz, spec.n_rows, heads * dhp
+    nbytes = 4 * hdp * (E + 2 * R) + 5 * 4 * heads * (E + R) + 4 * E
+    _launch("gat_softmax_bwd", 2, nbytes, 2.0 * hdp * (E + R),
+            lambda: _lib.check(_lib.lib().grd_gat_softmax_bwd(ctypes.byref(a), stream_ptr()),
+                               "gat_softmax_bwd"))
+
+
+def gat_src_grad(spec, heads, dhp, edge_perm, delta, delta_self, grad_ext) -> None:
+    a = _gat_args(spec, grad_ext, heads, dhp, edge_perm=edge_perm, delta=delta, delta_self=delta_self,
+                  grad_ext=grad_ext, ld_gext=_ld(grad_ext))
+    E, R = spec.nnz, spec.n_rows
+    _launch("gat_src_grad", 1, 8 * E + 4 * heads * (E + 2 * R), heads * E,
+            lambda: _lib.check(_lib.lib().grd_gat_src_grad(ctypes.byref(a), stream_ptr()),
+                               "gat_src_grad"))
+
+
+def gat_build_wext(w, att, d_in, heads, dh, dhp, wext) -> None:
+    _launch("gat_params", 1, 0, 0, lambda: _lib.check(_lib.lib().grd_gat_build_wext(
+        _p(w), _ld(w), _p(att), int(d_in), int(heads), int(dh), int(dhp), _p(wext), _ld(wext),
+        stream_ptr()), "gat_build_wext"))
+
+
+def gat_param_grads(dwext, w, att, d_in, heads, dh, dhp, dw, datt, lr) -> None:
+    _launch("gat_params", 3, 0, 0, lambda: _lib.check(_lib.lib().grd_gat_param_grads(
+        _p(dwext), _ld(dwext), _p(w), _ld(w), _p(att), int(d_in), int(heads), int(dh), int(dhp),
+        _p(dw), _p(datt), float(lr), stream_ptr()), "gat_param_grads"))
+
+
+def head_mean(o, n_rows, heads, dh, dhp, out, backward=False) -> None:
+    _launch("head_mean", 1, 4 * n_rows * heads * dhp * 2, n_rows * heads * dhp,
+            lambda: _lib.check(_lib.lib().grd_head_mean(
+                _p(o), _ld(o), int(n_rows), int(heads), int(dh), int(dhp), _p(out), _ld(out),
+                int(bool(backward)), stream_ptr()), "head_mean"))

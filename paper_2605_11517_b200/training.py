@@ -215,9 +215,10 @@ class TrainSession:
         with torch.cuda.stream(side):
             # warm-up outside capture so lazily built scale arrays / heavy-row
             # scratch exist before the graph records their addresses
-            snap = [w.clone() for w in eng.wts.w]
+            params = eng.wts.params()
+            snap = [w.clone() for w in params]
             eng.epoch(lr)
-            for w, s in zip(eng.wts.w, snap):
+            for w, s in zip(params, snap):
                 w.copy_(s)
         torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
@@ -284,7 +285,7 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
         raise ValueError("plan was built for a different graph")
     observed = hierarchy is not None or use_snapshots or grad_probe is not None \
         or partition_order is not None
-    if observed and model.kind != "gcn":
+    if observed and model.kind != "gcn":  # GraphSAGE / GAT: layer-wise engine only
         raise NotImplementedError("per-partition observers (hierarchy, probes, snapshots, "
                                   "partition_order) are implemented for GCN layers")
     from .hierarchy import TierSession

@@ -74,3 +74,39 @@ def test_sage_cached_session_is_bitwise_identical():
     b, tb, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
     assert ta == tb
     assert all(np.array_equal(x, y) for x, y in zip(a.weight_grads, b.weight_grads))
+
+
+@pytest.mark.parametrize("F,H,C,L,heads", [(6, 16, 3, 3, 4), (12, 8, 5, 2, 2), (8, 32, 7, 2, 4)])
+def test_gat_matches_oracle(F, H, C, L, heads):
+    g = g2.generate_kronecker(9, 8, seed=9)
+    ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=10)
+    part = g2.switching_aware_partition(g, 4, g2.PartitionerParams(seed=11))
+    plan = g2.build_partition_plan(g, part.labels, 4)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=12, aggregation_mode="gat",
+                            heads=heads)
+    one, tr1, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    W1, grads1, ref1 = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                          model.weights, heads, 1, 0.05)
+    assert abs(tr1[0][1] - ref1[0][1]) <= TOL * abs(ref1[0][1])
+    for a, b in zip(one.weight_grads, grads1):
+        assert a.shape == b.shape and rel_l2(a, b) < TOL
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=3, lr=0.05)
+    W, _, ref = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                   model.weights, heads, 3, 0.05)
+    for (_, l, _), (_, rl, _) in zip(trace, ref):
+        assert abs(l - rl) <= TOL * abs(rl)
+    for a, b in zip(trained.weights, W):
+        assert rel_l2(a, b) < TOL
+
+
+def test_gat_hub_rows():
+    g = g2.generate_kronecker(12, 16, seed=3)
+    ds = g2.make_random_dataset(g, feature_dim=8, num_classes=4, seed=4)
+    plan = g2.build_partition_plan(g, g2.random_partition(g.num_vertices, 4, 5), 4)
+    model = g2.create_model(8, 4, num_layers=2, hidden_dim=16, seed=6, aggregation_mode="gat", heads=4)
+    one, tr, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    _, grads, ref = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                       model.weights, 4, 1, 0.05)
+    assert abs(tr[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
+    for a, b in zip(one.weight_grads, grads):
+        assert rel_l2(a, b) < TOL
