@@ -44,6 +44,18 @@ WORKLOADS["products_sage"] = dict(
          "8 switching-aware partitions",
     scale=21, deg=30, F=100, C=47, L=3, H=256, P=8, mode="sage_mean",
     cpu_sample=dict(scale=19, deg=30))
+WORKLOADS["products_gat"] = dict(
+    desc="configs[2]: 3-layer GAT (4 heads x 64 concat, mean on the last layer) on the "
+         "ogbn-products-shaped generate_kronecker(21, 30): 2,097,152 V / 62,914,560 E, "
+         "100 feats, 47 classes, 8 switching-aware partitions",
+    scale=21, deg=30, F=100, C=47, L=3, H=256, P=8, mode="gat", heads=4,
+    cpu_sample=dict(scale=16, deg=30))
+WORKLOADS["papers_gcn"] = dict(
+    desc="configs[3] shape at 1/3.3 size (HBM-resident on one B200): 3-layer GCN hidden 128, "
+         "ogbn-papers100M-shaped generate_kronecker(25, 14): 33,554,432 V / 469,762,048 E "
+         "(papers100M average degree), 128 feats, 172 classes, 16 switching-aware partitions",
+    scale=25, deg=14, F=128, C=172, L=3, H=128, P=16, mode="mean_self_loop",
+    cpu_sample=dict(scale=17, deg=14))
 DEFAULT_WORKLOAD = "products_sage"
 LR = 0.01
 SEED = 0
@@ -67,7 +79,8 @@ def build_workload(spec):
     plan = g2.build_partition_plan(g, part.labels, spec["P"])
     t_plan = time.perf_counter() - t2
     model = g2.create_model(spec["F"], spec["C"], num_layers=spec["L"], hidden_dim=spec["H"],
-                            seed=SEED + 3, aggregation_mode=spec["mode"])
+                            seed=SEED + 3, aggregation_mode=spec["mode"],
+                            heads=spec.get("heads", 4))
     prep = {"generate_s": round(t_gen, 3), "partition_s": round(t_part, 3),
             "plan_s": round(t_plan, 3), "partitioner_iterations": part.iterations}
     return g, ds, plan, model, prep
@@ -146,7 +159,7 @@ def run_ours(args, spec, rank, world, local_rank):
     import torch.distributed as dist
     import paper_2605_11517_b200 as g2
     from paper_2605_11517_b200 import ops
-    from paper_2605_11517_b200.training import TrainSession
+    from paper_2605_11517_b200.training import session_for
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -154,11 +167,9 @@ def run_ours(args, spec, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
     g, ds, plan, model, prep = build_workload(spec)
     L, E = spec["L"], g.num_edges
-    comm = None
-    if world > 1:
-        from paper_2605_11517_b200.distributed import Communicator
-        comm = Communicator()
-    sess = TrainSession(ds, plan, model, comm=comm)
+    # the session partitioned_train itself uses (cached on the plan): the
+    # e2e leg below re-binds the same device buffers instead of a second copy
+    sess = session_for(ds, plan, model)
     flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     # ---- instrumented epoch: per-kernel CUDA-event timing + launch count --
@@ -313,6 +324,10 @@ def oracle_epoch_seconds(spec, ds, plan, model, epochs=1):
         from oracle import sage_gat
         sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, ds.graph.src_ptr, ds.graph.dst_idx,
                             model.weights, epochs, LR)
+    elif spec["mode"] == "gat":
+        from oracle import sage_gat
+        sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, ds.graph.src_ptr, ds.graph.dst_idx,
+                           model.weights, model.heads, epochs, LR)
     else:
         from oracle import gcn
         gcn.train_partitioned(ds.features, ds.labels, ds.train_mask, plan.topologies, model.weights,
@@ -336,7 +351,7 @@ def cpu_sample(spec, g, ds, plan, model):
 def cpu_baseline(spec, g, ds, plan, model):
     g, ds, plan, model, what = cpu_sample(spec, g, ds, plan, model)
     secs = oracle_epoch_seconds(spec, ds, plan, model)
-    oracle = "oracle/sage_gat.py (torch float64 CPU)" if spec["mode"] == "sage_mean" else \
+    oracle = "oracle/sage_gat.py (torch float64 CPU)" if spec["mode"] in ("sage_mean", "gat") else \
         "oracle/gcn.py (float64 numpy restatement of the reference, pinned to its golden vectors)"
     return {"value": round(spec["L"] * g.num_edges / secs, 1), "unit": "edges/s",
             "cores": os.cpu_count(), "kind": "port",

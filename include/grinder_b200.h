@@ -191,19 +191,32 @@ typedef struct grd_agg_args {
  * p_ext rows hold [P (heads x dhp) | s (heads) | t (heads)].
  *   grd_gat_softmax:     alpha[e,h] = softmax over in(v) U {v} of
  *                        LeakyReLU(s_u + t_v); self loop in alpha_self[v,h]
- *   grd_gat_softmax_bwd: dalpha = gO_h[v] . P_h[u]; delta = alpha (dalpha -
- *                        sum alpha dalpha) lrelu'(z); dt_v -> grad_ext
+ *   grd_gat_softmax_bwd: delta = alpha (gO_h[v].P_h[u] - gO_h[v].O_h[v])
+ *                        lrelu'(z) per edge; dt_v = sum delta -> grad_ext
+ *                        column hdp + H + h
  *   grd_gat_src_grad:    rows = sources over out-edges (edge_perm maps to the
- *                        in-edge order): ds_u = sum delta (+ self) -> grad_ext */
+ *                        in-edge order): ds_u = sum delta (+ self) -> grad_ext
+ *                        column hdp + h
+ * Rows above heavy_threshold (<= 128) edges are processed as seg_len-edge
+ * segments by separate warps, combined in a fixed order (deterministic);
+ * the segmentation is the same as grd_agg_args'. */
 typedef struct grd_gat_args {
     int64_t n_rows;
     const int64_t* row_ptr;
     const int32_t* idx;
     const int32_t* out_idx;
     const int32_t* edge_perm;
+    int32_t heavy_threshold;       /* light rows: at most this many edges (<= 128) */
+    int32_t seg_len;               /* edges per heavy-row segment (<= 128) */
+    int64_t n_heavy;
+    const int32_t* heavy_rows;     /* [n_heavy] */
+    const int64_t* heavy_seg_ptr;  /* [n_heavy+1] */
+    const int32_t* seg_heavy;      /* [n_segs] */
+    int64_t n_segs;
+    float* seg_scratch;            /* [n_segs * 2 * heads] when n_segs > 0 */
     const float* p_ext;
     int64_t ld_ext;
-    int32_t heads;
+    int32_t heads;                 /* 1..8 */
     int32_t hdp;                   /* heads * dhp (<= 256 for the backward) */
     int32_t dhp;                   /* padded per-head width, multiple of 4 */
     float slope;                   /* LeakyReLU negative slope (0.2) */
@@ -211,8 +224,9 @@ typedef struct grd_gat_args {
     float* alpha_self;
     const float* grad_o;           /* dL/dO [rows, hdp] (ld_go) */
     int64_t ld_go;
-    float* dalpha;
-    float* dalpha_self;
+    const float* o_fwd;            /* forward aggregate O (relu(O) when grad_o is
+                                      ReLU-masked) [rows, hdp] (ld_o) */
+    int64_t ld_o;
     float* delta;
     float* delta_self;
     float* grad_ext;               /* dL/dP_ext: s and t columns written here */

@@ -79,6 +79,14 @@ class GrdGatArgs(ctypes.Structure):
         ("idx", c_vp),
         ("out_idx", c_vp),
         ("edge_perm", c_vp),
+        ("heavy_threshold", c_i32),
+        ("seg_len", c_i32),
+        ("n_heavy", c_i64),
+        ("heavy_rows", c_vp),
+        ("heavy_seg_ptr", c_vp),
+        ("seg_heavy", c_vp),
+        ("n_segs", c_i64),
+        ("seg_scratch", c_vp),
         ("p_ext", c_vp),
         ("ld_ext", c_i64),
         ("heads", c_i32),
@@ -89,8 +97,8 @@ class GrdGatArgs(ctypes.Structure):
         ("alpha_self", c_vp),
         ("grad_o", c_vp),
         ("ld_go", c_i64),
-        ("dalpha", c_vp),
-        ("dalpha_self", c_vp),
+        ("o_fwd", c_vp),
+        ("ld_o", c_i64),
         ("delta", c_vp),
         ("delta_self", c_vp),
         ("grad_ext", c_vp),

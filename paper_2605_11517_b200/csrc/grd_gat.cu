@@ -43,156 +43,312 @@ inline int launch_status(const char* what) {
     return 0;
 }
 
+// ------------------------------------------------------------- work units --
+// A CSR row is processed either whole (a "light" row: at most
+// heavy_threshold edges, plus the self loop) or, when it is heavier, as
+// seg_len-edge segments handled by separate warps (the self loop rides with
+// segment 0) whose per-head partials a second, deterministic pass combines.
+// Warp w < n_rows takes light row w (and skips it when heavy); warp
+// n_rows + s takes segment s.  This keeps hub rows of the power-law graphs
+// from serialising a whole launch behind one warp.
+struct Unit {
+    int64_t row, beg, end;   // CSR row and the edge range of this unit
+    int64_t seg;             // segment index, -1 for a light row
+    bool self;               // the unit carries the implicit self loop
+};
+
+__device__ __forceinline__ bool unit_of(const grd_gat_args& a, int64_t w, Unit& u) {
+    if (w < a.n_rows) {
+        const int64_t b = a.row_ptr[w], e = a.row_ptr[w + 1];
+        if (e - b > a.heavy_threshold) return false;
+        u = Unit{w, b, e, -1, true};
+        return true;
+    }
+    const int64_t s = w - a.n_rows;
+    if (s >= a.n_segs) return false;
+    const int64_t hr = a.seg_heavy[s];
+    const int64_t row = a.heavy_rows[hr];
+    const int64_t k = s - a.heavy_seg_ptr[hr];
+    const int64_t b = a.row_ptr[row] + k * a.seg_len;
+    const int64_t e = min(b + int64_t(a.seg_len), a.row_ptr[row + 1]);
+    u = Unit{row, b, e, s, k == 0};
+    return true;
+}
+
+__device__ __forceinline__ int32_t vertex_of(const grd_gat_args& a, int64_t row) {
+    return a.out_idx ? a.out_idx[row] : static_cast<int32_t>(row);
+}
+
+// (max, sum-of-exp) pair combine for the online softmax; empty = (-inf, 0).
+__device__ __forceinline__ void lse_merge(float& m, float& d, float m2, float d2) {
+    if (m2 == -INFINITY) return;
+    if (m == -INFINITY) {
+        m = m2;
+        d = d2;
+        return;
+    }
+    const float mm = fmaxf(m, m2);
+    d = d * expf(m - mm) + d2 * expf(m2 - mm);
+    m = mm;
+}
+
+constexpr int kItems = 5;   // ceil((128 edges + self loop) / 32) scores per lane
+
 // ---------------------------------------------------------------- forward --
-// Warp per target row; lanes stride over the row's edges (self loop last).
-// Three passes over H scalars per edge: max, sum of exp, normalised alpha.
+// Scores of source u for heads [0, HM): s_u (H values at column hdp),
+// vectorised when the head count allows (rows are 16-byte aligned).
+template <int HM>
+__device__ __forceinline__ void load_heads(const float* p, int H, float (&out)[HM]) {
+    if constexpr (HM % 4 == 0) {
+#pragma unroll
+        for (int c = 0; c < HM / 4; ++c) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+            out[4 * c] = q.x;
+            out[4 * c + 1] = q.y;
+            out[4 * c + 2] = q.z;
+            out[4 * c + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int h = 0; h < HM; ++h) out[h] = h < H ? __ldg(p + h) : 0.f;
+    }
+}
+
+// Pass 1, one warp per unit: the unit's (<= 129) scores stay in registers
+// (kItems per lane); a light row is normalised in place, a heavy segment
+// leaves its per-head (max, sum exp) in seg_scratch[seg][2H].  HM = head
+// count rounded up to 1, 2, 4 or 8 (register arrays sized to it).
+template <int HM>
 __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
     const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    if (r >= a.n_rows) return;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, w, un)) return;
     const int H = a.heads;
-    const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
-    const int32_t v = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
-    const float* sv = a.p_ext + int64_t(v) * a.ld_ext + a.hdp;     // s_v (self), then t_v
-    const int64_t n = end - beg + 1;                                // + self loop
-    float mx[kMaxHeads], sm[kMaxHeads], tv[kMaxHeads];
+    const int32_t v = vertex_of(a, un.row);
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (un.self ? 1 : 0);
+    float tv[HM], z[kItems][HM], mx[HM], sm[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) tv[h] = h < H ? a.p_ext[int64_t(v) * a.ld_ext + a.hdp + H + h] : 0.f;
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        mx[h] = -INFINITY;
+        sm[h] = 0.f;
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const int64_t i = lane + kWarp * it;
+        if (it > 0 && kWarp * it >= n) {       // warp-uniform early exit
+#pragma unroll
+            for (int h = 0; h < HM; ++h) z[it][h] = -INFINITY;
+            continue;
+        }
+        const int32_t u = i < ne ? a.idx[un.beg + i] : v;
+        float su[HM];
+        load_heads<HM>(a.p_ext + int64_t(u) * a.ld_ext + a.hdp, H, su);
+#pragma unroll
+        for (int h = 0; h < HM; ++h) {
+            z[it][h] = (i < n && h < H) ? lrelu(su[h] + tv[h], a.slope) : -INFINITY;
+            mx[h] = fmaxf(mx[h], z[it][h]);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) mx[h] = warp_max(mx[h]);
+#pragma unroll
+    for (int it = 0; it < kItems; ++it)
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H && lane + kWarp * it < n) sm[h] += expf(z[it][h] - mx[h]);
+#pragma unroll
+    for (int h = 0; h < HM; ++h) sm[h] = warp_sum(sm[h]);
+    if (un.seg >= 0) {
+        float* part = a.seg_scratch + un.seg * 2 * H;
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H && lane == h) {
+                part[h] = mx[h];
+                part[H + h] = sm[h];
+            }
+        return;
+    }
+    float inv[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const int64_t i = lane + kWarp * it;
+        if (i >= n) continue;
+        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H) dst[h] = expf(z[it][h] - mx[h]) * inv[h];
+    }
+}
+
+// Pass 2, one warp per heavy segment: merge the row's segment partials in a
+// fixed order (every warp of the row gets bit-identical statistics), then
+// normalise this segment's scores.
+__global__ void __launch_bounds__(256) gat_softmax_heavy_kernel(grd_gat_args a) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, a.n_rows + s, un)) return;
+    const int H = a.heads;
+    const int64_t hr = a.seg_heavy[s];
+    const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
+    float mx[kMaxHeads], sm[kMaxHeads];
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) {
         mx[h] = -INFINITY;
         sm[h] = 0.f;
-        tv[h] = h < H ? sv[H + h] : 0.f;
     }
-    auto src_of = [&](int64_t i) -> int32_t { return i < end - beg ? a.idx[beg + i] : v; };
-    for (int64_t i = lane; i < n; i += kWarp) {
-        const float* su = a.p_ext + int64_t(src_of(i)) * a.ld_ext + a.hdp;
+    for (int64_t j = s0 + lane; j < s1; j += kWarp) {
+        const float* part = a.seg_scratch + j * 2 * H;
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) mx[h] = fmaxf(mx[h], lrelu(su[h] + tv[h], a.slope));
+            if (h < H) lse_merge(mx[h], sm[h], part[h], part[H + h]);
     }
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) mx[h] = warp_max(mx[h]);
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, mx[h], o);
+            const float d2 = __shfl_xor_sync(0xffffffffu, sm[h], o);
+            lse_merge(mx[h], sm[h], m2, d2);
+        }
+    const int32_t v = vertex_of(a, un.row);
+    const float* tvp = a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H;
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (un.self ? 1 : 0);
     for (int64_t i = lane; i < n; i += kWarp) {
-        const float* su = a.p_ext + int64_t(src_of(i)) * a.ld_ext + a.hdp;
+        const int32_t u = i < ne ? a.idx[un.beg + i] : v;
+        const float* su = a.p_ext + int64_t(u) * a.ld_ext + a.hdp;
+        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) sm[h] += expf(lrelu(su[h] + tv[h], a.slope) - mx[h]);
-    }
-#pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) sm[h] = warp_sum(sm[h]);
-    for (int64_t i = lane; i < n; i += kWarp) {
-        const float* su = a.p_ext + int64_t(src_of(i)) * a.ld_ext + a.hdp;
-        float* dst = i < end - beg ? a.alpha + (beg + i) * H : a.alpha_self + int64_t(v) * H;
-#pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) dst[h] = expf(lrelu(su[h] + tv[h], a.slope) - mx[h]) / sm[h];
+            if (h < H) dst[h] = expf(lrelu(su[h] + tvp[h], a.slope) - mx[h]) / sm[h];
     }
 }
 
 // --------------------------------------------------------------- backward --
-// dalpha_uv,h = gO_h[v] . P_h[u] for every in-edge (and the self loop).
-// Warp per target row: gO row in registers, one neighbour row per step,
-// per-head dot products combined through shared memory.
-__global__ void __launch_bounds__(256) gat_edge_dot_kernel(grd_gat_args a) {
-    __shared__ float part[8][64];
+// One warp per unit of target v, kU in-edges in flight:
+//   dalpha_uv,h = gO_v,h . P_u,h                      (row gather of P_u)
+//   c_v,h       = sum_u alpha_uv,h dalpha_uv,h = gO_v,h . O_v,h
+//   delta_uv,h  = alpha_uv,h (dalpha_uv,h - c_v,h) lrelu'(s_u,h + t_v,h)
+//   dt_v,h      = sum_u delta_uv,h                    (column hdp + H + h)
+// c comes from the stored forward aggregate (o_fwd; with a ReLU-masked gO,
+// relu(O) gives the same dot), so every edge is independent and one pass
+// suffices.  Per-head dot products are reduced through shared memory.
+constexpr int kU = 4;
+
+template <int NV>
+__global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
+    __shared__ float part[8][kU][kWarp * NV];
+    __shared__ float cs[8][kMaxHeads];
     const int lane = threadIdx.x & (kWarp - 1);
     const int wib = threadIdx.x / kWarp;
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    if (r >= a.n_rows) return;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, w, un)) return;
     const int H = a.heads;
-    const int q4 = a.hdp / 4;               // float4 chunks per row (<= 64)
-    const int per_head = a.dhp / 4;
-    const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
-    const int32_t v = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
-    float4 g[2];
+    const int q4 = a.hdp / 4;
+    const int cph = a.dhp / 4;
+    const int32_t v = vertex_of(a, un.row);
+    float4 g[NV];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < NV; ++c) {
         const int q = lane + c * kWarp;
-        g[c] = q < q4 ? *reinterpret_cast<const float4*>(a.grad_o + int64_t(v) * a.ld_go + 4 * q)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        float d = 0.f;
+        g[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < q4) {
+            g[c] = *reinterpret_cast<const float4*>(a.grad_o + int64_t(v) * a.ld_go + 4 * q);
+            const float4 o = *reinterpret_cast<const float4*>(a.o_fwd + int64_t(v) * a.ld_o + 4 * q);
+            d = g[c].x * o.x + g[c].y * o.y + g[c].z * o.z + g[c].w * o.w;
+        }
+        part[wib][0][q] = d;
     }
-    for (int64_t i = 0; i <= end - beg; ++i) {
-        const int32_t u = i < end - beg ? a.idx[beg + i] : v;
-        const float* pu = a.p_ext + int64_t(u) * a.ld_ext;
+    __syncwarp();
+    if (lane < H) {
+        float c = 0.f;
+        for (int k = 0; k < cph; ++k) c += part[wib][0][lane * cph + k];
+        cs[wib][lane] = c;
+    }
+    __syncwarp();
+    // lane L < kU*H owns (edge L / H of the batch, head L % H)
+    const bool scal = lane < kU * H;
+    const int my_h = lane % H, my_j = lane / H;
+    const float c_my = cs[wib][my_h];
+    const float t_my = a.p_ext[int64_t(v) * a.ld_ext + a.hdp + H + my_h];
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (un.self ? 1 : 0);
+    float dt = 0.f;
+    for (int64_t i0 = 0; i0 < n; i0 += kU) {
+        float4 p[kU][NV];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int q = lane + c * kWarp;
-            float d = 0.f;
-            if (q < q4) {
-                const float4 p = __ldg(reinterpret_cast<const float4*>(pu + 4 * q));
-                d = g[c].x * p.x + g[c].y * p.y + g[c].z * p.z + g[c].w * p.w;
+        for (int j = 0; j < kU; ++j) {
+            const int64_t i = i0 + j;
+            const int32_t u = i < ne ? a.idx[un.beg + i] : v;
+            const float* pu = a.p_ext + int64_t(u) * a.ld_ext;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                const int q = lane + c * kWarp;
+                p[j][c] = (i < n && q < q4) ? __ldg(reinterpret_cast<const float4*>(pu + 4 * q))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            part[wib][q] = d;
+        }
+        const int64_t im = i0 + my_j;
+        const bool mine = scal && im < n;
+        float s_my = 0.f, al_my = 0.f;
+        if (mine) {
+            const int32_t u = im < ne ? a.idx[un.beg + im] : v;
+            s_my = a.p_ext[int64_t(u) * a.ld_ext + a.hdp + my_h];
+            al_my = im < ne ? a.alpha[(un.beg + im) * H + my_h] : a.alpha_self[int64_t(v) * H + my_h];
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+#pragma unroll
+            for (int c = 0; c < NV; ++c)
+                part[wib][j][lane + c * kWarp] = g[c].x * p[j][c].x + g[c].y * p[j][c].y +
+                                                 g[c].z * p[j][c].z + g[c].w * p[j][c].w;
+        __syncwarp();
+        if (mine) {
+            float da = 0.f;
+            for (int k = 0; k < cph; ++k) da += part[wib][my_j][my_h * cph + k];
+            const float d = al_my * (da - c_my) * lrelu_grad(s_my + t_my, a.slope);
+            if (im < ne)
+                a.delta[(un.beg + im) * H + my_h] = d;
+            else
+                a.delta_self[int64_t(v) * H + my_h] = d;
+            dt += d;
         }
         __syncwarp();
-        if (lane < H) {
-            float s = 0.f;
-            for (int k = 0; k < per_head; ++k) s += part[wib][lane * per_head + k];
-            float* dst = i < end - beg ? a.dalpha + (beg + i) * H : a.dalpha_self + int64_t(v) * H;
-            dst[lane] = s;
-        }
-        __syncwarp();
     }
-}
-
-// delta_uv,h = alpha (dalpha - sum_u' alpha dalpha) * lrelu'(z); the target
-// score gradient dt_v,h = sum_u delta_uv,h lands in column hdp+H+h of grad_ext.
-__global__ void __launch_bounds__(256) gat_softmax_bwd_kernel(grd_gat_args a) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    if (r >= a.n_rows) return;
-    const int H = a.heads;
-    const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
-    const int32_t v = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
-    const int64_t n = end - beg + 1;
-    const float* tvp = a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H;
-    float c[kMaxHeads], dt[kMaxHeads], tv[kMaxHeads];
-#pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) {
-        c[h] = 0.f;
-        dt[h] = 0.f;
-        tv[h] = h < H ? tvp[h] : 0.f;
+    part[wib][0][lane] = scal ? dt : 0.f;
+    __syncwarp();
+    if (lane < H) {
+        float t = 0.f;
+        for (int j = 0; j < kU; ++j) t += part[wib][0][j * H + lane];
+        if (un.seg < 0)
+            a.grad_ext[int64_t(v) * a.ld_gext + a.hdp + H + lane] = t;
+        else
+            a.seg_scratch[un.seg * H + lane] = t;
     }
-    for (int64_t i = lane; i < n; i += kWarp) {
-        const float* al = i < end - beg ? a.alpha + (beg + i) * H : a.alpha_self + int64_t(v) * H;
-        const float* da = i < end - beg ? a.dalpha + (beg + i) * H : a.dalpha_self + int64_t(v) * H;
-#pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) c[h] = fmaf(al[h], da[h], c[h]);
-    }
-#pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) c[h] = warp_sum(c[h]);
-    for (int64_t i = lane; i < n; i += kWarp) {
-        const bool self = i == end - beg;
-        const int32_t u = self ? v : a.idx[beg + i];
-        const float* su = a.p_ext + int64_t(u) * a.ld_ext + a.hdp;
-        const float* al = self ? a.alpha_self + int64_t(v) * H : a.alpha + (beg + i) * H;
-        const float* da = self ? a.dalpha_self + int64_t(v) * H : a.dalpha + (beg + i) * H;
-        float* de = self ? a.delta_self + int64_t(v) * H : a.delta + (beg + i) * H;
-#pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h) {
-            if (h >= H) continue;
-            const float d = al[h] * (da[h] - c[h]) * lrelu_grad(su[h] + tv[h], a.slope);
-            de[h] = d;
-            dt[h] += d;
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) dt[h] = warp_sum(dt[h]);
-    if (lane < H) a.grad_ext[int64_t(v) * a.ld_gext + a.hdp + H + lane] = dt[lane];
 }
 
 // Source score gradient ds_u,h = sum over u's out-edges of delta (edges
-// addressed through the transposed CSR's permutation) + the self loop.
+// addressed through the transposed CSR's permutation) + the self loop; one
+// warp per unit of the out-edge CSR.
 __global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a) {
     const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    if (r >= a.n_rows) return;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, w, un)) return;
     const int H = a.heads;
-    const int64_t beg = a.row_ptr[r], end = a.row_ptr[r + 1];
     float ds[kMaxHeads];
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) ds[h] = 0.f;
-    for (int64_t i = beg + lane; i < end; i += kWarp) {
+    for (int64_t i = un.beg + lane; i < un.end; i += kWarp) {
         const float* de = a.delta + int64_t(a.edge_perm[i]) * H;
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h)
@@ -200,8 +356,39 @@ __global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a) {
     }
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) ds[h] = warp_sum(ds[h]);
-    if (lane < H)
-        a.grad_ext[r * a.ld_gext + a.hdp + lane] = ds[lane] + a.delta_self[r * H + lane];
+    const int32_t r = vertex_of(a, un.row);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+        if (h >= H || lane != h) continue;
+        const float t = ds[h] + (un.self ? a.delta_self[int64_t(r) * H + h] : 0.f);
+        if (un.seg < 0)
+            a.grad_ext[int64_t(r) * a.ld_gext + a.hdp + h] = t;
+        else
+            a.seg_scratch[un.seg * H + h] = t;
+    }
+}
+
+// Heavy rows of the two backward passes: one warp per heavy row sums its
+// segments' per-head partials (fixed order) into grad_ext column col0 + h.
+__global__ void __launch_bounds__(256) gat_heavy_sum_kernel(grd_gat_args a, int col0) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t hr = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (hr >= a.n_heavy) return;
+    const int H = a.heads;
+    const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
+    float t[kMaxHeads];
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) t[h] = 0.f;
+    for (int64_t j = s0 + lane; j < s1; j += kWarp)
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h)
+            if (h < H) t[h] += a.seg_scratch[j * H + h];
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) t[h] = warp_sum(t[h]);
+    const int32_t r = vertex_of(a, a.heavy_rows[hr]);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h)
+        if (h < H && lane == h) a.grad_ext[int64_t(r) * a.ld_gext + col0 + h] = t[h];
 }
 
 // W_ext = [W | W a_src | W a_dst]  (rows d_in, thread per (row, column))
@@ -283,35 +470,68 @@ __global__ void head_mean_kernel(const float* o, int64_t ldo, int64_t n_rows, in
 unsigned warps_blocks(int64_t rows) { return static_cast<unsigned>((rows * kWarp + 255) / 256); }
 unsigned blocks(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
+unsigned unit_blocks(const grd_gat_args& a) { return warps_blocks(a.n_rows + a.n_segs); }
+
+int check_units(const grd_gat_args* a, const char* what) {
+    if (!a || a->heads < 1 || a->heads > kMaxHeads) return fail(kErrArg, "%s: heads must be 1..%d", what, kMaxHeads);
+    if (a->heavy_threshold < 0 || a->heavy_threshold > 128 || a->seg_len < 1 || a->seg_len > 128)
+        return fail(kErrArg, "%s: heavy_threshold and seg_len must be <= 128", what);
+    if (a->n_segs > 0 && (!a->heavy_rows || !a->heavy_seg_ptr || !a->seg_heavy || !a->seg_scratch))
+        return fail(kErrArg, "%s: heavy rows need their segmentation and seg_scratch", what);
+    return 0;
+}
+
 }  // namespace
 
 extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
     clear_error();
-    if (!args || args->heads < 1 || args->heads > kMaxHeads) return fail(kErrArg, "gat_softmax: bad heads");
+    if (int rc = check_units(args, "gat_softmax")) return rc;
     if (args->n_rows == 0) return 0;
-    gat_softmax_kernel<<<warps_blocks(args->n_rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(*args);
-    return launch_status("gat_softmax");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int H = args->heads;
+    if (H == 1)
+        gat_softmax_kernel<1><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    else if (H == 2)
+        gat_softmax_kernel<2><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    else if (H <= 4)
+        gat_softmax_kernel<4><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    else
+        gat_softmax_kernel<8><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    int rc = launch_status("gat_softmax");
+    if (rc || args->n_segs == 0) return rc;
+    gat_softmax_heavy_kernel<<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
+    return launch_status("gat_softmax_heavy");
 }
 
 extern "C" int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream) {
     clear_error();
-    if (!args || args->heads < 1 || args->heads > kMaxHeads || args->hdp > 256 || args->hdp % 4)
-        return fail(kErrArg, "gat_softmax_bwd: bad shape");
+    if (int rc = check_units(args, "gat_softmax_bwd")) return rc;
+    if (args->hdp > 256 || args->hdp % 4 || args->dhp % 4 || !args->grad_o || !args->o_fwd ||
+        args->ld_go % 4 || args->ld_o % 4 || args->ld_ext % 4)
+        return fail(kErrArg, "gat_softmax_bwd: hdp <= 256, 16-byte aligned rows, grad_o and o_fwd required");
     if (args->n_rows == 0) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    gat_edge_dot_kernel<<<warps_blocks(args->n_rows), 256, 0, st>>>(*args);
-    int rc = launch_status("gat_edge_dot");
-    if (rc) return rc;
-    gat_softmax_bwd_kernel<<<warps_blocks(args->n_rows), 256, 0, st>>>(*args);
-    return launch_status("gat_softmax_bwd");
+    if (args->hdp <= 128)
+        gat_edge_bwd_kernel<1><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    else
+        gat_edge_bwd_kernel<2><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    int rc = launch_status("gat_edge_bwd");
+    if (rc || args->n_heavy == 0) return rc;
+    gat_heavy_sum_kernel<<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args, args->hdp + args->heads);
+    return launch_status("gat_heavy_sum");
 }
 
 extern "C" int grd_gat_src_grad(const grd_gat_args* args, void* stream) {
     clear_error();
-    if (!args || !args->edge_perm) return fail(kErrArg, "gat_src_grad: needs edge_perm");
+    if (int rc = check_units(args, "gat_src_grad")) return rc;
+    if (!args->edge_perm) return fail(kErrArg, "gat_src_grad: needs edge_perm");
     if (args->n_rows == 0) return 0;
-    gat_src_grad_kernel<<<warps_blocks(args->n_rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(*args);
-    return launch_status("gat_src_grad");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    gat_src_grad_kernel<<<unit_blocks(*args), 256, 0, st>>>(*args);
+    int rc = launch_status("gat_src_grad");
+    if (rc || args->n_heavy == 0) return rc;
+    gat_heavy_sum_kernel<<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args, args->hdp);
+    return launch_status("gat_heavy_sum");
 }
 
 extern "C" int grd_gat_build_wext(const float* w, int64_t ldw, const float* att, int64_t d_in, int32_t heads,

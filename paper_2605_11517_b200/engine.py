@@ -519,13 +519,15 @@ class LayerwiseEngine(_EngineBase):
         H = model.heads
         E = dg.fwd.nnz
         self.alpha = torch.zeros(max(E * H, 1), dtype=torch.float32, device=dev)
-        self.dalpha = torch.zeros_like(self.alpha)
         self.delta = torch.zeros_like(self.alpha)
         self.alpha_self = torch.zeros(self.NL * H, dtype=torch.float32, device=dev)
-        self.dalpha_self = torch.zeros_like(self.alpha_self)
         self.delta_self = torch.zeros_like(self.alpha_self)
         self.edge_perm = dg.out_to_in_perm()
-        self.t2 = ops.zeros_rows(self.NL, max(c.hdp for c in self.cfg), dev)
+        # t2: the last layer's per-head aggregate O (kept for the backward's
+        # gO.O term); t3: its per-head upstream gradient
+        hdp = self.cfg[-1].hdp
+        self.t2 = ops.zeros_rows(self.NL, hdp, dev)
+        self.t3 = ops.zeros_rows(self.NL, hdp, dev)
 
     def _gat_transform(self, l: int, x: torch.Tensor) -> torch.Tensor:
         """P_ext = X [W | W a_src | W a_dst] and the attention (forward, and
@@ -553,14 +555,15 @@ class LayerwiseEngine(_EngineBase):
         wt = self.wts
         d_in, dh, dhp = wt.shape[l]
         if c.last:
-            go = self.t2[:, : c.hdp]
+            go, o_fwd = self.t3[:, : c.hdp], self.t2[:, : c.hdp]
             ops.head_mean(self.g, self.V, c.heads, c.dh, c.dhp, go, backward=True)
         else:
-            go = self.g[:, : c.hdp]                  # ReLU mask applied by the producer
+            # ReLU mask applied by the producer, so gO.relu(O) = gO.O
+            go, o_fwd = self.g[:, : c.hdp], self.acts[l + 1]
         pext = self._gat_transform(l, x)
         gext = self.h[:, : c.ld_ext]
-        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go,
-                            self.dalpha, self.dalpha_self, self.delta, self.delta_self, gext)
+        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go, o_fwd,
+                            self.delta, self.delta_self, gext)
         ops.agg_sum(dg.bwd, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha, edge_w_perm=self.edge_perm,
                     self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
         ops.gat_src_grad(dg.bwd, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)

@@ -311,6 +311,14 @@ def _gat_args(spec: AggSpec, p_ext, heads, dhp, **kw):
     a.ld_ext = _ld(p_ext)
     a.heads, a.dhp, a.hdp = int(heads), int(dhp), int(heads) * int(dhp)
     a.slope = 0.2
+    a.heavy_threshold = HEAVY_THRESHOLD
+    a.seg_len = SEGMENT_EDGES
+    a.n_heavy = spec.n_heavy
+    a.heavy_rows = _p(spec.heavy_rows)
+    a.heavy_seg_ptr = _p(spec.heavy_seg_ptr)
+    a.seg_heavy = _p(spec.seg_heavy)
+    a.n_segs = spec.n_segs
+    a.seg_scratch = _p(spec.partial(2 * int(heads)))
     for k, v in kw.items():
         if k.startswith("ld_"):
             setattr(a, k, int(v))
@@ -320,21 +328,25 @@ def _gat_args(spec: AggSpec, p_ext, heads, dhp, **kw):
 
 
 def gat_softmax(spec, p_ext, heads, dhp, alpha, alpha_self) -> None:
+    """alpha = edge softmax of LeakyReLU(s_u + t_v) over in(v) + self loop."""
     a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self)
     E, R = spec.nnz, spec.n_rows
-    _launch("gat_softmax", 1, 3 * 4 * heads * (E + R) + 8 * (R + 1) + 4 * E + 4 * heads * (E + R),
-            8.0 * heads * (E + R),
+    # idx + s_u sector per edge, t_v per row, alpha written
+    nbytes = 8 * (R + 1) + 4 * E + 4 * heads * (E + R) * 2 + 4 * heads * R
+    _launch("gat_softmax", 1 + (spec.n_segs > 0), nbytes, 8.0 * heads * (E + R),
             lambda: _lib.check(_lib.lib().grd_gat_softmax(ctypes.byref(a), stream_ptr()), "gat_softmax"))
 
 
-def gat_softmax_bwd(spec, p_ext, heads, dhp, alpha, alpha_self, grad_o, dalpha, dalpha_self, delta,
-                    delta_self, grad_ext) -> None:
+def gat_softmax_bwd(spec, p_ext, heads, dhp, alpha, alpha_self, grad_o, o_fwd, delta, delta_self,
+                    grad_ext) -> None:
+    """Per-edge score gradients delta and the target-score gradient dt."""
     a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self, grad_o=grad_o,
-                  ld_go=_ld(grad_o), dalpha=dalpha, dalpha_self=dalpha_self, delta=delta,
+                  ld_go=_ld(grad_o), o_fwd=o_fwd, ld_o=_ld(o_fwd), delta=delta,
                   delta_self=delta_self, grad_ext=grad_ext, ld_gext=_ld(grad_ext))
     E, R, hdp = spec.nnz, spec.n_rows, heads * dhp
-    nbytes = 4 * hdp * (E + 2 * R) + 5 * 4 * heads * (E + R) + 4 * E
-    _launch("gat_softmax_bwd", 2, nbytes, 2.0 * hdp * (E + R),
+    # P_u row per edge (+ self), gO and O rows per target, alpha/s read, delta written
+    nbytes = 8 * (R + 1) + 4 * E + 4 * hdp * (E + 3 * R) + 3 * 4 * heads * (E + R)
+    _launch("gat_softmax_bwd", 1 + (spec.n_heavy > 0), nbytes, 2.0 * hdp * (E + 2 * R),
             lambda: _lib.check(_lib.lib().grd_gat_softmax_bwd(ctypes.byref(a), stream_ptr()),
                                "gat_softmax_bwd"))
 
@@ -343,7 +355,7 @@ def gat_src_grad(spec, heads, dhp, edge_perm, delta, delta_self, grad_ext) -> No
     a = _gat_args(spec, grad_ext, heads, dhp, edge_perm=edge_perm, delta=delta, delta_self=delta_self,
                   grad_ext=grad_ext, ld_gext=_ld(grad_ext))
     E, R = spec.nnz, spec.n_rows
-    _launch("gat_src_grad", 1, 8 * E + 4 * heads * (E + 2 * R), heads * E,
+    _launch("gat_src_grad", 1 + (spec.n_heavy > 0), 8 * E + 4 * heads * (E + 2 * R), heads * E,
             lambda: _lib.check(_lib.lib().grd_gat_src_grad(ctypes.byref(a), stream_ptr()),
                                "gat_src_grad"))
 

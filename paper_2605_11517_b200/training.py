@@ -174,7 +174,7 @@ class TrainSession:
 
     def signature(self) -> tuple:
         m = self.model
-        return (tuple(m.dims), m.aggregation_mode, m.row_normalize, m.dropout_rate,
+        return (tuple(m.dims), m.aggregation_mode, m.heads, m.row_normalize, m.dropout_rate,
                 m.dropout_seed, self.layerwise)
 
     def upload_features(self, dataset: LabeledDataset) -> int:
@@ -335,7 +335,7 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
     Inside an initialised torch.distributed job with several ranks the
     session is this rank's shard of the partitions (distributed.py)."""
     comm = _communicator()
-    key = ("session", tuple(model.dims), model.aggregation_mode, model.row_normalize,
+    key = ("session", tuple(model.dims), model.aggregation_mode, model.heads, model.row_normalize,
            model.dropout_rate, model.dropout_seed, layerwise, comm is not None)
     sess = plan.device_cache.get(key)
     if sess is None:
