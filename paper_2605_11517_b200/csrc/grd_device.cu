@@ -177,7 +177,7 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
 // of the partitions currently in flight, which keeps that slice of the
 // gathered set L2-resident (the partition order of the rows is the locality).
 template <int LPR, int NV, int U, bool WE>
-__global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, int64_t light_warps,
+__global__ void __launch_bounds__(256, (WE && LPR == 32 && NV <= 2) ? 4 : 0) agg_sum_kernel(const grd_agg_args a_in, int64_t light_warps,
                                                       int chunk_cols) {
     constexpr int NG = kWarp / LPR;
     grd_agg_args a = a_in;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) agg_sum_kernel(const grd_agg_args a_in, i
     const int64_t rb = a.row_ptr[r], re = a.row_ptr[r + 1];
     const int64_t beg = rb + (s - seg0) * a.seg_len;
     const int64_t end = min(beg + int64_t(a.seg_len), re);
-    agg_edges<LPR, NV, 4, WE>(a, beg + g, end, NG, sub, w4, hd, acc);
+    agg_edges<LPR, NV, U, WE>(a, beg + g, end, NG, sub, w4, hd, acc);
 #pragma unroll
     for (int off = kWarp / 2; off >= LPR; off >>= 1)
 #pragma unroll
@@ -556,12 +556,14 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     if (a.n_segs > 0 && (a.width + cc - 1) / cc > kMaxAggChunks)
         return fail(kErrArg, "agg_sum: too many column chunks");
     const int w4 = (cc + 3) / 4;
+    // rows in flight per warp: 8 for the 17..32-chunk rows (measured +15% at
+    // width 100), 4 above (width 256 runs at the L2 throughput cap already)
     if (w4 <= 1) return launch_agg<1, 1, 4>(a, cc, st);
     if (w4 <= 2) return launch_agg<2, 1, 4>(a, cc, st);
     if (w4 <= 4) return launch_agg<4, 1, 4>(a, cc, st);
     if (w4 <= 8) return launch_agg<8, 1, 4>(a, cc, st);
     if (w4 <= 16) return launch_agg<16, 1, 4>(a, cc, st);
-    if (w4 <= 32) return launch_agg<32, 1, 4>(a, cc, st);
+    if (w4 <= 32) return launch_agg<32, 1, 8>(a, cc, st);
     if (w4 <= 64) return launch_agg<32, 2, 4>(a, cc, st);
     if (w4 <= 128) return launch_agg<32, 4, 2>(a, cc, st);
     return launch_agg<32, 8, 1>(a, cc, st);
