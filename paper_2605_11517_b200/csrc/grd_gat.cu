@@ -99,7 +99,7 @@ constexpr int kItems = 5;   // ceil((128 edges + self loop) / 32) scores per lan
 // vectorised when the head count allows (rows are 16-byte aligned).
 template <int HM>
 __device__ __forceinline__ void load_heads(const float* p, int H, float (&out)[HM]) {
-    if constexpr (HM % 4 == 0) {
+    if (HM % 4 == 0 && H == HM) {          // 16-byte aligned: hdp and H are multiples of 4
 #pragma unroll
         for (int c = 0; c < HM / 4; ++c) {
             const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
@@ -108,34 +108,22 @@ __device__ __forceinline__ void load_heads(const float* p, int H, float (&out)[H
             out[4 * c + 2] = q.z;
             out[4 * c + 3] = q.w;
         }
-    } else {
-#pragma unroll
-        for (int h = 0; h < HM; ++h) out[h] = h < H ? __ldg(p + h) : 0.f;
+        return;
     }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) out[h] = h < H ? __ldg(p + h) : 0.f;
 }
 
-// Pass 1, one warp per unit: the unit's (<= 129) scores stay in registers
-// (kItems per lane); a light row is normalised in place, a heavy segment
-// leaves its per-head (max, sum exp) in seg_scratch[seg][2H].  HM = head
-// count rounded up to 1, 2, 4 or 8 (register arrays sized to it).
+// Scores z = LeakyReLU(s_u + t_v) of one unit's (<= 129) items, kItems per
+// lane (item lane + 32 it), -inf where absent; all loads issued up front.
 template <int HM>
-__global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    Unit un;
-    if (!unit_of(a, w, un)) return;
+__device__ __forceinline__ void unit_scores(const grd_gat_args& a, const Unit& un, int32_t v, int lane,
+                                            float (&z)[kItems][HM]) {
     const int H = a.heads;
-    const int32_t v = vertex_of(a, un.row);
     const int64_t ne = un.end - un.beg;
     const int64_t n = ne + (un.self ? 1 : 0);
-    float tv[HM], z[kItems][HM], mx[HM], sm[HM];
-#pragma unroll
-    for (int h = 0; h < HM; ++h) tv[h] = h < H ? a.p_ext[int64_t(v) * a.ld_ext + a.hdp + H + h] : 0.f;
-#pragma unroll
-    for (int h = 0; h < HM; ++h) {
-        mx[h] = -INFINITY;
-        sm[h] = 0.f;
-    }
+    float tv[HM];
+    load_heads<HM>(a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H, H, tv);
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const int64_t i = lane + kWarp * it;
@@ -148,20 +136,55 @@ __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
         float su[HM];
         load_heads<HM>(a.p_ext + int64_t(u) * a.ld_ext + a.hdp, H, su);
 #pragma unroll
-        for (int h = 0; h < HM; ++h) {
-            z[it][h] = (i < n && h < H) ? lrelu(su[h] + tv[h], a.slope) : -INFINITY;
-            mx[h] = fmaxf(mx[h], z[it][h]);
-        }
+        for (int h = 0; h < HM; ++h) z[it][h] = (i < n && h < H) ? lrelu(su[h] + tv[h], a.slope) : -INFINITY;
     }
+}
+
+template <int HM>
+__device__ __forceinline__ void write_alpha(const grd_gat_args& a, const Unit& un, int32_t v, int lane,
+                                            const float (&z)[kItems][HM], const float (&mx)[HM],
+                                            const float (&inv)[HM]) {
+    const int H = a.heads;
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (un.self ? 1 : 0);
 #pragma unroll
-    for (int h = 0; h < HM; ++h) mx[h] = warp_max(mx[h]);
-#pragma unroll
-    for (int it = 0; it < kItems; ++it)
+    for (int it = 0; it < kItems; ++it) {
+        const int64_t i = lane + kWarp * it;
+        if (i >= n) continue;
+        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
 #pragma unroll
         for (int h = 0; h < HM; ++h)
-            if (h < H && lane + kWarp * it < n) sm[h] += expf(z[it][h] - mx[h]);
+            if (h < H) dst[h] = expf(z[it][h] - mx[h]) * inv[h];
+    }
+}
+
+// Pass 1, one warp per unit: the unit's scores stay in registers; a light
+// row is normalised in place, a heavy segment leaves its per-head (max, sum
+// exp) in seg_scratch[seg][2H].  HM = head count rounded up to 1, 2, 4 or 8
+// (register arrays sized to it).
+template <int HM>
+__global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, w, un)) return;
+    const int H = a.heads;
+    const int32_t v = vertex_of(a, un.row);
+    const int64_t n = un.end - un.beg + (un.self ? 1 : 0);
+    float z[kItems][HM], mx[HM], sm[HM];
+    unit_scores<HM>(a, un, v, lane, z);
 #pragma unroll
-    for (int h = 0; h < HM; ++h) sm[h] = warp_sum(sm[h]);
+    for (int h = 0; h < HM; ++h) {
+        mx[h] = z[0][h];
+#pragma unroll
+        for (int it = 1; it < kItems; ++it) mx[h] = fmaxf(mx[h], z[it][h]);
+        mx[h] = warp_max(mx[h]);
+        sm[h] = 0.f;
+#pragma unroll
+        for (int it = 0; it < kItems; ++it)
+            if (h < H && lane + kWarp * it < n) sm[h] += expf(z[it][h] - mx[h]);
+        sm[h] = warp_sum(sm[h]);
+    }
     if (un.seg >= 0) {
         float* part = a.seg_scratch + un.seg * 2 * H;
 #pragma unroll
@@ -175,60 +198,48 @@ __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
     float inv[HM];
 #pragma unroll
     for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-        const int64_t i = lane + kWarp * it;
-        if (i >= n) continue;
-        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
-#pragma unroll
-        for (int h = 0; h < HM; ++h)
-            if (h < H) dst[h] = expf(z[it][h] - mx[h]) * inv[h];
-    }
+    write_alpha<HM>(a, un, v, lane, z, mx, inv);
 }
 
 // Pass 2, one warp per heavy segment: merge the row's segment partials in a
 // fixed order (every warp of the row gets bit-identical statistics), then
-// normalise this segment's scores.
+// normalise this segment's scores (recomputed, loads issued up front).
+template <int HM>
 __global__ void __launch_bounds__(256) gat_softmax_heavy_kernel(grd_gat_args a) {
     const int lane = threadIdx.x & (kWarp - 1);
     const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     Unit un;
     if (!unit_of(a, a.n_rows + s, un)) return;
     const int H = a.heads;
+    const int32_t v = vertex_of(a, un.row);
+    float z[kItems][HM];
+    unit_scores<HM>(a, un, v, lane, z);
     const int64_t hr = a.seg_heavy[s];
     const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
-    float mx[kMaxHeads], sm[kMaxHeads];
+    float mx[HM], sm[HM];
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) {
+    for (int h = 0; h < HM; ++h) {
         mx[h] = -INFINITY;
         sm[h] = 0.f;
     }
     for (int64_t j = s0 + lane; j < s1; j += kWarp) {
         const float* part = a.seg_scratch + j * 2 * H;
 #pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) lse_merge(mx[h], sm[h], part[h], part[H + h]);
+        for (int h = 0; h < HM; ++h)
+            if (h < H) lse_merge(mx[h], sm[h], __ldg(part + h), __ldg(part + H + h));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h) {
+        for (int h = 0; h < HM; ++h) {
             const float m2 = __shfl_xor_sync(0xffffffffu, mx[h], o);
             const float d2 = __shfl_xor_sync(0xffffffffu, sm[h], o);
             lse_merge(mx[h], sm[h], m2, d2);
         }
-    const int32_t v = vertex_of(a, un.row);
-    const float* tvp = a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H;
-    const int64_t ne = un.end - un.beg;
-    const int64_t n = ne + (un.self ? 1 : 0);
-    for (int64_t i = lane; i < n; i += kWarp) {
-        const int32_t u = i < ne ? a.idx[un.beg + i] : v;
-        const float* su = a.p_ext + int64_t(u) * a.ld_ext + a.hdp;
-        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
+    float inv[HM];
 #pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) dst[h] = expf(lrelu(su[h] + tvp[h], a.slope) - mx[h]) / sm[h];
-    }
+    for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
+    write_alpha<HM>(a, un, v, lane, z, mx, inv);
 }
 
 // --------------------------------------------------------------- backward --
@@ -499,7 +510,14 @@ extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
         gat_softmax_kernel<8><<<unit_blocks(*args), 256, 0, st>>>(*args);
     int rc = launch_status("gat_softmax");
     if (rc || args->n_segs == 0) return rc;
-    gat_softmax_heavy_kernel<<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
+    if (H == 1)
+        gat_softmax_heavy_kernel<1><<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
+    else if (H == 2)
+        gat_softmax_heavy_kernel<2><<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
+    else if (H <= 4)
+        gat_softmax_heavy_kernel<4><<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
+    else
+        gat_softmax_heavy_kernel<8><<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
     return launch_status("gat_softmax_heavy");
 }
 
