@@ -263,6 +263,7 @@ def run_ours(args, spec, rank, world, local_rank):
                 "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None,
                 "peak_source": peak_kind, "launches_per_epoch": k["launches"],
                 "ms_per_epoch": round(k["ms"], 4),
+                "algorithmic_bytes_per_launch": int(k["bytes"] / k["launches"]),
                 "share_of_epoch": round(k["ms"] / epoch_ms_instr, 4)}
 
     traffic_file = ROOT / "profiles" / "traffic.json"
@@ -272,7 +273,10 @@ def run_ours(args, spec, rank, world, local_rank):
         tr = json.loads(traffic_file.read_text()).get(args.workload, {})
         for r in (roofline, agg_roof):
             if r["kernel"] in tr:
+                # DRAM bytes per launch (ncu) and the DRAM-side rate they imply
                 r["traffic"] = tr[r["kernel"]]
+                per_launch_s = r["ms_per_epoch"] * 1e-3 / r["launches_per_epoch"]
+                r["dram_GBs_implied"] = round(r["traffic"] / per_launch_s / 1e9, 1)
     edges_per_epoch = L * E
     value = world * edges_per_epoch / (ms_per_step * 1e-3)
     out = {

@@ -127,9 +127,10 @@ __device__ __forceinline__ void agg_edges(const grd_agg_args& a, int64_t beg, in
 // self term, post-scale, activation, mask, store — by the LPR lanes of a group
 template <int LPR, int NV, bool WE>
 __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int64_t deg, int sub,
-                                           int w4, const int (&hd)[NV], float4 (&acc)[NV]) {
+                                           int w4, const int (&hd)[NV], float4 (&acc)[NV],
+                                           bool add_self = true) {
     const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
-    const int32_t srow = a.no_self ? -1 : (a.self_idx ? a.self_idx[r] : orow);
+    const int32_t srow = (a.no_self || !add_self) ? -1 : (a.self_idx ? a.self_idx[r] : orow);
     if (srow >= 0) {
         float s[NV];
         if constexpr (WE) {
@@ -170,6 +171,47 @@ __device__ __forceinline__ void agg_finish(const grd_agg_args& a, int64_t r, int
         }
         *reinterpret_cast<float4*>(out + 4 * q) = v;
     }
+}
+
+// A heavy-row segment's partial (held by lanes < LPR) goes to seg_partial;
+// the last segment of the row to arrive sums the partials in segment order
+// and finishes the row (deterministic).
+template <int LPR, int NV, bool WE>
+__device__ __forceinline__ void heavy_tail(const grd_agg_args& a, int64_t s, int lane, int sub, int w4, int ldp,
+                                           const int (&hd)[NV], float4 (&acc)[NV]) {
+    const int32_t h = a.seg_heavy[s];
+    const int64_t r = a.heavy_rows[h];
+    const int64_t seg0 = a.heavy_seg_ptr[h], nseg = a.heavy_seg_ptr[h + 1] - seg0;
+    const int64_t rb = a.row_ptr[r], re = a.row_ptr[r + 1];
+    if (lane < LPR) {
+        float* part = a.seg_partial + s * ldp;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) __stcg(reinterpret_cast<float4*>(part + 4 * q), acc[c]);
+        }
+    }
+    __threadfence();
+    __syncwarp();
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(a.heavy_counter + h, 1);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket != nseg - 1) return;
+    // Last segment to finish: combine partials in segment order.
+    __threadfence();
+    if (lane >= LPR) return;
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t t = 0; t < nseg; ++t) {
+        const float* part = a.seg_partial + (seg0 + t) * ldp;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int q = sub + c * LPR;
+            if (q < w4) acc[c] = f4_add(acc[c], __ldcg(reinterpret_cast<const float4*>(part + 4 * q)));
+        }
+    }
+    agg_finish<LPR, NV, WE>(a, r, re - rb, sub, w4, hd, acc);
+    if (lane == 0) a.heavy_counter[h] = 0;
 }
 
 // Column chunking: blockIdx.y selects a chunk of `chunk_cols` columns.  Blocks
@@ -225,35 +267,165 @@ __global__ void __launch_bounds__(256, (WE && LPR == 32 && NV <= 2) ? 4 : 0) agg
     for (int off = kWarp / 2; off >= LPR; off >>= 1)
 #pragma unroll
         for (int c = 0; c < NV; ++c) acc[c] = f4_add(acc[c], f4_shfl_xor(acc[c], off));
-    if (lane < LPR) {
-        float* part = a.seg_partial + s * ldp;
+    heavy_tail<LPR, NV, WE>(a, s, lane, sub, w4, ldp, hd, acc);
+}
+
+// ---------------------------------------------------- K2 staged variant --
+// Rows of 17..64 float4 chunks (one row per warp, LPR = 32): each lane
+// streams its NV 16-byte chunks of the next K-1 neighbour rows into a private
+// shared-memory ring with cp.async, so loads in flight hold no registers and
+// a warp keeps K rows in flight (the register-staged kernel above keeps 4-8).
+// A row's weight (src_scale, or the GAT per-head edge weight) rides along as
+// a 4-byte cp.async into a parallel ring; each lane reads back only what it
+// copied, so wait_group alone orders the ring (no warp barrier).  The light
+// row's self term is the last item of its stream.  Source ids come from a
+// 32-edge index window loaded one window ahead.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(unsigned dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int kAsyncWarps = 4;   // warps per block of the staged kernel
+
+template <int NV, int G, int K, bool SCALED>
+__global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_agg_args a, int64_t light_warps) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int kSlots = G * K;                     // rows in flight per warp
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int wib = threadIdx.x / kWarp;
+    float4* ring = reinterpret_cast<float4*>(smem_raw) + size_t(wib) * kSlots * NV * kWarp;
+    float* wring = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw) +
+                                            size_t(kAsyncWarps) * kSlots * NV * kWarp) +
+                   size_t(wib) * kSlots * kWarp;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const int w4 = (a.width + 3) / 4;
+    const int ldp = 4 * w4;
+    int hd[NV];
 #pragma unroll
-        for (int c = 0; c < NV; ++c) {
-            const int q = sub + c * LPR;
-            if (q < w4) __stcg(reinterpret_cast<float4*>(part + 4 * q), acc[c]);
-        }
+    for (int c = 0; c < NV; ++c) hd[c] = 0;
+
+    int64_t r, beg, end, seg = -1;
+    if (warp < light_warps) {
+        r = warp;
+        if (r >= a.n_rows) return;
+        beg = a.row_ptr[r];
+        end = a.row_ptr[r + 1];
+        if (a.heavy_threshold > 0 && end - beg > a.heavy_threshold) return;  // segmented
+    } else {
+        seg = warp - light_warps;
+        if (seg >= a.n_segs) return;
+        const int32_t h = a.seg_heavy[seg];
+        r = a.heavy_rows[h];
+        beg = a.row_ptr[r] + (seg - a.heavy_seg_ptr[h]) * a.seg_len;
+        end = min(beg + int64_t(a.seg_len), a.row_ptr[r + 1]);
     }
-    __threadfence();
-    __syncwarp();
-    int ticket = 0;
-    if (lane == 0) ticket = atomicAdd(a.heavy_counter + h, 1);
-    ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    if (ticket != nseg - 1) return;
-    // Last segment to finish: combine partials in segment order.
-    __threadfence();
-    if (lane >= LPR) return;
+    const int32_t orow = a.out_idx ? a.out_idx[r] : static_cast<int32_t>(r);
+    const int32_t srow = (seg >= 0 || a.no_self) ? -1 : (a.self_idx ? a.self_idx[r] : orow);
+    const int64_t ne = end - beg;
+    const int64_t n = ne + (srow >= 0 ? 1 : 0);
+
+    auto window = [&](int64_t m) -> int32_t {
+        const int64_t i = m * kWarp + lane;
+        return i < ne ? __ldg(a.idx + beg + i) : srow;
+    };
+    // SCALED: the windows' per-source scales, gathered one window ahead too
+    auto scales = [&](int32_t j) -> float { return (SCALED && j >= 0) ? __ldg(a.src_scale + j) : 0.f; };
+    int32_t wa = window(0), wb = n > kWarp ? window(1) : 0;
+    float sa = scales(wa), sb = n > kWarp ? scales(wb) : 0.f;
+    int64_t ma = 0;
+    // group g = rows 4g .. 4g+G-1 (G divides 32: a group never straddles a window)
+    auto issue = [&](int64_t g) {
+        const int64_t p0 = g * G;
+        if (p0 < n) {
+            const int64_t m = p0 >> 5;
+            if (m != ma) {
+                wa = wb;
+                sa = sb;
+                ma = m;
+                if ((m + 1) * kWarp < n) {
+                    wb = window(m + 1);
+                    sb = scales(wb);
+                }
+            }
+            const int slot0 = static_cast<int>(g % K) * G;
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int64_t p = p0 + u;
+                const int32_t j = __shfl_sync(0xffffffffu, wa, static_cast<int>(p & (kWarp - 1)));
+                if (p < n) {
+                    const float* row = a.y + int64_t(j) * a.ldy;
+#pragma unroll
+                    for (int c = 0; c < NV; ++c) {
+                        const int q = lane + c * kWarp;
+                        if (q < w4) cp_async16(smem_u32(ring + ((slot0 + u) * NV + c) * kWarp + lane), row + 4 * q);
+                    }
+                    if constexpr (SCALED)   // after the row copies: the scale load may still be in flight
+                        wring[(slot0 + u) * kWarp + lane] =
+                            __shfl_sync(0xffffffffu, sa, static_cast<int>(p & (kWarp - 1)));
+                }
+            }
+        }
+        cp_commit();
+    };
+
+#pragma unroll
+    for (int g = 0; g < K - 1; ++g) issue(g);
+    float4 acc[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t t = 0; t < nseg; ++t) {
-        const float* part = a.seg_partial + (seg0 + t) * ldp;
+    const int64_t ng = (n + G - 1) / G;
+    for (int64_t g = 0; g < ng; ++g) {
+        issue(g + K - 1);
+        cp_wait<K - 1>();
+        const int slot0 = static_cast<int>(g % K) * G;
 #pragma unroll
-        for (int c = 0; c < NV; ++c) {
-            const int q = sub + c * LPR;
-            if (q < w4) acc[c] = f4_add(acc[c], __ldcg(reinterpret_cast<const float4*>(part + 4 * q)));
+        for (int u = 0; u < G; ++u) {
+            if (g * G + u >= n) break;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                const float w = SCALED ? wring[(slot0 + u) * kWarp + lane] : 1.f;
+                acc[c] = f4_fma(w, ring[((slot0 + u) * NV + c) * kWarp + lane], acc[c]);
+            }
         }
     }
-    agg_finish<LPR, NV, WE>(a, r, re - rb, sub, w4, hd, acc);
-    if (lane == 0) a.heavy_counter[h] = 0;
+    cp_wait<0>();
+    if (seg < 0) {
+        agg_finish<32, NV, false>(a, r, ne, lane, w4, hd, acc, /*add_self=*/false);
+        return;
+    }
+    heavy_tail<32, NV, false>(a, seg, lane, lane, w4, ldp, hd, acc);
+}
+
+template <int NV, int G, int K, bool SCALED>
+int launch_async_t(const grd_agg_args& a, cudaStream_t st) {
+    const int64_t warps = a.n_rows + a.n_segs;
+    if (warps == 0) return 0;
+    const size_t smem = size_t(kAsyncWarps) * G * K * kWarp * (16 * NV + (SCALED ? 4 : 0));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(agg_async_kernel<NV, G, K, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        attr = true;
+    }
+    const int64_t blocks = (warps + kAsyncWarps - 1) / kAsyncWarps;
+    agg_async_kernel<NV, G, K, SCALED><<<static_cast<unsigned>(blocks), kAsyncWarps * kWarp, smem, st>>>(a, a.n_rows);
+    return launch_status("agg_sum(staged)");
+}
+
+template <int NV, int G, int K>
+int launch_async(const grd_agg_args& a, cudaStream_t st) {
+    if (a.src_scale) return launch_async_t<NV, G, K, true>(a, st);
+    return launch_async_t<NV, G, K, false>(a, st);
 }
 
 template <int LPR, int NV, int U, bool WE>
@@ -556,8 +728,18 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     if (a.n_segs > 0 && (a.width + cc - 1) / cc > kMaxAggChunks)
         return fail(kErrArg, "agg_sum: too many column chunks");
     const int w4 = (cc + 3) / 4;
+    // Unweighted rows of 17..64 chunks: the cp.async-staged kernel, 2 groups
+    // of 2 rows in flight per warp (swept on B200 over 4..12 rows in flight and
+    // group sizes 1..4: -12% at widths 100 and 256 against the register-
+    // staged kernel; weighted rows stay on the latter, where staging the
+    // per-edge weights costs more than it hides).  GRD_AGG_ASYNC=0 disables.
+    const char* async_env = getenv("GRD_AGG_ASYNC");
+    const int async_on = async_env ? atoi(async_env) : 1;
+    // (scaled rows of <= 32 chunks measured faster on the register kernel)
+    if (async_on && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64)
+        return w4 <= 32 ? launch_async<1, 2, 2>(a, st) : launch_async<2, 2, 2>(a, st);
     // rows in flight per warp: 8 for the 17..32-chunk rows (measured +15% at
-    // width 100), 4 above (width 256 runs at the L2 throughput cap already)
+    // width 100), 4 above
     if (w4 <= 1) return launch_agg<1, 1, 4>(a, cc, st);
     if (w4 <= 2) return launch_agg<2, 1, 4>(a, cc, st);
     if (w4 <= 4) return launch_agg<4, 1, 4>(a, cc, st);

@@ -1,8 +1,9 @@
-"""Aggregation micro-benchmark at the products shape (2.1 M V / 62.9 M E):
-plain mean sums at widths 47/100/256 (forward in-CSR and transposed pull)
-and the GAT weighted forward / permuted pull at 4 x 64, L2 flushed between
-launches.  Prints ms and algorithmic GB/s per case."""
-import sys, json
+"""Aggregation micro-benchmark at the products shape (2.1 M V / 62.9 M E),
+the aggregation calls of the bench epochs: GCN mean (self loop), SAGE mean
+(no self, root add) forward, scaled transposed pulls, GAT weighted forward /
+permuted pull; A/B over GRD_AGG_ASYNC in one process, L2 flushed between
+launches.  Prints ms per case and variant."""
+import os, sys, json
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2605_11517_b200 as g2
@@ -15,7 +16,7 @@ dev = 'cuda'
 dg = DeviceGraph(g, plan, dev)
 n, E = g.num_vertices, g.num_edges
 flush = torch.zeros(128 * 1024 * 1024, device=dev)
-def timeit(fn, reps=10):
+def timeit(fn, reps=8):
     fn(); torch.cuda.synchronize()
     t = 0.0
     for _ in range(reps):
@@ -24,22 +25,20 @@ def timeit(fn, reps=10):
         s.record(); fn(); e.record(); torch.cuda.synchronize()
         t += s.elapsed_time(e)
     return t / reps
+variants = sys.argv[1:] or ["0", "1"]
 res = {}
-for w in (47, 100, 256):
+inv_deg = dg.scale("inv_deg")
+for w in (100, 256):
     y = torch.randn(n, ops.ld_of(w), device=dev); out = ops.zeros_rows(n, w, dev)
-    for name, spec, kw in (("fwd", dg.fwd, dict(post_div_deg=True)), ("pull", dg.bwd, {})):
-        ms = timeit(lambda: ops.agg_sum(spec, y, out, w, **kw))
-        gb = (8 * (n + 1) + 4 * E + 4 * w * (E + n) + 4 * w * n) / 1e9
-        res[f"mean_{name}_{w}"] = dict(ms=round(ms, 3), GBs=round(gb / ms * 1e3, 1))
-H, dhp = 4, 64
-hdp = H * dhp
-y = torch.randn(n, hdp, device=dev); out = ops.zeros_rows(n, hdp, dev)
-alpha = torch.rand(E * H, device=dev); aself = torch.rand(n * H, device=dev)
-perm = dg.out_to_in_perm()
-ms = timeit(lambda: ops.agg_sum(dg.fwd, y, out, hdp, edge_w=alpha, self_w=aself, heads=H, head_ld=dhp))
-gb = (8 * (n + 1) + 4 * E + 4 * hdp * (E + 2 * n) + 16 * (E + n)) / 1e9
-res["gat_fwd_256"] = dict(ms=round(ms, 3), GBs=round(gb / ms * 1e3, 1))
-ms = timeit(lambda: ops.agg_sum(dg.bwd, y, out, hdp, edge_w=alpha, edge_w_perm=perm, self_w=aself, heads=H,
-                                head_ld=dhp))
-res["gat_pull_256"] = dict(ms=round(ms, 3), GBs=round((gb + 4 * E) / ms * 1e3, 1))
+    addy = torch.randn(n, ops.ld_of(w), device=dev)
+    cases = {
+        "gcn_fwd": (dg.fwd, dict(post_div_deg=True)),
+        "sage_fwd": (dg.fwd, dict(post_div_deg=2, no_self=True, add_y=addy)),
+        "sage_pull_scaled": (dg.bwd, dict(src_scale=inv_deg, no_self=True)),
+        "gcn_pull": (dg.bwd, {}),
+    }
+    for name, (spec, kw) in cases.items():
+        for v in variants:
+            os.environ["GRD_AGG_ASYNC"] = v
+            res[f"{name}_{w}_v{v}"] = round(timeit(lambda: ops.agg_sum(spec, y, out, w, **kw)), 3)
 print(json.dumps(res))
