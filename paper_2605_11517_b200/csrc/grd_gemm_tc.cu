@@ -364,15 +364,30 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const int64_t m0 = (r / nt) * kBM, n0 = (r % nt) * bn;
             const int acc = static_cast<int>(i & 1);
             const bool has_k = kblocks_of(z) > 0;
-            if (has_k) {
-                mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-            }
             const int64_t row = m0 + q * 32 + lane;
             const bool row_ok = row < p.m;
             const float rs = (row_ok && p.row_scale) ? p.row_scale[row] : 1.0f;
             const int64_t n_pad = (p.n + 3) / 4 * 4;
             for (int c0 = 0; c0 < bn; c0 += 32) {
+                // epilogue operands of this chunk first (independent loads in
+                // flight while the accumulator is waited for / read from TMEM)
+                const bool live = row_ok && n0 + c0 < n_pad && !p.partial;
+                float* crow = p.c + row * p.ldc + n0 + c0;
+                float4 o[8], e[8];
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const int64_t n = n0 + c0 + 4 * j4;
+                    const bool ok = live && n < n_pad;
+                    o[j4] = (ok && p.accumulate) ? *reinterpret_cast<const float4*>(crow + 4 * j4)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                    e[j4] = (ok && p.relu_ref)
+                                ? __ldg(reinterpret_cast<const float4*>(p.relu_ref + row * p.ld_relu_ref + n))
+                                : make_float4(1.f, 1.f, 1.f, 1.f);
+                }
+                if (has_k && c0 == 0) {
+                    mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
                 float v[32];
                 if (has_k) {
                     tmem_ld32(tmem + lane_base + static_cast<uint32_t>(acc * bn + c0), v);
@@ -388,28 +403,23 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         if (n0 + c0 + j < n_pad) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     continue;
                 }
-                float* crow = p.c + row * p.ldc + n0 + c0;
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
                     const int64_t n = n0 + c0 + j;
                     if (n >= n_pad) continue;
                     float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    if (p.accumulate) {
-                        const float4 o = *reinterpret_cast<const float4*>(crow + j);
-                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
-                    }
+                    const float4 oo = o[j / 4];
+                    x.x += oo.x; x.y += oo.y; x.z += oo.z; x.w += oo.w;
                     if (p.row_scale) { x.x *= rs; x.y *= rs; x.z *= rs; x.w *= rs; }
                     if (p.elem_mul) {
-                        const float4 e = *reinterpret_cast<const float4*>(p.elem_mul + row * p.ld_elem_mul + n);
-                        x.x *= e.x; x.y *= e.y; x.z *= e.z; x.w *= e.w;
+                        const float4 m = *reinterpret_cast<const float4*>(p.elem_mul + row * p.ld_elem_mul + n);
+                        x.x *= m.x; x.y *= m.y; x.z *= m.z; x.w *= m.w;
                     }
-                    if (p.relu_ref) {
-                        const float4 e = *reinterpret_cast<const float4*>(p.relu_ref + row * p.ld_relu_ref + n);
-                        if (!(e.x > 0.f)) x.x = 0.f;
-                        if (!(e.y > 0.f)) x.y = 0.f;
-                        if (!(e.z > 0.f)) x.z = 0.f;
-                        if (!(e.w > 0.f)) x.w = 0.f;
-                    }
+                    const float4 ee = e[j / 4];
+                    if (!(ee.x > 0.f)) x.x = 0.f;
+                    if (!(ee.y > 0.f)) x.y = 0.f;
+                    if (!(ee.z > 0.f)) x.z = 0.f;
+                    if (!(ee.w > 0.f)) x.w = 0.f;
                     if (p.relu_out) {
                         x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
                     }
