@@ -38,3 +38,15 @@ def test_abi_version_and_error_slot():
 def test_library_is_sm100a():
     data = _lib.LIB_PATH.read_bytes()
     assert b"sm_100a" in data
+
+
+def test_integration_doc_struct_matches_the_abi():
+    """INTEGRATION.md's reference-side ctypes binding lists GrdAggArgs field
+    for field (a stale copy would make the library read past the struct)."""
+    import re
+    from pathlib import Path
+    from paper_2605_11517_b200 import _lib
+    doc = (Path(__file__).resolve().parents[1] / "INTEGRATION.md").read_text()
+    body = doc[doc.index("class GrdAggArgs"):doc.index("def aggregate_mean")]
+    names = re.findall(r'\("(\w+)", ctypes\.c_', body)
+    assert names == [f[0] for f in _lib.GrdAggArgs._fields_]
