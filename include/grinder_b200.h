@@ -111,6 +111,11 @@ void grd_plan_destroy(grd_plan* plan);
  *   scatter-add dst[idx[i],:] += src[i,:]   (host gradient write-back buffer;
  *                                            idx duplicate-free, training.py:166-175)
  * OpenMP over rows; row-major fp32 with leading dimensions. */
+/* Stable CSR transpose (counting sort): col_ptr[n_cols+1], col_rows[nnz] =
+ * for each column the referencing rows in ascending order (the edge order of
+ * np.add.at in a partition's transposed aggregation, training.py:141). */
+int grd_csr_transpose(int64_t n_rows, const int64_t* row_ptr, const int32_t* idx,
+                      int64_t n_cols, int64_t* col_ptr, int32_t* col_rows);
 int grd_host_gather_rows(const float* src, int64_t ld_src, const int64_t* idx,
                          int64_t n_rows, int32_t width, float* dst,
                          int64_t ld_dst, int32_t num_threads);

@@ -550,6 +550,31 @@ extern "C" int grd_plan_export(const grd_plan* plan, int64_t* part_ptr, int32_t*
 extern "C" void grd_plan_destroy(grd_plan* plan) { delete plan; }
 
 // --------------------------------------------------------------------------
+// Stable CSR transpose (counting sort): for every column c, the rows that
+// reference it in ascending row order -- the order np.argsort(idx, "stable")
+// yields, i.e. np.add.at's edge order of a partition's transposed
+// aggregation (training.py:141).
+// --------------------------------------------------------------------------
+extern "C" int grd_csr_transpose(int64_t n_rows, const int64_t* row_ptr, const int32_t* idx, int64_t n_cols,
+                                 int64_t* col_ptr, int32_t* col_rows) {
+    clear_error();
+    if (n_rows < 0 || n_cols < 0 || !row_ptr || !col_ptr || (row_ptr[n_rows] > 0 && (!idx || !col_rows)))
+        return fail(kErrArg, "csr_transpose: bad arguments");
+    const int64_t nnz = row_ptr[n_rows];
+    std::vector<int64_t> fill(static_cast<size_t>(n_cols) + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) {
+        const int32_t c = idx[e];
+        if (c < 0 || c >= n_cols) return fail(kErrArg, "csr_transpose: column %d out of range", c);
+        ++fill[static_cast<size_t>(c) + 1];
+    }
+    for (int64_t c = 0; c < n_cols; ++c) fill[c + 1] += fill[c];
+    std::copy(fill.begin(), fill.end(), col_ptr);
+    for (int64_t r = 0; r < n_rows; ++r)
+        for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) col_rows[fill[idx[e]]++] = static_cast<int32_t>(r);
+    return 0;
+}
+
+// --------------------------------------------------------------------------
 // Host-tier row gather / scatter-add for the SSO path.
 // --------------------------------------------------------------------------
 extern "C" int grd_host_gather_rows(const float* src, int64_t ld_src, const int64_t* idx, int64_t n_rows,

@@ -33,7 +33,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import ops
+from . import _lib, ops
 from .ops import AggSpec, ld_of
 
 __all__ = ["DeviceGraph", "DevicePartition", "LayerOps", "LayerwiseEngine", "PartitionEngine",
@@ -174,7 +174,7 @@ class DevicePartition:
         self.dev = device
         self.num_targets = int(len(targets))
         self.num_gather = int(len(gather_map))
-        tgt_ptr = np.asarray(tgt_ptr, dtype=np.int64)
+        tgt_ptr = np.ascontiguousarray(tgt_ptr, dtype=np.int64)
         src_pos = np.asarray(src_pos, dtype=np.int64)
         self_pos = np.asarray(self_pos, dtype=np.int64)
         self.targets = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.int32)).to(device)
@@ -182,13 +182,15 @@ class DevicePartition:
         self.fwd = AggSpec.build(tgt_ptr, src_pos, device, self_idx=self_pos)
         # Transposed local aggregation: for gather row g, its targets in
         # ascending order (np.add.at's edge order, training.py:141), self last.
-        local_t = np.repeat(np.arange(self.num_targets, dtype=np.int64), np.diff(tgt_ptr))
-        order = np.argsort(src_pos, kind="stable")
-        csc_ptr = np.zeros(self.num_gather + 1, dtype=np.int64)
-        np.cumsum(np.bincount(src_pos, minlength=self.num_gather), out=csc_ptr[1:])
+        csc_ptr = np.empty(self.num_gather + 1, dtype=np.int64)
+        csc_rows = np.empty(src_pos.size, dtype=np.int32)
+        src32 = np.ascontiguousarray(src_pos, dtype=np.int32)
+        _lib.check(_lib.lib().grd_csr_transpose(self.num_targets, tgt_ptr.ctypes.data, src32.ctypes.data,
+                                                self.num_gather, csc_ptr.ctypes.data, csc_rows.ctypes.data),
+                   "csr_transpose")
         self_t = np.full(self.num_gather, -1, dtype=np.int32)
         self_t[self_pos] = np.arange(self.num_targets, dtype=np.int32)
-        self.bwd = AggSpec.build(csc_ptr, local_t[order], device, self_idx=self_t)
+        self.bwd = AggSpec.build(csc_ptr, csc_rows, device, self_idx=self_t)
         self._deg = {"targets": np.asarray(target_indeg, dtype=np.float64),
                      "gather": np.asarray(gather_indeg, dtype=np.float64)}
         self._scales: dict = {}

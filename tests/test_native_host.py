@@ -134,3 +134,28 @@ def test_plan_kat_and_edge_cases():
     p3 = build_partition_plan(g3, np.zeros(g3.num_vertices, dtype=np.int32), 1)
     np.testing.assert_array_equal(p3.gather_maps[0], np.arange(g3.num_vertices))
     assert p3.topologies[0].num_edges == g3.num_edges
+
+
+def test_csr_transpose_is_the_stable_argsort():
+    """grd_csr_transpose == the transposed edge order np.argsort(kind="stable")
+    gives (np.add.at's order in a partition's backward, training.py:141)."""
+    import ctypes
+    from paper_2605_11517_b200 import _lib
+    rng = np.random.default_rng(5)
+    for n_rows, n_cols, nnz in ((0, 3, 0), (7, 1, 20), (500, 97, 4000), (50, 1000, 300)):
+        deg = np.bincount(rng.integers(0, max(n_rows, 1), nnz), minlength=n_rows)[:n_rows] if n_rows else []
+        ptr = np.zeros(n_rows + 1, dtype=np.int64)
+        np.cumsum(deg, out=ptr[1:])
+        idx = rng.integers(0, n_cols, int(ptr[-1])).astype(np.int32)
+        col_ptr = np.empty(n_cols + 1, dtype=np.int64)
+        rows = np.empty(idx.size, dtype=np.int32)
+        assert _lib.lib().grd_csr_transpose(n_rows, ptr.ctypes.data, idx.ctypes.data, n_cols,
+                                            col_ptr.ctypes.data, rows.ctypes.data) == 0
+        local = np.repeat(np.arange(n_rows), np.diff(ptr))
+        want = local[np.argsort(idx, kind="stable")]
+        assert np.array_equal(rows, want)
+        assert np.array_equal(np.diff(col_ptr), np.bincount(idx, minlength=n_cols))
+    bad = np.array([0, 1], dtype=np.int64)
+    assert _lib.lib().grd_csr_transpose(1, bad.ctypes.data, np.array([5], np.int32).ctypes.data, 2,
+                                        np.empty(3, np.int64).ctypes.data,
+                                        np.empty(1, np.int32).ctypes.data) < 0
