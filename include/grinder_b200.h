@@ -116,6 +116,14 @@ void grd_plan_destroy(grd_plan* plan);
  * np.add.at in a partition's transposed aggregation, training.py:141). */
 int grd_csr_transpose(int64_t n_rows, const int64_t* row_ptr, const int32_t* idx,
                       int64_t n_cols, int64_t* col_ptr, int32_t* col_rows);
+/* Row-set equality: *equal_out = 1 iff sorted(row r of A) == row r of B
+ * for every r (B rows ascending).  With B = grd_csr_transpose(A) this tests
+ * that the graph is symmetric (the reference's generators are,
+ * graph.py:158-209), so the streaming engine keeps one CSR in HBM for both
+ * aggregation directions. */
+int grd_csr_same_rows(int64_t n_rows, const int64_t* ptr_a, const int32_t* idx_a,
+                      const int64_t* ptr_b, const int32_t* idx_b,
+                      int32_t num_threads, int32_t* equal_out);
 int grd_host_gather_rows(const float* src, int64_t ld_src, const int64_t* idx,
                          int64_t n_rows, int32_t width, float* dst,
                          int64_t ld_dst, int32_t num_threads);

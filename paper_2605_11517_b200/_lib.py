@@ -144,6 +144,7 @@ SIGNATURES = {
     "grd_plan_export": (c_i32, [c_vp] + [c_vp] * 9),
     "grd_plan_destroy": (None, [c_vp]),
     "grd_csr_transpose": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "grd_csr_same_rows": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "grd_host_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32]),
     "grd_host_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32]),
     "grd_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),

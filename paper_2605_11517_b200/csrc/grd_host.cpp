@@ -574,6 +574,37 @@ extern "C" int grd_csr_transpose(int64_t n_rows, const int64_t* row_ptr, const i
     return 0;
 }
 
+// Row-set equality of two CSRs with the same row count: row r of A, sorted,
+// equals row r of B (B's rows ascending, e.g. a grd_csr_transpose result).
+// A graph whose transpose has the same rows is symmetric, so one CSR serves
+// both the forward in-edge aggregation and the transposed pull.
+extern "C" int grd_csr_same_rows(int64_t n_rows, const int64_t* ptr_a, const int32_t* idx_a,
+                                 const int64_t* ptr_b, const int32_t* idx_b, int32_t num_threads,
+                                 int32_t* equal_out) {
+    clear_error();
+    if (n_rows < 0 || !ptr_a || !ptr_b || !equal_out) return fail(kErrArg, "csr_same_rows: bad arguments");
+    *equal_out = 0;
+    if (ptr_a[n_rows] != ptr_b[n_rows]) return 0;
+    for (int64_t r = 0; r <= n_rows; ++r)
+        if (ptr_a[r] != ptr_b[r]) return 0;
+    const int nt = threads_or_default(num_threads);
+    int64_t bad = 0;
+#pragma omp parallel num_threads(nt) reduction(+ : bad)
+    {
+        std::vector<int32_t> row;
+#pragma omp for schedule(dynamic, 8192)
+        for (int64_t r = 0; r < n_rows; ++r) {
+            if (bad) continue;
+            const int64_t b = ptr_a[r], e = ptr_a[r + 1];
+            row.assign(idx_a + b, idx_a + e);
+            std::sort(row.begin(), row.end());
+            if (!std::equal(row.begin(), row.end(), idx_b + b)) ++bad;
+        }
+    }
+    *equal_out = bad == 0 ? 1 : 0;
+    return 0;
+}
+
 // --------------------------------------------------------------------------
 // Host-tier row gather / scatter-add for the SSO path.
 // --------------------------------------------------------------------------

@@ -1,0 +1,573 @@
+"""Layer-streaming engine: the partition-wise GCN epoch for graphs whose
+layers do not all fit in HBM (BASELINE configs[3], ogbn-papers100M-shaped:
+134 M vertices x 128 features = 68.7 GB per fp32 layer, against 180 GB of
+HBM per B200).
+
+The HBM-resident engine (engine.LayerwiseEngine) keeps every layer, its
+gradient and three scratch layers in HBM.  Here HBM holds only what the
+aggregation must gather at random — the whole graph (one CSR when the graph
+is symmetric) and TWO whole-height layer buffers — and everything that is
+only ever read or written row-sequentially streams through HBM in row
+chunks:
+
+* the features X stay in the host tier (the dataset's own fp32 array,
+  page-locked in place) and are streamed H2D in row chunks on a copy stream,
+  double-buffered against the chunk GEMMs, wherever a layer needs them
+  (forward transform, the layer-1 regather, the layer-0 weight gradient);
+* the hidden layer A_1 is *regathered* in backward — recomputed from the
+  streamed X as act(A_hat (X W_0)) chunk by chunk — instead of being kept
+  (the reference's regather-based backward, training.py:113-114, applied
+  to the one layer that does not fit); deeper hidden layers (L > 3) go to
+  pinned host memory at forward time and stream back;
+* the last layer, the loss and the last layer's backward are ONE chunked
+  pass (aggregate, transform, softmax-CE, weight gradient, input gradient),
+  so the logits and their gradient are never materialised whole.
+
+The association per layer is the LayerwiseEngine's (transform-first when
+d_out <= d_in: aggregation at the narrow width and no forward recompute);
+every kernel is the same sm_100a kernel with the same epilogue fusions, so
+results equal the resident engine's up to fp32 summation order (split-K
+chunks of the weight gradients).  Chunks are contiguous vertex ranges;
+aggregation over a chunk is a view of the whole CSR (row-pointer slice,
+shared edge array, global self rows), so nothing is copied per chunk.
+
+Supported: GCN layers (mean_self_loop / symmetric_norm) without row
+normalisation or dropout, L >= 2, hidden layers transform-first
+(d_{l+1} <= d_l for l < L-1); the last layer either way.
+"""
+
+from __future__ import annotations
+
+import os
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .engine import _degree_scale, _LayerCfg, _Weights
+from .ops import HEAVY_THRESHOLD, SEGMENT_EDGES, AggSpec, ld_of
+
+__all__ = ["StreamGraph", "StreamingEngine", "streaming_supported", "register_host"]
+
+
+def streaming_supported(model) -> str | None:
+    """None if the streaming engine can train ``model``, else the reason."""
+    if model.kind != "gcn":
+        return "the streaming engine trains GCN layers"
+    if model.row_normalize or model.dropout_rate:
+        return "the streaming engine trains without row normalisation / dropout"
+    dims = model.dims
+    L = len(dims) - 1
+    if L < 2:
+        return "the streaming engine needs at least two layers"
+    if any(dims[l + 1] > dims[l] for l in range(L - 1)):
+        return "hidden layers must be transform-first (d_out <= d_in)"
+    return None
+
+
+_REGISTERED: dict[int, int] = {}
+
+
+def _unregister(ptr: int) -> None:
+    if _REGISTERED.pop(ptr, None) is not None:
+        torch._C._cudart.cudaHostUnregister(ptr)
+
+
+def register_host(t: torch.Tensor, owner=None) -> torch.Tensor:
+    """Page-lock a CPU tensor's memory in place (cudaHostRegister), so chunk
+    copies from it are true async DMA without a staging copy.  The
+    registration is dropped when ``owner`` (the numpy array that owns the
+    memory) is collected, before its memory is freed."""
+    ptr, nbytes = t.data_ptr(), t.numel() * t.element_size()
+    if ptr in _REGISTERED and _REGISTERED[ptr] >= nbytes:
+        return t
+    if t.is_pinned():
+        return t
+    if owner is None:
+        raise ValueError("register_host needs the owner of the memory")
+    rc = torch._C._cudart.cudaHostRegister(ptr, nbytes, 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister of {nbytes} bytes failed ({int(rc)})")
+    _REGISTERED[ptr] = nbytes
+    weakref.finalize(owner, _unregister, ptr)
+    return t
+
+
+def _chunk_ranges(n: int, rows: int) -> list[tuple[int, int]]:
+    return [(r0, min(r0 + rows, n)) for r0 in range(0, n, rows)]
+
+
+def _chunk_spec(parent: AggSpec, host_ptr: np.ndarray, r0: int, r1: int,
+                self_ids: torch.Tensor) -> AggSpec:
+    """Rows [r0, r1) of ``parent`` as a spec of their own: a view of the
+    parent's row pointers and edges, output rows 0..r1-r0, self rows (and
+    thus sources) global, heavy rows re-segmented locally."""
+    sub = host_ptr[r0:r1 + 1]
+    deg = np.diff(sub)
+    heavy = np.flatnonzero(deg > HEAVY_THRESHOLD).astype(np.int32)
+    nseg = (deg[heavy] + SEGMENT_EDGES - 1) // SEGMENT_EDGES
+    seg_ptr = np.zeros(heavy.size + 1, dtype=np.int64)
+    np.cumsum(nseg, out=seg_ptr[1:])
+    seg_heavy = np.repeat(np.arange(heavy.size, dtype=np.int32), nseg)
+    dev = parent.row_ptr.device
+    has = heavy.size > 0
+    spec = AggSpec(
+        n_rows=r1 - r0, row_ptr=parent.row_ptr[r0:r1 + 1], idx=parent.idx, out_idx=None,
+        self_idx=self_ids[r0:r1],
+        heavy_rows=torch.from_numpy(heavy).to(dev) if has else None,
+        heavy_seg_ptr=torch.from_numpy(seg_ptr).to(dev) if has else None,
+        seg_heavy=torch.from_numpy(seg_heavy).to(dev) if has else None,
+        heavy_counter=torch.zeros(16 * max(heavy.size, 1), dtype=torch.int32, device=dev)
+        if has else None,
+        n_heavy=int(heavy.size), n_segs=int(seg_heavy.size), nnz=int(sub[-1] - sub[0]))
+    spec._partial = parent._partial      # same stream, sequential: one scratch
+    return spec
+
+
+class StreamGraph:
+    """The graph on the device for the streaming engine, in vertex order:
+    forward in-CSR (the transpose of the graph's CSR, sources ascending),
+    the out-CSR for the transposed pull (the same arrays when the graph is
+    symmetric), per-chunk views of both, and degree scales."""
+
+    def __init__(self, graph, device, chunk_rows: int, max_width: int, threads: int = 0):
+        n, m = graph.num_vertices, graph.num_edges
+        L = _lib.lib()
+        src_ptr = np.ascontiguousarray(graph.src_ptr, dtype=np.int64)
+        dst_idx = np.ascontiguousarray(graph.dst_idx, dtype=np.int32)
+        t_ptr = np.empty(n + 1, dtype=np.int64)
+        t_idx = np.empty(max(m, 1), dtype=np.int32)
+        _lib.check(L.grd_csr_transpose(n, _lib.ptr(src_ptr), _lib.ptr(dst_idx), n, _lib.ptr(t_ptr),
+                                       _lib.ptr(t_idx)), "csr_transpose")
+        t_idx = t_idx[:m]
+        eq = np.zeros(1, dtype=np.int32)
+        _lib.check(L.grd_csr_same_rows(n, _lib.ptr(src_ptr), _lib.ptr(dst_idx), _lib.ptr(t_ptr),
+                                       _lib.ptr(t_idx), int(threads), _lib.ptr(eq)), "csr_same_rows")
+        self.symmetric = bool(eq[0])
+        self.device = device
+        self.num_vertices, self.num_edges = n, m
+        self.fwd = AggSpec.build(t_ptr, t_idx, device)
+        self.fwd.partial(max_width)
+        if self.symmetric:
+            self.bwd, bwd_ptr = self.fwd, t_ptr
+        else:
+            self.bwd, bwd_ptr = AggSpec.build(src_ptr, dst_idx, device), src_ptr
+            self.bwd.partial(max_width)
+        del t_idx
+        self.self_ids = torch.arange(n, dtype=torch.int32, device=device)
+        self.chunks = _chunk_ranges(n, int(chunk_rows))
+        self.fwd_chunks = [_chunk_spec(self.fwd, t_ptr, r0, r1, self.self_ids) for r0, r1 in self.chunks]
+        self.bwd_chunks = self.fwd_chunks if self.symmetric else \
+            [_chunk_spec(self.bwd, bwd_ptr, r0, r1, self.self_ids) for r0, r1 in self.chunks]
+        self._deg = np.diff(t_ptr).astype(np.float64)
+        self._scales: dict[str, torch.Tensor] = {}
+
+    def scale(self, name: str | None) -> torch.Tensor | None:
+        if name is None:
+            return None
+        t = self._scales.get(name)
+        if t is None:
+            t = torch.from_numpy(_degree_scale(name, self._deg).astype(np.float32)).to(self.device)
+            self._scales[name] = t
+        return t
+
+
+def _rows(t: torch.Tensor | None, r0: int, r1: int) -> torch.Tensor | None:
+    return None if t is None else t[r0:r1]
+
+
+class StreamingEngine:
+    """One GCN epoch with host-resident features (module docstring)."""
+
+    def __init__(self, sg: StreamGraph, model, features: torch.Tensor, labels: np.ndarray,
+                 train_mask: np.ndarray, x_cache_bytes: int | None = None):
+        why = streaming_supported(model)
+        if why is not None:
+            raise NotImplementedError(why)
+        dev = sg.device
+        self.sg, self.device, self.model = sg, dev, model
+        self.dims = model.dims
+        self.L = model.num_layers
+        self.V = sg.num_vertices
+        self.mode = model.aggregation_mode
+        self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1) for l in range(self.L)]
+        self.wts = _Weights(model, dev)
+        F = self.dims[0]
+        if features.shape != (self.V, ld_of(F)) or features.dtype != torch.float32 or \
+                features.device.type != "cpu" or not features.is_contiguous():
+            raise ValueError("features must be a contiguous host fp32 [V, round_up(F, 4)] tensor")
+        if not features.is_pinned() and features.data_ptr() not in _REGISTERED:
+            raise ValueError("features must be page-locked (host_features / register_host)")
+        self.x_host = features
+        self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
+        self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
+        self.mask_count = int(np.count_nonzero(train_mask))
+        if self.mask_count == 0:
+            raise ValueError("loss mask selects no vertices")
+        last = self.cfg[-1]
+        hid = max(ld_of(d) for d in self.dims[1:self.L])
+        width = max(hid, last.ld_out if last.transform_first else 0)
+        # two whole-height layer buffers (zeroed once: pad columns stay 0)
+        self.buf = [ops.zeros_rows(self.V, width, dev), ops.zeros_rows(self.V, width, dev)]
+        # transform-first last layer: its scaled logit gradient G' is pulled
+        # whole, so it needs a third (narrow) buffer
+        self.gbuf = ops.zeros_rows(self.V, last.d_out, dev) if last.transform_first else None
+        # deeper hidden layers (l >= 2) kept in pinned host memory
+        self.host_acts = {l: torch.zeros((self.V, width), dtype=torch.float32, pin_memory=True)
+                          for l in range(2, self.L - 1)}
+        cr = max(r1 - r0 for r0, r1 in sg.chunks)
+        self.chunk_rows = cr
+        maxw = max(ld_of(d) for d in self.dims)
+        # streamed host rows (features, or a deeper hidden layer kept on the host)
+        xw = max([ld_of(F)] + [t.shape[1] for t in self.host_acts.values()])
+        self.xc = [torch.zeros(cr * xw, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.ac = ops.zeros_rows(cr, maxw, dev)                       # regathered hidden rows
+        self.nc = ops.zeros_rows(cr, maxw, dev)                       # aggregate / pull rows
+        self.lc = ops.zeros_rows(cr, last.d_out, dev)                 # logits
+        self.gc = ops.zeros_rows(cr, last.d_out, dev)                 # logit gradient
+        self.dc = ops.zeros_rows(cr, maxw, dev)                       # input-gradient rows
+        self.copy_stream = torch.cuda.Stream(dev)
+        self._ready = [torch.cuda.Event() for _ in range(2)]
+        self._free = [torch.cuda.Event() for _ in range(2)]
+        self.n_chunks = len(sg.chunks)
+        self.stats_all = torch.zeros((self.n_chunks, 4), dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.partials = ops.loss_partials(cr, dev)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        # HBM cache of the leading feature rows (X never changes within a
+        # call): whatever HBM is left after the working set, in whole chunks
+        self._cache_ready = torch.cuda.Event()
+        row_bytes = 4 * ld_of(F)
+        if x_cache_bytes is None:
+            free, _ = torch.cuda.mem_get_info(dev)
+            x_cache_bytes = max(0, free - (4 << 30))
+        rows = min(self.V, int(x_cache_bytes) // row_bytes)
+        rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
+        self.cache_rows = rows
+        self.x_cache = torch.empty((rows, ld_of(F)), dtype=torch.float32, device=dev) if rows else None
+        self.x_cache_valid = False
+
+    # ------------------------------------------------------------ helpers --
+    def _scale(self, c) -> torch.Tensor | None:
+        return self.sg.scale("s") if c.sym else None
+
+    def _pre_scale(self, l: int) -> torch.Tensor | None:
+        """Scale the producer of dA_{l+1} applies for a transform-first
+        consumer layer l (LayerwiseEngine._consumer_epilogue)."""
+        c = self.cfg[l]
+        return self.sg.scale(c.pre_scale) if c.transform_first else None
+
+    def _combine(self, sym: bool, consumer_scale):
+        if consumer_scale is None:
+            return self.sg.scale("s") if sym else None
+        if not sym:
+            return consumer_scale
+        return self.sg.scale("inv_deg1")
+
+    def _stream(self, host: torch.Tensor, fn) -> None:
+        """For every row chunk: fn(rows, r0, r1) on the compute stream, the
+        rows coming from the HBM feature cache when cached, else by H2D of
+        host[r0:r1] on the copy stream into one of two device buffers.  A
+        buffer's copy waits only for that buffer's last use, so the first
+        transfers of a pass overlap whatever compute precedes it."""
+        cur = torch.cuda.current_stream(self.device)
+        cs = self.copy_stream
+        width = host.shape[1]
+        cached = host is self.x_host and self.x_cache is not None
+        if cached and not self.x_cache_valid:
+            cs.wait_stream(cur)            # earlier readers of the cache are done
+        nb = 0
+        for r0, r1 in self.sg.chunks:
+            n = r1 - r0
+            if cached and r1 <= self.cache_rows:
+                dst = self.x_cache[r0:r1]
+                if not self.x_cache_valid:         # first pass fills the cache
+                    with torch.cuda.stream(cs):
+                        dst.copy_(host[r0:r1], non_blocking=True)
+                        self._cache_ready.record(cs)
+                    cur.wait_event(self._cache_ready)
+                    self.h2d_bytes += n * width * 4
+                fn(dst, r0, r1)
+                continue
+            b = nb & 1
+            nb += 1
+            dst = self.xc[b][: n * width].view(n, width)
+            with torch.cuda.stream(cs):
+                cs.wait_event(self._free[b])
+                dst.copy_(host[r0:r1], non_blocking=True)
+                self._ready[b].record(cs)
+            cur.wait_event(self._ready[b])
+            fn(dst, r0, r1)
+            self._free[b].record(cur)
+            self.h2d_bytes += n * width * 4
+        if cached:
+            self.x_cache_valid = True
+
+    def set_features(self, features: torch.Tensor) -> None:
+        """Re-bind the host features (the HBM cache refills on the next pass)."""
+        if not features.is_pinned() and features.data_ptr() not in _REGISTERED:
+            raise ValueError("features must be page-locked (host_features / register_host)")
+        self.x_host = features
+        self.x_cache_valid = False
+
+    def _to_host(self, src: torch.Tensor, host: torch.Tensor) -> None:
+        """D2H of a whole layer in row chunks on the copy stream."""
+        cur = torch.cuda.current_stream(self.device)
+        self.copy_stream.wait_stream(cur)
+        with torch.cuda.stream(self.copy_stream):
+            for r0, r1 in self.sg.chunks:
+                host[r0:r1].copy_(src[r0:r1, : host.shape[1]], non_blocking=True)
+        cur.wait_stream(self.copy_stream)
+        self.d2h_bytes += host.numel() * 4
+
+    # -------------------------------------------------------------- epoch --
+    def epoch(self, lr: float) -> None:
+        sg, cfg, L, V = self.sg, self.cfg, self.L, self.V
+        W, dW = self.wts.w, self.wts.dw
+        for dw in dW:
+            dw.zero_()
+        B = list(self.buf)                  # B[1] holds the current layer input
+        # ---- forward of the hidden (transform-first) layers ----
+        for l in range(L - 1):
+            c = cfg[l]
+            s = self._scale(c)
+            P = B[0][:, : c.ld_out]
+            if l == 0:
+                self._stream(self.x_host, lambda x, r0, r1: ops.gemm(
+                    x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)))
+            else:
+                ops.gemm(B[1][:, : c.ld_in], W[l], P, V, c.d_out, c.d_in, row_scale=s)
+            ops.agg_sum(sg.fwd, P, B[1][:, : c.ld_out], c.d_out, post_div_deg=not c.sym,
+                        post_scale=s, relu=True)
+            if l + 1 in self.host_acts:
+                self._to_host(B[1], self.host_acts[l + 1])
+        # ---- last layer + loss + last layer backward, one chunked pass ----
+        self._last_layer(B)
+        # ---- backward of the hidden layers: B[1] = dA_{l+1} (pre-scaled) ----
+        for l in reversed(range(L - 1)):
+            c = cfg[l]
+            s = self._scale(c)
+            D = B[1][:, : c.ld_out]
+            if l == 0:
+                self._backward_first(D, s)
+                break
+            H = B[0][:, : c.ld_out]
+            ops.agg_sum(sg.bwd, D, H, c.d_out, post_scale=s)            # H = A_hat^T D
+            ref_scale = self._pre_scale(l - 1)
+            if l == 1:
+                # regather A_1 = act(A_hat (X W_0)) chunk by chunk from P_0
+                c0 = cfg[0]
+                s0 = self._scale(c0)
+                P0 = B[1][:, : c0.ld_out]
+                self._stream(self.x_host, lambda x, r0, r1: ops.gemm(
+                    x, W[0], P0[r0:r1], r1 - r0, c0.d_out, c0.d_in, row_scale=_rows(s0, r0, r1)))
+                for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
+                    n = r1 - r0
+                    a = self.ac[:n, : c.ld_in]
+                    ops.agg_sum(spec, P0, a, c0.d_out, post_div_deg=not c0.sym,
+                                post_scale=_rows(s0, r0, r1), relu=True)
+                    self._hidden_grad(l, a, H, B[0], r0, r1, ref_scale)
+            else:
+                def step(a, r0, r1):
+                    self._hidden_grad(l, a, H, B[0], r0, r1, ref_scale)
+                self._stream(self.host_acts[l], step)
+            B[0], B[1] = B[1], B[0]
+        # ---- SGD (training.py:352-354) ----
+        for w, dw in zip(W, dW):
+            ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
+
+    def _hidden_grad(self, l: int, a: torch.Tensor, H: torch.Tensor, out: torch.Tensor, r0: int,
+                     r1: int, ref_scale) -> None:
+        """Rows [r0, r1) of a transform-first layer's backward given its input
+        rows a: dW_l += a^T H, dA_l = relu'(a) (H W_l^T) * pre-scale(l-1),
+        written over the (consumed) rows of ``out``, the buffer holding H."""
+        c = self.cfg[l]
+        n = r1 - r0
+        Hc = H[r0:r1]
+        ops.wgrad_sgd(a, Hc, self.wts.dw[l], c.d_in, c.d_out, n, accumulate=True)
+        d = self.dc[:n, : c.ld_in]
+        ops.gemm(Hc, self.wts.w[l], d, n, c.d_in, c.d_out, trans_b=True,
+                 row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
+        out[r0:r1, : c.ld_in].copy_(d)    # dA_l rows replace H rows (consumed)
+
+    def _backward_first(self, D: torch.Tensor, s) -> None:
+        """Layer 0: dW_0 = X^T (A_hat^T D), chunk by chunk with X streamed."""
+        c = self.cfg[0]
+        specs = self.sg.bwd_chunks
+
+        def step(x, r0, r1, _it=iter(specs)):
+            n = r1 - r0
+            h = self.nc[:n, : c.ld_out]
+            ops.agg_sum(next(_it), D, h, c.d_out, post_scale=_rows(s, r0, r1))
+            ops.wgrad_sgd(x, h, self.wts.dw[0], c.d_in, c.d_out, n, accumulate=True)
+        self._stream(self.x_host, step)
+
+    def _last_layer(self, B: list) -> None:
+        """Forward, loss and backward of the last layer in one chunked pass;
+        leaves dA_{L-1} (masked, pre-scaled for layer L-2) in B[1]."""
+        sg, L = self.sg, self.L
+        l = L - 1
+        c = self.cfg[l]
+        W, dW = self.wts.w[l], self.wts.dw[l]
+        s = self._scale(c)
+        A = B[1][:, : c.ld_in]
+        C = c.d_out
+        prev_ref_scale = self._pre_scale(l - 1)
+        if not c.transform_first:
+            # N = A_hat A (regathered per chunk), logits = N W; gn = (G W^T) * pre_scale
+            Q = B[0][:, : c.ld_in]
+            for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
+                n = r1 - r0
+                N = self.nc[:n, : c.ld_in]
+                ops.agg_sum(spec, A, N, c.d_in, src_scale=s, post_div_deg=not c.sym,
+                            post_scale=_rows(s, r0, r1))
+                lg = self.lc[:n]
+                ops.gemm(N, W, lg, n, C, c.d_in)
+                g = self.gc[:n]
+                ops.softmax_xent(lg, n, C, self.labels[r0:r1], self.mask[r0:r1], self.mask_count,
+                                 g, self.stats_all[i], self.partials)
+                ops.wgrad_sgd(N, g, dW, c.d_in, C, n, accumulate=True)
+                ops.gemm(g, W, Q[r0:r1], n, c.d_in, C, trans_b=True,
+                         row_scale=_rows(self.sg.scale(c.pre_scale), r0, r1))
+            post = self._combine(c.sym, prev_ref_scale)
+            # dA_{L-1} = relu'(A) (A_hat^T Q) * post, in place over A
+            ops.agg_sum(sg.bwd, Q, A, c.d_in, post_scale=post, mask_ref=A)
+            return
+        # transform-first: P = A W (whole), logits rows = act-free A_hat P
+        P = B[0][:, : c.ld_out]
+        ops.gemm(A, W, P, self.V, C, c.d_in, row_scale=s)
+        G = self.gbuf
+        pre = self.sg.scale(c.pre_scale)
+        for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
+            n = r1 - r0
+            lg = self.lc[:n]
+            ops.agg_sum(spec, P, lg, C, post_div_deg=not c.sym, post_scale=_rows(s, r0, r1))
+            ops.softmax_xent(lg, n, C, self.labels[r0:r1], self.mask[r0:r1], self.mask_count,
+                             G[r0:r1], self.stats_all[i], self.partials, grad_scale=pre[r0:r1])
+        H = B[0][:, : c.ld_out]
+        ops.agg_sum(sg.bwd, G, H, C, post_scale=s)                  # H = A_hat^T G'
+        for r0, r1 in sg.chunks:
+            self._hidden_grad(l, A[r0:r1], H, B[0], r0, r1, prev_ref_scale)
+        B[0], B[1] = B[1], B[0]   # dA_{L-1} now in the buffer that held H
+
+    def read_stats(self) -> tuple[float, float]:
+        """(loss, accuracy) of the last epoch: per-chunk sums added in chunk
+        order on the host (float64)."""
+        s = self.stats_all.cpu().numpy()
+        loss = float(np.sum(s[:, 2])) / self.mask_count
+        acc = float(np.sum(s[:, 3])) / self.mask_count
+        self.stats.copy_(torch.tensor([loss, acc, s[:, 2].sum(), s[:, 3].sum()], dtype=torch.float64))
+        return loss, acc
+
+
+# --------------------------------------------------------------------------
+# when to stream, and the session partitioned_train drives
+# --------------------------------------------------------------------------
+def resident_bytes(num_vertices: int, num_edges: int, model) -> int:
+    """HBM the layer-wise resident engine needs (engine.LayerwiseEngine):
+    forward + backward CSRs, every layer, three scratch layers of the widest
+    width, heavy-row scratch, degree scales."""
+    V, E = int(num_vertices), int(num_edges)
+    lds = [ld_of(d) for d in model.dims]
+    wide = max(lds) * (2 if model.kind == "sage" else 1)
+    if model.kind == "gat":
+        wide = max(wide, model.heads * max(lds) + 2 * model.heads + 4)
+    graph = 2 * (8 * (V + 1) + 4 * E) + 4 * V
+    layers = 4 * V * (sum(lds) + 3 * wide)
+    scratch = 4 * E * max(lds) // 64 + 16 * V
+    edge_state = 8 * E * model.heads if model.kind == "gat" else 0
+    return graph + layers + scratch + edge_state
+
+
+def streaming_bytes(num_vertices: int, num_edges: int, model, chunk_rows: int,
+                    symmetric: bool = True) -> int:
+    """HBM the streaming engine needs (StreamingEngine)."""
+    V, E = int(num_vertices), int(num_edges)
+    lds = [ld_of(d) for d in model.dims]
+    width = max(lds[1:-1] + ([lds[-1]] if lds[-1] <= lds[-2] else []))
+    graph = (1 if symmetric else 2) * (8 * (V + 1) + 4 * E) + 4 * V
+    layers = 2 * 4 * V * width + (4 * V * lds[-1] if lds[-1] <= lds[-2] else 0)
+    chunks = 4 * int(chunk_rows) * (2 * max(lds) + 3 * max(lds) + 2 * lds[-1])
+    return graph + layers + chunks + 4 * E * max(lds) // 64 + 16 * V
+
+
+DEFAULT_CHUNK_ROWS = 1 << 20
+
+
+def host_features(dataset) -> torch.Tensor:
+    """The dataset's features as a page-locked host fp32 [V, round_up(F, 4)]
+    tensor: the array itself when it already is fp32 with F % 4 == 0
+    (registered in place), else a padded pinned copy kept on the dataset."""
+    feats = dataset.features
+    f = feats.shape[1]
+    if feats.dtype == np.float32 and feats.flags.c_contiguous and f % 4 == 0:
+        root = feats
+        while isinstance(root.base, np.ndarray):
+            root = root.base
+        return register_host(torch.from_numpy(feats), owner=root)
+    stage = getattr(dataset, "_stream_stage", None)
+    if stage is None or tuple(stage.shape) != (feats.shape[0], ld_of(f)):
+        stage = torch.zeros((feats.shape[0], ld_of(f)), dtype=torch.float32, pin_memory=True)
+        dataset._stream_stage = stage
+    np.copyto(stage.numpy()[:, :f], feats, casting="same_kind")
+    return stage
+
+
+class StreamSession:
+    """Device session (training.TrainSession's interface) over the
+    streaming engine: graph upload cached on the plan, features streamed
+    from the host on every epoch."""
+
+    layerwise = True
+
+    def __init__(self, dataset, plan, model, chunk_rows: int = DEFAULT_CHUNK_ROWS,
+                 x_cache_bytes: int | None = None):
+        from .model import copy_model
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        key = ("stream_graph", str(self.dev), int(chunk_rows))
+        sg = plan.device_cache.get(key)
+        if sg is None:
+            maxw = max(ld_of(d) for d in model.dims)
+            sg = StreamGraph(dataset.graph, self.dev, chunk_rows, maxw)
+            plan.device_cache[key] = sg
+        self.sg = sg
+        self.dg = sg
+        self.model = copy_model(model)
+        self.dataset = dataset
+        if x_cache_bytes is None and os.environ.get("GRD_X_CACHE_GB"):
+            x_cache_bytes = int(float(os.environ["GRD_X_CACHE_GB"]) * 2**30)
+        self.engine = StreamingEngine(sg, self.model, host_features(dataset), dataset.labels,
+                                      dataset.train_mask, x_cache_bytes=x_cache_bytes)
+
+    def reset(self, dataset, model) -> int:
+        from .model import copy_model
+        eng = self.engine
+        eng.set_features(host_features(dataset))
+        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)))
+        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)))
+        eng.mask_count = int(np.count_nonzero(dataset.train_mask))
+        self.model = copy_model(model)
+        eng.model = self.model
+        eng.wts.load(self.model)
+        self.dataset = dataset
+        return eng.labels.numel() * 4 + eng.mask.numel() + sum(w.size * 4 for w in self.model.weights)
+
+    def run_epoch(self, epoch: int, lr: float, use_graph: bool = True) -> None:
+        self.engine.epoch(lr)
+
+    def read_stats(self) -> tuple[float, float]:
+        return self.engine.read_stats()
+
+    def train(self, epochs: int, lr: float, **_):
+        trace = []
+        for epoch in range(epochs):
+            self.engine.epoch(lr)
+            loss, acc = self.read_stats()
+            if not np.isfinite(loss):
+                raise ValueError(f"non-finite loss {loss} at epoch {epoch}; "
+                                 f"reduce the learning rate or check the inputs")
+            trace.append((epoch, loss, acc))
+        self.engine.wts.export(self.model)
+        return self.model, trace

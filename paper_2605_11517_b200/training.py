@@ -335,17 +335,40 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
     Inside an initialised torch.distributed job with several ranks the
     session is this rank's shard of the partitions (distributed.py)."""
     comm = _communicator()
+    stream = layerwise and comm is None and _use_streaming(dataset, model)
     key = ("session", tuple(model.dims), model.aggregation_mode, model.heads, model.row_normalize,
-           model.dropout_rate, model.dropout_seed, layerwise, comm is not None)
+           model.dropout_rate, model.dropout_seed, layerwise, comm is not None, stream)
     sess = plan.device_cache.get(key)
     if sess is None:
-        sess = TrainSession(dataset, plan, model, layerwise=layerwise, comm=comm)
+        if stream:
+            from .stream import StreamSession
+            sess = StreamSession(dataset, plan, model)
+        else:
+            sess = TrainSession(dataset, plan, model, layerwise=layerwise, comm=comm)
         plan.device_cache[key] = sess
     else:
         if plan.num_vertices != dataset.graph.num_vertices:
             raise ValueError("plan was built for a different graph")
         sess.reset(dataset, model)
     return sess
+
+
+def _use_streaming(dataset: LabeledDataset, model: ModelState) -> bool:
+    """Stream the layers through HBM (stream.py) when the resident engine's
+    working set does not fit the device; GRD_ENGINE=stream|resident forces."""
+    import os
+    from .stream import resident_bytes, streaming_supported
+    forced = os.environ.get("GRD_ENGINE", "")
+    if forced in ("stream", "resident"):
+        if forced == "stream" and streaming_supported(model) is not None:
+            raise NotImplementedError(streaming_supported(model))
+        return forced == "stream"
+    if streaming_supported(model) is not None:
+        return False
+    free, _ = torch.cuda.mem_get_info()
+    avail = free + torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+    g = dataset.graph
+    return resident_bytes(g.num_vertices, g.num_edges, model) > 0.9 * avail
 
 
 def _offloaded_train(dataset, plan, model, epochs, lr, hierarchy, grad_probe, partition_order):

@@ -1,0 +1,126 @@
+"""Layer-streaming engine (stream.py) for graphs whose layers exceed HBM:
+same epoch as the HBM-resident engine and the pinned oracle, with small row
+chunks so every chunked path (split heavy rows, chunk-local outputs with
+global self rows, double-buffered host streaming, host-kept deep layers)
+runs on a small graph.
+
+Tolerance: weights and weight gradients within 1e-4 L2-relative of the
+oracle (north star) and within 1e-5 of the resident engine (same kernels,
+different split-K summation order); loss within 1e-5 relative.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from conftest import rel_l2  # noqa: E402
+from oracle import gcn, plan as oplan  # noqa: E402
+import paper_2605_11517_b200 as g2  # noqa: E402
+from paper_2605_11517_b200.stream import StreamSession  # noqa: E402
+from paper_2605_11517_b200.training import TrainSession  # noqa: E402
+
+
+def _setup(scale, deg, F, C, L, H, mode, directed=False, f32=True):
+    g = g2.generate_kronecker(scale, deg, seed=scale)
+    if directed:   # drop every other edge: a non-symmetric graph
+        src = np.repeat(np.arange(g.num_vertices), np.diff(g.src_ptr))
+        keep = (np.arange(g.num_edges) % 3) != 1
+        g = g2.build_csr(np.stack([src[keep], g.dst_idx[keep]], 1), g.num_vertices)
+    ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=scale + 1)
+    if f32:
+        ds.features = ds.features.astype(np.float32)
+    part = g2.switching_aware_partition(g, 4, g2.PartitionerParams(seed=scale + 2))
+    plan = g2.build_partition_plan(g, part.labels, 4)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=scale + 3, aggregation_mode=mode)
+    return g, ds, plan, model
+
+
+CASES = [
+    # (scale, deg, F, C, L, H, mode, directed, f32)
+    (11, 12, 32, 40, 3, 32, "mean_self_loop", False, True),    # papers-like: AF last layer
+    (11, 12, 32, 7, 2, 16, "mean_self_loop", False, True),     # transform-first last layer
+    (11, 12, 32, 40, 3, 32, "symmetric_norm", False, False),   # sym, f64 features (staged)
+    (10, 16, 30, 9, 2, 24, "symmetric_norm", True, True),      # directed graph, F % 4 != 0
+]
+
+
+@pytest.mark.parametrize("cache", ["none", "part"])
+@pytest.mark.parametrize("case", CASES)
+def test_streaming_matches_resident_and_oracle(case, cache):
+    scale, deg, F, C, L, H, mode, directed, f32 = case
+    g, ds, plan, model = _setup(scale, deg, F, C, L, H, mode, directed, f32)
+    epochs, lr = 2, 0.05
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(epochs, lr, use_graph=False)
+    # no HBM feature cache (every pass streams), or the first chunks cached
+    xb = 0 if cache == "none" else 900 * 4 * ((F + 3) // 4 * 4)
+    ss = StreamSession(ds, plan, model, chunk_rows=300, x_cache_bytes=xb)
+    assert ss.engine.cache_rows == (0 if cache == "none" else 900)
+    assert ss.sg.symmetric == (not directed)
+    assert len(ss.sg.chunks) > 3 and any(s.n_segs for s in ss.sg.fwd_chunks)
+    m_st, tr_st = ss.train(epochs, lr)
+    for (_, l1, a1), (_, l2, a2) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+        assert abs(a1 - a2) <= 2.0 / ds.train_mask.sum()
+    topos = oplan.build_plan(g.src_ptr, g.dst_idx, plan.labels, 4)
+    W, grads, tr_or = gcn.train_partitioned(np.asarray(ds.features, np.float64), ds.labels,
+                                            ds.train_mask, topos, model.weights, epochs, lr, mode=mode)
+    for i in range(L):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+        assert rel_l2(m_st.weight_grads[i], m_ref.weight_grads[i]) < 1e-5
+        assert rel_l2(m_st.weights[i], W[i]) < 1e-4
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_or):
+        assert abs(l1 - l2) <= 1e-4 * abs(l2)
+
+
+def test_streaming_deep_hidden_layers_on_host():
+    """L = 4: A_2 goes to pinned host memory in forward and streams back."""
+    g, ds, plan, model = _setup(11, 12, 32, 48, 4, 32, "mean_self_loop")
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(2, 0.05, use_graph=False)
+    ss = StreamSession(ds, plan, model, chunk_rows=500, x_cache_bytes=0)
+    assert 2 in ss.engine.host_acts
+    m_st, tr_st = ss.train(2, 0.05)
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+    for i in range(4):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+
+
+def test_partitioned_train_selects_streaming(monkeypatch):
+    """GRD_ENGINE=stream routes the public API through the streaming engine
+    (the automatic choice makes it when the resident working set exceeds
+    the free HBM)."""
+    g, ds, plan, model = _setup(10, 8, 16, 5, 2, 8, "mean_self_loop")
+    monkeypatch.setenv("GRD_ENGINE", "stream")
+    m1, tr1, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    assert any(isinstance(v, StreamSession) for v in plan.device_cache.values())
+    monkeypatch.setenv("GRD_ENGINE", "resident")
+    plan2 = g2.build_partition_plan(g, plan.labels, 4)
+    m2, tr2, _ = g2.partitioned_train(ds, plan2, model, epochs=1, lr=0.05)
+    assert abs(tr1[0][1] - tr2[0][1]) <= 1e-5 * abs(tr2[0][1])
+    for a, b in zip(m1.weights, m2.weights):
+        assert rel_l2(a, b) < 1e-5
+
+
+def test_streaming_session_rebinds_features(monkeypatch):
+    """A second call on the same plan with other features refills the HBM
+    feature cache (no stale rows)."""
+    g, ds, plan, model = _setup(10, 8, 16, 5, 2, 8, "mean_self_loop")
+    monkeypatch.setenv("GRD_ENGINE", "stream")
+    g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    ds2 = g2.LabeledDataset(graph=g, features=(ds.features * 0.5).astype(np.float32),
+                            labels=ds.labels, train_mask=ds.train_mask)
+    m1, tr1, _ = g2.partitioned_train(ds2, plan, model, epochs=1, lr=0.05)
+    sess = [v for v in plan.device_cache.values() if isinstance(v, StreamSession)][0]
+    assert sess.engine.cache_rows == g.num_vertices      # fully cached
+    ref = TrainSession(ds2, plan, model)
+    m2, tr2 = ref.train(1, 0.05, use_graph=False)
+    assert abs(tr1[0][1] - tr2[0][1]) <= 1e-5 * abs(tr2[0][1])
+    for a, b in zip(m1.weights, m2.weights):
+        assert rel_l2(a, b) < 1e-5

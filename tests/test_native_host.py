@@ -159,3 +159,31 @@ def test_csr_transpose_is_the_stable_argsort():
     assert _lib.lib().grd_csr_transpose(1, bad.ctypes.data, np.array([5], np.int32).ctypes.data, 2,
                                         np.empty(3, np.int64).ctypes.data,
                                         np.empty(1, np.int32).ctypes.data) < 0
+
+
+def test_csr_same_rows_detects_symmetry():
+    """grd_csr_same_rows(G, transpose(G)) == 1 exactly for symmetric graphs
+    (the streaming engine then keeps one CSR for both directions)."""
+    from paper_2605_11517_b200 import _lib, build_csr, generate_kronecker
+
+    def same(g):
+        n, m = g.num_vertices, g.num_edges
+        tp = np.empty(n + 1, np.int64)
+        ti = np.empty(max(m, 1), np.int32)
+        L = _lib.lib()
+        _lib.check(L.grd_csr_transpose(n, _lib.ptr(g.src_ptr), _lib.ptr(g.dst_idx), n,
+                                       _lib.ptr(tp), _lib.ptr(ti)))
+        assert np.all(np.diff(tp) >= 0)
+        for v in range(0, n, max(1, n // 50)):        # rows ascending
+            assert np.all(np.diff(ti[tp[v]:tp[v + 1]]) > 0)
+        eq = np.zeros(1, np.int32)
+        _lib.check(L.grd_csr_same_rows(n, _lib.ptr(g.src_ptr), _lib.ptr(g.dst_idx), _lib.ptr(tp),
+                                       _lib.ptr(ti), 4, _lib.ptr(eq)))
+        return bool(eq[0])
+
+    g = generate_kronecker(12, 8, seed=3)
+    assert same(g)
+    src = np.repeat(np.arange(g.num_vertices), np.diff(g.src_ptr))
+    keep = np.arange(g.num_edges) != 17
+    assert not same(build_csr(np.stack([src[keep], g.dst_idx[keep]], 1), g.num_vertices))
+    assert same(build_csr(np.zeros((0, 2), np.int64), 5))
