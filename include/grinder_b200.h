@@ -132,6 +132,22 @@ int grd_host_scatter_add_rows(const float* src, int64_t ld_src,
                               int32_t width, float* dst, int64_t ld_dst,
                               int32_t num_threads);
 
+/* Storage tier (SSO, the ledger's gpu_storage /
+ * host_storage links, hierarchy.py:519-583): page-cache-bypassing (O_DIRECT)
+ * file I/O between tier files and page-locked host buffers, split into
+ * 8 MiB requests served by num_threads threads.  offset, nbytes and the
+ * buffer address must be multiples of grd_direct_alignment() (4096).
+ * grd_direct_open reports in *direct_out whether O_DIRECT is in effect (a
+ * filesystem without it falls back to buffered I/O).  Reads past the end of
+ * the file return zeros. */
+int64_t grd_direct_alignment(void);
+int grd_direct_open(const char* path, int32_t writable, int64_t size, int32_t* fd_out,
+                    int32_t* direct_out);
+int grd_direct_close(int32_t fd);
+int grd_direct_read(int32_t fd, int64_t offset, int64_t nbytes, void* dst, int32_t num_threads);
+int grd_direct_write(int32_t fd, int64_t offset, int64_t nbytes, const void* src,
+                     int32_t num_threads);
+
 /* ------------------------------------------------------------------------
  * Device kernels (sm_100a).  All take `stream` = cudaStream_t.
  * --------------------------------------------------------------------- */

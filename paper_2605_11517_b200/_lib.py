@@ -147,6 +147,11 @@ SIGNATURES = {
     "grd_csr_same_rows": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "grd_host_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32]),
     "grd_host_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32]),
+    "grd_direct_alignment": (c_i64, []),
+    "grd_direct_open": (c_i32, [ctypes.c_char_p, c_i32, c_i64, c_vp, c_vp]),
+    "grd_direct_close": (c_i32, [c_i32]),
+    "grd_direct_read": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i32]),
+    "grd_direct_write": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i32]),
     "grd_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_agg_sum": (c_i32, [ctypes.POINTER(GrdAggArgs), c_vp]),

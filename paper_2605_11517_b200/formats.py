@@ -61,15 +61,21 @@ def write_features(path: str | Path, matrix: np.ndarray) -> None:
         fh.write(mat.tobytes())
 
 
-def read_features(path: str | Path, dtype=np.float64) -> np.ndarray:
+def read_features(path: str | Path, dtype=np.float64, mmap: bool = False) -> np.ndarray:
     """Feature matrix as f64 (the reference's type) or, with dtype=float32,
-    the stored values without conversion."""
+    the stored values without conversion; ``mmap=True`` (float32 only)
+    returns the memory-mapped rows themselves (no read), which the streaming
+    engine serves from the file as its storage tier."""
     raw = np.memmap(path, dtype=np.uint8, mode="r")
     rows, cols = struct.unpack("<QQ", bytes(raw[:16]))
     need = 16 + 4 * rows * cols
     if raw.size != need:
         raise ValueError(f"truncated feature file: expected {need} bytes, found {raw.size}")
     vals = np.frombuffer(raw, dtype="<f4", count=rows * cols, offset=16).reshape(rows, cols)
+    if mmap:
+        if np.dtype(dtype) != np.float32:
+            raise ValueError("mmap=True needs dtype=float32")
+        return vals
     return vals.astype(dtype)
 
 

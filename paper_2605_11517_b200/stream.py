@@ -47,6 +47,7 @@ import torch
 from . import _lib, ops
 from .engine import _degree_scale, _LayerCfg, _Weights
 from .ops import HEAVY_THRESHOLD, SEGMENT_EDGES, AggSpec, ld_of
+from .tiers import FileRows, HostRows, file_backing
 
 __all__ = ["StreamGraph", "StreamingEngine", "streaming_supported", "register_host"]
 
@@ -180,7 +181,7 @@ def _rows(t: torch.Tensor | None, r0: int, r1: int) -> torch.Tensor | None:
 class StreamingEngine:
     """One GCN epoch with host-resident features (module docstring)."""
 
-    def __init__(self, sg: StreamGraph, model, features: torch.Tensor, labels: np.ndarray,
+    def __init__(self, sg: StreamGraph, model, features, labels: np.ndarray,
                  train_mask: np.ndarray, x_cache_bytes: int | None = None):
         why = streaming_supported(model)
         if why is not None:
@@ -194,12 +195,6 @@ class StreamingEngine:
         self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1) for l in range(self.L)]
         self.wts = _Weights(model, dev)
         F = self.dims[0]
-        if features.shape != (self.V, ld_of(F)) or features.dtype != torch.float32 or \
-                features.device.type != "cpu" or not features.is_contiguous():
-            raise ValueError("features must be a contiguous host fp32 [V, round_up(F, 4)] tensor")
-        if not features.is_pinned() and features.data_ptr() not in _REGISTERED:
-            raise ValueError("features must be page-locked (host_features / register_host)")
-        self.x_host = features
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
         self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
         self.mask_count = int(np.count_nonzero(train_mask))
@@ -247,7 +242,7 @@ class StreamingEngine:
         rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
         self.cache_rows = rows
         self.x_cache = torch.empty((rows, ld_of(F)), dtype=torch.float32, device=dev) if rows else None
-        self.x_cache_valid = False
+        self.set_features(features)
 
     # ------------------------------------------------------------ helpers --
     def _scale(self, c) -> torch.Tensor | None:
@@ -266,50 +261,62 @@ class StreamingEngine:
             return consumer_scale
         return self.sg.scale("inv_deg1")
 
-    def _stream(self, host: torch.Tensor, fn) -> None:
+    def _stream(self, src, fn) -> None:
         """For every row chunk: fn(rows, r0, r1) on the compute stream, the
-        rows coming from the HBM feature cache when cached, else by H2D of
-        host[r0:r1] on the copy stream into one of two device buffers.  A
-        buffer's copy waits only for that buffer's last use, so the first
-        transfers of a pass overlap whatever compute precedes it."""
+        rows coming from the HBM feature cache when cached, else by H2D from
+        the row source (tiers.py: host memory or the NVMe tier file) on the
+        copy stream into one of two device buffers.  A buffer's copy waits
+        only for that buffer's last use, so the first transfers of a pass
+        overlap whatever compute precedes it."""
         cur = torch.cuda.current_stream(self.device)
         cs = self.copy_stream
-        width = host.shape[1]
-        cached = host is self.x_host and self.x_cache is not None
-        if cached and not self.x_cache_valid:
+        width = src.width
+        cached = src is self.x_src and self.x_cache is not None
+        fill = cached and not self.x_cache_valid
+        if fill:
             cs.wait_stream(cur)            # earlier readers of the cache are done
-        nb = 0
-        for r0, r1 in self.sg.chunks:
-            n = r1 - r0
-            if cached and r1 <= self.cache_rows:
-                dst = self.x_cache[r0:r1]
-                if not self.x_cache_valid:         # first pass fills the cache
-                    with torch.cuda.stream(cs):
-                        dst.copy_(host[r0:r1], non_blocking=True)
-                        self._cache_ready.record(cs)
-                    cur.wait_event(self._cache_ready)
-                    self.h2d_bytes += n * width * 4
+        hits = self.cache_rows if cached and not fill else 0
+        src.begin_pass([(r0, r1) for r0, r1 in self.sg.chunks if r1 > hits])
+        try:
+            nb = 0
+            for r0, r1 in self.sg.chunks:
+                n = r1 - r0
+                if r1 <= hits:
+                    fn(self.x_cache[r0:r1], r0, r1)
+                    continue
+                to_cache = cached and r1 <= self.cache_rows
+                if to_cache:                    # first pass fills the HBM cache
+                    dst, ready, free = self.x_cache[r0:r1], self._cache_ready, None
+                else:
+                    b = nb & 1
+                    nb += 1
+                    dst = self.xc[b][: n * width].view(n, width)
+                    ready, free = self._ready[b], self._free[b]
+                with torch.cuda.stream(cs):
+                    if free is not None:
+                        cs.wait_event(free)
+                    view, token = src.acquire(r0, r1)
+                    dst.copy_(view, non_blocking=True)
+                    ready.record(cs)
+                    done = torch.cuda.Event()
+                    done.record(cs)
+                src.release(token, done)
+                cur.wait_event(ready)
                 fn(dst, r0, r1)
-                continue
-            b = nb & 1
-            nb += 1
-            dst = self.xc[b][: n * width].view(n, width)
-            with torch.cuda.stream(cs):
-                cs.wait_event(self._free[b])
-                dst.copy_(host[r0:r1], non_blocking=True)
-                self._ready[b].record(cs)
-            cur.wait_event(self._ready[b])
-            fn(dst, r0, r1)
-            self._free[b].record(cur)
-            self.h2d_bytes += n * width * 4
+                if free is not None:
+                    free.record(cur)
+                self.h2d_bytes += n * width * 4
+        finally:
+            src.end_pass()
         if cached:
             self.x_cache_valid = True
 
-    def set_features(self, features: torch.Tensor) -> None:
-        """Re-bind the host features (the HBM cache refills on the next pass)."""
-        if not features.is_pinned() and features.data_ptr() not in _REGISTERED:
-            raise ValueError("features must be page-locked (host_features / register_host)")
-        self.x_host = features
+    def set_features(self, src) -> None:
+        """Re-bind the feature rows (the HBM cache refills on the next pass)."""
+        if src.n_rows != self.V or src.width != ld_of(self.dims[0]):
+            raise ValueError("feature rows must be [V, round_up(F, 4)]")
+        src.configure(self.cache_rows)
+        self.x_src = src
         self.x_cache_valid = False
 
     def _to_host(self, src: torch.Tensor, host: torch.Tensor) -> None:
@@ -335,7 +342,7 @@ class StreamingEngine:
             s = self._scale(c)
             P = B[0][:, : c.ld_out]
             if l == 0:
-                self._stream(self.x_host, lambda x, r0, r1: ops.gemm(
+                self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
                     x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)))
             else:
                 ops.gemm(B[1][:, : c.ld_in], W[l], P, V, c.d_out, c.d_in, row_scale=s)
@@ -361,7 +368,7 @@ class StreamingEngine:
                 c0 = cfg[0]
                 s0 = self._scale(c0)
                 P0 = B[1][:, : c0.ld_out]
-                self._stream(self.x_host, lambda x, r0, r1: ops.gemm(
+                self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
                     x, W[0], P0[r0:r1], r1 - r0, c0.d_out, c0.d_in, row_scale=_rows(s0, r0, r1)))
                 for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
                     n = r1 - r0
@@ -372,7 +379,7 @@ class StreamingEngine:
             else:
                 def step(a, r0, r1):
                     self._hidden_grad(l, a, H, B[0], r0, r1, ref_scale)
-                self._stream(self.host_acts[l], step)
+                self._stream(HostRows(self.host_acts[l]), step)
             B[0], B[1] = B[1], B[0]
         # ---- SGD (training.py:352-354) ----
         for w, dw in zip(W, dW):
@@ -402,7 +409,7 @@ class StreamingEngine:
             h = self.nc[:n, : c.ld_out]
             ops.agg_sum(next(_it), D, h, c.d_out, post_scale=_rows(s, r0, r1))
             ops.wgrad_sgd(x, h, self.wts.dw[0], c.d_in, c.d_out, n, accumulate=True)
-        self._stream(self.x_host, step)
+        self._stream(self.x_src, step)
 
     def _last_layer(self, B: list) -> None:
         """Forward, loss and backward of the last layer in one chunked pass;
@@ -496,23 +503,44 @@ def streaming_bytes(num_vertices: int, num_edges: int, model, chunk_rows: int,
 DEFAULT_CHUNK_ROWS = 1 << 20
 
 
-def host_features(dataset) -> torch.Tensor:
-    """The dataset's features as a page-locked host fp32 [V, round_up(F, 4)]
-    tensor: the array itself when it already is fp32 with F % 4 == 0
-    (registered in place), else a padded pinned copy kept on the dataset."""
+def feature_rows(dataset, chunk_rows: int = DEFAULT_CHUNK_ROWS, host_cache_bytes: int | None = None):
+    """The dataset's features as a row source (tiers.py) of fp32
+    [V, round_up(F, 4)] rows:
+
+    * features memory-mapped from a GRIN feature file (``load_dataset(...,
+      mmap_features=True)``) stay in that file — the NVMe tier — with a
+      pinned host-cache window of ``host_cache_bytes`` (default: host memory
+      available less 16 GiB; GRD_HOST_CACHE_GB overrides);
+    * fp32 features with F % 4 == 0 in memory are page-locked in place;
+    * anything else is converted once into a padded pinned copy."""
     feats = dataset.features
     f = feats.shape[1]
+    backing = file_backing(feats) if feats.dtype == np.float32 else None
+    if backing is not None and f % 4 == 0:
+        src = getattr(dataset, "_file_rows", None)
+        if src is None or (src.path, src.data_offset) != backing:
+            if host_cache_bytes is None:
+                env = os.environ.get("GRD_HOST_CACHE_GB")
+                if env:
+                    host_cache_bytes = int(float(env) * 2**30)
+                else:
+                    import psutil
+                    host_cache_bytes = max(0, psutil.virtual_memory().available - (16 << 30))
+            src = FileRows(backing[0], backing[1], feats.shape[0], f, chunk_rows,
+                           host_cache_bytes=host_cache_bytes)
+            dataset._file_rows = src
+        return src
     if feats.dtype == np.float32 and feats.flags.c_contiguous and f % 4 == 0:
         root = feats
         while isinstance(root.base, np.ndarray):
             root = root.base
-        return register_host(torch.from_numpy(feats), owner=root)
+        return HostRows(register_host(torch.from_numpy(feats), owner=root))
     stage = getattr(dataset, "_stream_stage", None)
     if stage is None or tuple(stage.shape) != (feats.shape[0], ld_of(f)):
         stage = torch.zeros((feats.shape[0], ld_of(f)), dtype=torch.float32, pin_memory=True)
         dataset._stream_stage = stage
     np.copyto(stage.numpy()[:, :f], feats, casting="same_kind")
-    return stage
+    return HostRows(stage)
 
 
 class StreamSession:
@@ -523,7 +551,7 @@ class StreamSession:
     layerwise = True
 
     def __init__(self, dataset, plan, model, chunk_rows: int = DEFAULT_CHUNK_ROWS,
-                 x_cache_bytes: int | None = None):
+                 x_cache_bytes: int | None = None, host_cache_bytes: int | None = None):
         from .model import copy_model
         self.dev = torch.device("cuda", torch.cuda.current_device())
         key = ("stream_graph", str(self.dev), int(chunk_rows))
@@ -538,13 +566,13 @@ class StreamSession:
         self.dataset = dataset
         if x_cache_bytes is None and os.environ.get("GRD_X_CACHE_GB"):
             x_cache_bytes = int(float(os.environ["GRD_X_CACHE_GB"]) * 2**30)
-        self.engine = StreamingEngine(sg, self.model, host_features(dataset), dataset.labels,
-                                      dataset.train_mask, x_cache_bytes=x_cache_bytes)
+        self.engine = StreamingEngine(sg, self.model, feature_rows(dataset, chunk_rows, host_cache_bytes),
+                                      dataset.labels, dataset.train_mask, x_cache_bytes=x_cache_bytes)
 
     def reset(self, dataset, model) -> int:
         from .model import copy_model
         eng = self.engine
-        eng.set_features(host_features(dataset))
+        eng.set_features(feature_rows(dataset, self.sg.chunks[0][1] if self.sg.chunks else 1))
         eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)))
         eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)))
         eng.mask_count = int(np.count_nonzero(dataset.train_mask))

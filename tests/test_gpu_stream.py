@@ -124,3 +124,32 @@ def test_streaming_session_rebinds_features(monkeypatch):
     assert abs(tr1[0][1] - tr2[0][1]) <= 1e-5 * abs(tr2[0][1])
     for a, b in zip(m1.weights, m2.weights):
         assert rel_l2(a, b) < 1e-5
+
+
+@pytest.mark.parametrize("host_rows", [0, 700])
+def test_streaming_from_nvme_tier(tmp_path, host_rows):
+    """Features kept in their GRIN file (load_dataset(mmap_features=True)):
+    HBM cache (first 600 rows) -> pinned host cache window -> direct reads
+    from the file through the bounce-buffer ring.  Same epoch as the
+    resident engine on the in-memory features."""
+    from paper_2605_11517_b200.tiers import FileRows
+    g, ds, plan, model = _setup(11, 12, 32, 40, 3, 32, "mean_self_loop")
+    ds.save(tmp_path)
+    mm = g2.load_dataset(tmp_path, mmap_features=True)
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(2, 0.05, use_graph=False)
+    ss = StreamSession(mm, plan, model, chunk_rows=300, x_cache_bytes=600 * 32 * 4,
+                       host_cache_bytes=host_rows * 32 * 4)
+    src = ss.engine.x_src
+    assert isinstance(src, FileRows)
+    assert (src.host_lo, src.host_hi) == (600, 600 + host_rows)
+    m_st, tr_st = ss.train(2, 0.05)
+    # pass 1 reads every non-HBM-cached row from the file; later passes only
+    # the rows outside both caches (5 passes over X in 2 epochs)
+    V, rb = g.num_vertices, 32 * 4
+    outside = V - 600 - host_rows
+    assert src.storage_bytes >= rb * ((V - 600) + 4 * outside)
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+    for i in range(3):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5

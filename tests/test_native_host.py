@@ -187,3 +187,57 @@ def test_csr_same_rows_detects_symmetry():
     keep = np.arange(g.num_edges) != 17
     assert not same(build_csr(np.stack([src[keep], g.dst_idx[keep]], 1), g.num_vertices))
     assert same(build_csr(np.zeros((0, 2), np.int64), 5))
+
+
+def _aligned(nbytes, align=4096):
+    raw = np.zeros(nbytes + align, dtype=np.uint8)
+    pad = (-raw.ctypes.data) % align
+    return raw[pad: pad + nbytes]
+
+
+def test_direct_io_roundtrip(tmp_path):
+    """Storage-tier I/O (grd_direct_*): aligned multi-threaded write / read
+    round trip, zero fill past EOF, alignment errors raise ValueError."""
+    from paper_2605_11517_b200 import _lib
+    L = _lib.lib()
+    al = int(L.grd_direct_alignment())
+    assert al == 4096
+    path = str(tmp_path / "tier.bin").encode()
+    fd, direct = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    n = 3 * (8 << 20) + 5 * al                     # several 8 MiB slices + a tail
+    _lib.check(L.grd_direct_open(path, 1, n, _lib.ptr(fd), _lib.ptr(direct)))
+    src = _aligned(n)
+    src[:] = np.random.default_rng(0).integers(0, 256, n, dtype=np.uint8)
+    _lib.check(L.grd_direct_write(int(fd[0]), 0, n, _lib.ptr(src), 4))
+    _lib.check(L.grd_direct_close(int(fd[0])))
+    _lib.check(L.grd_direct_open(path, 0, 0, _lib.ptr(fd), _lib.ptr(direct)))
+    dst = _aligned(n + 2 * al)
+    dst[:] = 7
+    _lib.check(L.grd_direct_read(int(fd[0]), 0, n + 2 * al, _lib.ptr(dst), 3))
+    np.testing.assert_array_equal(dst[:n], src)
+    assert not dst[n:].any()                       # past EOF reads as zeros
+    part = _aligned(2 * al)
+    _lib.check(L.grd_direct_read(int(fd[0]), 4 * al, 2 * al, _lib.ptr(part), 2))
+    np.testing.assert_array_equal(part, src[4 * al: 6 * al])
+    with pytest.raises(ValueError):
+        _lib.check(L.grd_direct_read(int(fd[0]), 100, al, _lib.ptr(part), 1))
+    _lib.check(L.grd_direct_close(int(fd[0])))
+
+
+def test_file_backing_of_mmapped_features(tmp_path):
+    """load_dataset(..., mmap_features=True) keeps the features in their file;
+    file_backing() finds (path, offset of row 0) for the storage tier."""
+    import paper_2605_11517_b200 as g2
+    from paper_2605_11517_b200.tiers import file_backing
+    g = g2.generate_kronecker(8, 4, seed=1)
+    ds = g2.make_random_dataset(g, feature_dim=12, num_classes=3, seed=2)
+    ds.save(tmp_path)
+    mm = g2.load_dataset(tmp_path, mmap_features=True)
+    assert mm.features.dtype == np.float32
+    np.testing.assert_array_equal(mm.features, ds.features.astype(np.float32))
+    path, off = file_backing(mm.features)
+    assert path.endswith("features.bin") and off == 16
+    raw = np.fromfile(path, dtype=np.uint8)
+    row5 = raw[off + 5 * 48: off + 6 * 48].view(np.float32)
+    np.testing.assert_array_equal(row5, mm.features[5])
+    assert file_backing(np.zeros((3, 4), np.float32)) is None
