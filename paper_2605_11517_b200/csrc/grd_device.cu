@@ -736,7 +736,9 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     const char* async_env = getenv("GRD_AGG_ASYNC");
     const int async_on = async_env ? atoi(async_env) : 1;
     // (scaled rows of <= 32 chunks measured faster on the register kernel)
-    if (async_on && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64)
+    const char* mid_env = getenv("GRD_AGG_MID");
+    const bool mid_override = mid_env && atoi(mid_env) > 0;
+    if (async_on && !mid_override && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64)
         return w4 <= 32 ? launch_async<1, 2, 2>(a, st) : launch_async<2, 2, 2>(a, st);
     // rows in flight per warp: 8 for the 17..32-chunk rows (measured +15% at
     // width 100), 4 above
@@ -744,8 +746,41 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     if (w4 <= 2) return launch_agg<2, 1, 4>(a, cc, st);
     if (w4 <= 4) return launch_agg<4, 1, 4>(a, cc, st);
     if (w4 <= 8) return launch_agg<8, 1, 4>(a, cc, st);
-    if (w4 <= 16) return launch_agg<16, 1, 4>(a, cc, st);
-    if (w4 <= 32) return launch_agg<32, 1, 8>(a, cc, st);
+    if (w4 <= 16) {
+        // narrow rows: lane groups of LPR lanes with NV chunks each; swept on
+        // B200 at the products shape (tools/agg_bench.py, GRD_AGG_NARROW):
+        // 4 lanes x 3 chunks, 8 rows deep: -15..19% at widths 40/48 against
+        // 16 lanes x 1 chunk; 8 x 2, 4 deep: -12% at width 64
+        const char* nv_env = getenv("GRD_AGG_NARROW");
+        const int nv = nv_env ? atoi(nv_env) : -1;
+        switch (nv) {
+            case 0: return launch_agg<16, 1, 4>(a, cc, st);
+            case 1: return launch_agg<8, 2, 4>(a, cc, st);
+            case 3: return launch_agg<4, 4, 4>(a, cc, st);
+            case 4: return launch_agg<8, 2, 8>(a, cc, st);
+            case 5: return launch_agg<4, 4, 2>(a, cc, st);
+            default: break;
+        }
+        if (w4 <= 12) return launch_agg<4, 3, 8>(a, cc, st);
+        return launch_agg<8, 2, 4>(a, cc, st);
+    }
+    if (w4 <= 64) {
+        // mid widths: register variants against the staged kernel above
+        const char* mv_env = getenv("GRD_AGG_MID");
+        const int mv = mv_env ? atoi(mv_env) : 0;
+        switch (mv) {
+            case 1: if (w4 <= 32) return launch_agg<8, 4, 4>(a, cc, st); break;
+            case 2: if (w4 <= 32) return launch_agg<16, 2, 4>(a, cc, st); break;
+            case 3: return launch_agg<16, 4, 2>(a, cc, st);
+            case 4: return launch_agg<8, 8, 2>(a, cc, st);
+            case 5: if (w4 <= 32) return launch_agg<8, 4, 8>(a, cc, st); break;
+            default: break;
+        }
+    }
+    // scaled rows of 17..32 chunks (staged kernel off): 16 lanes x 2 chunks,
+    // 4 deep (-7% at width 100 against one row per warp, 8 deep)
+    if (w4 <= 32) return a.src_scale && !a.edge_w ? launch_agg<16, 2, 4>(a, cc, st)
+                                                  : launch_agg<32, 1, 8>(a, cc, st);
     if (w4 <= 64) return launch_agg<32, 2, 4>(a, cc, st);
     if (w4 <= 128) return launch_agg<32, 4, 2>(a, cc, st);
     return launch_agg<32, 8, 1>(a, cc, st);

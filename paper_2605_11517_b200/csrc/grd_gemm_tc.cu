@@ -18,6 +18,12 @@
 //   warps 10-13 epilogue: tcgen05.ld of the double-buffered TMEM accumulator,
 //              fused row-scale / element-multiply / ReLU-mask / ReLU /
 //              accumulate, 128-byte row stores (or split-K partial tiles).
+// Clusters of C = 1, 2 or 4 CTAs along M share the weight operand: each CTA of
+// a cluster fetches 1/C of every B stage and multicasts it into all C CTAs'
+// shared memory (TMA / bulk-copy .multicast::cluster), and the MMA issuer's
+// stage-release commit arrives on the empty barrier of every CTA of the
+// cluster, so a stage is refilled only when all C consumers are done with it.
+// This divides the L2->SM traffic of the (re-read per M tile) B operand by C.
 // Shared-memory tiles use the canonical 128-byte swizzled layouts: K-major
 // SWIZZLE_128B for row-major activations (TMA box 32 K x 128 rows) and, for
 // the weight-gradient operands whose rows run along K, MN-major
@@ -57,6 +63,7 @@ struct Params {
     int64_t kchunk;                 // split-K chunk (multiple of 32)
     int splits;
     int stages;
+    int cluster;                    // CTAs per cluster along M (1, 2, 4)
     float* c; int64_t ldc;
     const float* row_scale;
     const float* elem_mul; int64_t ld_elem_mul;
@@ -120,6 +127,37 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
                      smem_u32(dst)),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+}
+__device__ __forceinline__ void tma_2d_mc(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                          uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_copy_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -211,9 +249,14 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int C = p.cluster;
+    const int crank = C > 1 ? static_cast<int>(cluster_rank()) : 0;
+    const uint16_t cmask = static_cast<uint16_t>((1u << C) - 1u);
     const int64_t mt = (p.m + kBM - 1) / kBM;
+    const int64_t mg = (mt + C - 1) / C;            // M groups of C tiles (one per CTA)
     const int64_t nt = (p.n + bn - 1) / bn;
-    const int64_t ntiles = mt * nt * p.splits;
+    const int64_t ntiles = mg * nt * p.splits;      // cluster work items
+    const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
     const int64_t nkb_full = (p.kchunk + kBK - 1) / kBK;
     uint32_t tmem_cols = 32;
     while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
@@ -227,7 +270,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
             mbar_init(conv + s, kConvThreads);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, static_cast<uint32_t>(C));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
@@ -239,6 +282,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (C > 1) cluster_sync();     // peers' barriers exist before any multicast
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
@@ -252,10 +296,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // ------------------------------------------------ TMA producer --
         if (lane == 0) {
             uint64_t g = 0;
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int z = static_cast<int>(t / (mt * nt));
-                const int64_t r = t % (mt * nt);
-                const int64_t m0 = (r / nt) * kBM, ntile = r % nt, n0 = ntile * bn;
+            for (int64_t t = cid; t < ntiles; t += ncl) {
+                const int z = static_cast<int>(t / (mg * nt));
+                const int64_t r = t % (mg * nt);
+                const int64_t m0 = ((r / nt) * C + crank) * kBM, ntile = r % nt, n0 = ntile * bn;
                 const int64_t nkb = kblocks_of(z);
                 for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
                     const int s = static_cast<int>(g % S);
@@ -277,13 +321,24 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         const int64_t kbg = (k0 / kBK);
                         const int64_t nkb_all = (p.k + kBK - 1) / kBK;
                         const float* src = p.b_packed + (ntile * nkb_all + kbg) * (2 * int64_t(bn) * kBK);
-                        bulk_copy(bdst, src, 2u * b_bytes, full + s);
+                        if (C == 1) {
+                            bulk_copy(bdst, src, 2u * b_bytes, full + s);
+                        } else {   // this CTA's 1/C slice of the hi|lo tile, into every CTA
+                            const uint32_t slice = 2u * b_bytes / static_cast<uint32_t>(C);
+                            bulk_copy_mc(bdst + crank * slice, reinterpret_cast<const uint8_t*>(src) + crank * slice,
+                                         slice, full + s, cmask);
+                        }
                     } else if (p.b_mode == kKMajorTma) {
                         tma_2d(bdst, &map_b, static_cast<int32_t>(k0), static_cast<int32_t>(n0), full + s);
                     } else {
-                        for (int j = 0; j < bn / 32; ++j)
-                            tma_2d(bdst + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
-                                   static_cast<int32_t>(k0), full + s);
+                        for (int j = 0; j < bn / 32; ++j) {
+                            if (C == 1)
+                                tma_2d(bdst + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
+                                       static_cast<int32_t>(k0), full + s);
+                            else if (j % C == crank)
+                                tma_2d_mc(bdst + j * 4096, &map_b, static_cast<int32_t>(n0 + 32 * j),
+                                          static_cast<int32_t>(k0), full + s, cmask);
+                        }
                     }
                 }
             }
@@ -304,8 +359,8 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t a_lay = a_mn ? 1u : 2u, b_lay = b_mn ? 1u : 2u;
             uint64_t g = 0;
             int64_t i = 0;   // tiles with K work (empty split-K tiles are skipped)
-            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int z = static_cast<int>(t / (mt * nt));
+            for (int64_t t = cid; t < ntiles; t += ncl) {
+                const int z = static_cast<int>(t / (mg * nt));
                 const int64_t nkb = kblocks_of(z);
                 if (nkb == 0) continue;
                 const int acc = static_cast<int>(i & 1);
@@ -329,7 +384,8 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         mma_tf32(tacc, dah, dbl, idesc, 1u);
                         mma_tf32(tacc, dah, dbh, idesc, 1u);
                     }
-                    mma_commit(empty + s);
+                    if (C == 1) mma_commit(empty + s);
+                    else mma_commit_mc(empty + s, cmask);   // release the stage in every CTA
                 }
                 mma_commit(tfull + acc);
                 ++i;
@@ -339,8 +395,8 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // -------------------------------------------------- converters --
         const int ctid = threadIdx.x - kConvWarp0 * 32;
         uint64_t g = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int z = static_cast<int>(t / (mt * nt));
+        for (int64_t t = cid; t < ntiles; t += ncl) {
+            const int z = static_cast<int>(t / (mg * nt));
             const int64_t nkb = kblocks_of(z);
             for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
                 const int s = static_cast<int>(g % S);
@@ -358,10 +414,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int q = warp & 3;                       // TMEM lane quarter
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int64_t i = 0;   // same work counter as the MMA issuer
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int z = static_cast<int>(t / (mt * nt));
-            const int64_t r = t % (mt * nt);
-            const int64_t m0 = (r / nt) * kBM, n0 = (r % nt) * bn;
+        for (int64_t t = cid; t < ntiles; t += ncl) {
+            const int z = static_cast<int>(t / (mg * nt));
+            const int64_t r = t % (mg * nt);
+            const int64_t m0 = ((r / nt) * C + crank) * kBM, n0 = (r % nt) * bn;
             const int acc = static_cast<int>(i & 1);
             const bool has_k = kblocks_of(z) > 0;
             const int64_t row = m0 + q * 32 + lane;
@@ -435,6 +491,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (C > 1) cluster_sync();     // no peer still multicasts into this CTA
     if (warp == 0) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
     }
@@ -517,6 +574,17 @@ inline int pick_bn(int64_t n) {
     return bn < 16 ? 16 : bn;
 }
 
+// CTAs per cluster sharing the B operand (GRD_GEMM_CLUSTER = 1, 2 or 4)
+inline int cluster_pref() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("GRD_GEMM_CLUSTER");
+        v = e ? atoi(e) : 1;   // measured: 2 / 4 do not pay (see DESIGN 2.5)
+        if (v != 1 && v != 2 && v != 4) v = 1;
+    }
+    return v;
+}
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -592,10 +660,31 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int64_t tiles = ((g.m + kBM - 1) / kBM) * ((g.n + p.bn - 1) / p.bn) * p.splits;
-    const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-    gemm_tf32x3_ws<<<grid, kThreads, smem, st>>>(map_a, map_b, p);
-    return cudaGetLastError();
+    const int64_t mt = (g.m + kBM - 1) / kBM;
+    int C = cluster_pref();
+    while (C > 1 && mt < C) C >>= 1;               // at most the last group has idle CTAs
+    if (p.b_mode == kKMajorTma) C = 1;
+    p.cluster = C;
+    const int64_t tiles = ((mt + C - 1) / C) * ((g.n + p.bn - 1) / p.bn) * p.splits;
+    const int64_t max_cl = num_sms() / C;
+    const int grid = static_cast<int>((tiles < max_cl ? tiles : max_cl) * C);
+    if (C == 1) {
+        gemm_tf32x3_ws<<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeClusterDimension;
+    attr_c[0].val.clusterDim.x = static_cast<unsigned>(C);
+    attr_c[0].val.clusterDim.y = 1;
+    attr_c[0].val.clusterDim.z = 1;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws, map_a, map_b, p);
 }
 
 cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,

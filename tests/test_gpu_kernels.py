@@ -87,7 +87,8 @@ def test_agg_sum_mask_ref_and_defaults():
 
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
-@pytest.mark.parametrize("m,n,k", [(1000, 64, 128), (257, 10, 64), (131, 47, 100), (64, 256, 300)])
+@pytest.mark.parametrize("m,n,k", [(1000, 64, 128), (257, 10, 64), (131, 47, 100), (64, 256, 300),
+                                   (1300, 96, 64), (2000, 512, 100)])
 def test_gemm_matches_numpy(ta, tb, m, n, k):
     rng = np.random.default_rng(m + n + k)
     a = rng.normal(size=(k, m) if ta else (m, k))
@@ -112,7 +113,8 @@ def test_gemm_relu_out_and_accumulate():
     assert rel_l2(_host(c, 9), np.maximum(c0 + a @ b, 0)) < 5e-6   # relu(C + AB)
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000)])
+@pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000),
+                                   (384, 10, 20000), (512, 96, 9000)])
 def test_wgrad_sgd(m, n, k):
     rng = np.random.default_rng(k)
     a = rng.normal(size=(k, m)).astype(np.float32)

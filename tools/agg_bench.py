@@ -25,10 +25,12 @@ def timeit(fn, reps=8):
         s.record(); fn(); e.record(); torch.cuda.synchronize()
         t += s.elapsed_time(e)
     return t / reps
+env = os.environ.get("AGG_BENCH_ENV", "GRD_AGG_ASYNC")
+widths = [int(w) for w in os.environ.get("AGG_BENCH_WIDTHS", "100,256").split(",")]
 variants = sys.argv[1:] or ["0", "1"]
 res = {}
 inv_deg = dg.scale("inv_deg")
-for w in (100, 256):
+for w in widths:
     y = torch.randn(n, ops.ld_of(w), device=dev); out = ops.zeros_rows(n, w, dev)
     addy = torch.randn(n, ops.ld_of(w), device=dev)
     cases = {
@@ -39,6 +41,6 @@ for w in (100, 256):
     }
     for name, (spec, kw) in cases.items():
         for v in variants:
-            os.environ["GRD_AGG_ASYNC"] = v
+            os.environ[env] = v
             res[f"{name}_{w}_v{v}"] = round(timeit(lambda: ops.agg_sum(spec, y, out, w, **kw)), 3)
 print(json.dumps(res))
