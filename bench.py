@@ -65,12 +65,12 @@ WORKLOADS["papers_full"] = dict(
     scale=27, deg=12, F=128, C=172, L=3, H=128, P=16, mode="mean_self_loop",
     feature_dtype="float32", host_gb=150, cpu_sample=dict(scale=17, deg=12))
 WORKLOADS["igb_nvme"] = dict(
-    desc="configs[4]-style host+NVMe SSO tiers: IGB-shaped 1024-wide features on "
-         "generate_kronecker(22, 12) (4,194,304 V / 50,331,648 E), 3-layer GCN hidden 256, 19 "
-         "classes, 8 partitions; the 17.2 GB feature file stays on the box's disk "
+    desc="configs[4] model and tiers at 1/24 of its size: 3-layer GraphSAGE-mean hidden 256 on "
+         "IGB-shaped 1024-wide features, generate_kronecker(22, 12) (4,194,304 V / 50,331,648 E), "
+         "19 classes, 8 partitions; the 17.2 GB feature file stays on the box's disk "
          "(load_dataset(mmap_features=True)) behind a 4 GiB HBM cache and a 4 GiB pinned host "
-         "cache, the rest read per pass with direct I/O (tiers.py)",
-    scale=22, deg=12, F=1024, C=19, L=3, H=256, P=8, mode="mean_self_loop",
+         "cache, the rest read per pass with direct I/O (tiers.py, streaming engine)",
+    scale=22, deg=12, F=1024, C=19, L=3, H=256, P=8, mode="sage_mean",
     feature_dtype="float32", tier="nvme", x_cache_gb=4, host_cache_gb=4,
     cpu_sample=dict(scale=14, deg=12))
 DEFAULT_WORKLOAD = "products_sage"

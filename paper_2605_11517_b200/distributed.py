@@ -12,7 +12,11 @@ Per layer the engine exchanges only the rows an aggregation actually reads:
 forward, the transformed rows ``P = X W`` (transform-first) or the layer
 input (aggregate-first); backward, the pre-scaled gradient rows for the
 transposed pull.  Exchanges are one ``all_to_all_single`` each (packed by
-a gather kernel, received straight into the contiguous halo block); the
+a gather kernel, received straight into the contiguous halo block).  GAT's
+transposed pull needs per-edge attention that only the target's owner
+holds, so it runs over the transpose of the local in-CSR instead: halo rows
+collect partial sums that a reverse all-to-all returns to their owners,
+added in ascending source-rank order (``ShardDeviceGraph.reverse_add``).  The
 weight gradients of all layers are summed with one bucketed ``all_reduce``
 before the replicated SGD step, and the loss/accuracy partial sums with a
 second one.  Owner-side accumulation replaces the paper's host atomics, so
@@ -100,6 +104,20 @@ class ShardPlan:
     @property
     def local_ids(self) -> np.ndarray:
         return np.concatenate([self.owned, self.halo])
+
+    def local_transpose(self):
+        """Transpose of the local in-CSR: rows = every local id (owned and
+        halo sources), neighbours = the owned targets it feeds, ascending,
+        and for each such edge its position in the in-CSR.  GAT's
+        transposed pull reads the per-edge attention computed here; rows of
+        halo sources hold partial sums for their owners (reverse exchange)."""
+        n = self.n_local
+        deg = np.diff(self.in_ptr)
+        tgt = np.repeat(np.arange(self.n_own, dtype=np.int32), deg)
+        order = np.argsort(self.in_idx, kind="stable")
+        ptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(self.in_idx, minlength=n), out=ptr[1:])
+        return ptr, tgt[order], order.astype(np.int32)
 
 
 def build_shard_plan(graph, plan, rank: int, world: int, comm=None) -> ShardPlan:

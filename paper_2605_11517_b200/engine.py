@@ -98,6 +98,15 @@ class DeviceGraph:
         """Rows of a per-vertex host array in this device's row order."""
         return arr
 
+    def gat_pull(self):
+        """(spec, edge_perm) of GAT's transposed pull: the graph's out-CSR
+        with each out-edge's position in the forward in-CSR."""
+        return self.bwd, self.out_to_in_perm()
+
+    def reverse_add(self, buf: torch.Tensor, width: int) -> None:
+        """Add halo rows' partial sums into their owners' rows (no-op on one device)."""
+        return None
+
     def scale(self, name: str | None) -> torch.Tensor | None:
         if name is None:
             return None
@@ -159,6 +168,30 @@ class ShardDeviceGraph(DeviceGraph):
 
     def local_rows(self, arr: np.ndarray) -> np.ndarray:
         return arr[self.shard.local_ids]
+
+    def gat_pull(self):
+        if getattr(self, "_gat_pull", None) is None:
+            ptr, idx, perm = self.shard.local_transpose()
+            self._gat_pull = (AggSpec.build(ptr, idx, self.device),
+                              torch.from_numpy(perm).to(self.device))
+        return self._gat_pull
+
+    def reverse_add(self, buf: torch.Tensor, width: int) -> None:
+        """The forward exchange reversed: halo rows of ``buf`` (partial sums
+        for rows other ranks own) go back to their owners, which add them
+        into the rows they sent, one source rank after another (fixed
+        order: deterministic for a given world size)."""
+        ld = ld_of(width)
+        send = self._buf("rsend", self.n_recv, ld)
+        recv = self._buf("rrecv", self.n_send, ld)
+        if self.n_recv:
+            ops.gather_rows(buf[self.n_own:], self.recv_ident, send, width)
+        self.comm.all_to_all_rows(recv, send, self.shard.send_counts, self.shard.recv_counts)
+        r0 = 0
+        for cnt in (int(x) for x in self.shard.send_counts):
+            if cnt:
+                ops.scatter_add_rows(recv[r0:r0 + cnt], self.send_idx[r0:r0 + cnt], buf, width)
+            r0 += cnt
 
     def partition(self, q: int):
         raise NotImplementedError("per-partition operators run on one device")
@@ -422,8 +455,6 @@ class LayerwiseEngine(_EngineBase):
         dev = self.device
         wide = 2 * ld_of(self.maxw) if model.kind == "sage" else self.maxw
         if model.kind == "gat":
-            if self.comm is not None:
-                raise NotImplementedError("GAT layers run on one device")
             wide = max([self.maxw] + [c.ld_ext for c in self.cfg])
             self._gat_buffers(dg, model)
         self.t1 = ops.zeros_rows(self.NL, wide, dev)
@@ -524,7 +555,7 @@ class LayerwiseEngine(_EngineBase):
         self.delta = torch.zeros_like(self.alpha)
         self.alpha_self = torch.zeros(self.NL * H, dtype=torch.float32, device=dev)
         self.delta_self = torch.zeros_like(self.alpha_self)
-        self.edge_perm = dg.out_to_in_perm()
+        self.pull, self.edge_perm = dg.gat_pull()
         # t2: the last layer's per-head aggregate O (kept for the backward's
         # gO.O term); t3: its per-head upstream gradient
         hdp = self.cfg[-1].hdp
@@ -540,6 +571,7 @@ class LayerwiseEngine(_EngineBase):
         ops.gat_build_wext(wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.wext[l])
         pext = self.t1[:, : c.ld_ext]
         ops.gemm(x, wt.wext[l], pext, self.V, c.n_ext, c.d_in)
+        dg.exchange(pext, c.n_ext)                # halo rows of [P | s | t]
         ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self)
         return pext
 
@@ -566,15 +598,21 @@ class LayerwiseEngine(_EngineBase):
         gext = self.h[:, : c.ld_ext]
         ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go, o_fwd,
                             self.delta, self.delta_self, gext)
-        ops.agg_sum(dg.bwd, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha, edge_w_perm=self.edge_perm,
-                    self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
-        ops.gat_src_grad(dg.bwd, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
+        if self.NL > self.V:
+            go[self.V:].zero_()    # halo rows: no self term, no stale gradient
+        # dP_u = sum_v alpha_uv gO_v and ds_u = sum_v delta_uv over u's out-edges
+        # (sharded: owned targets only; halo rows are partials for their owners)
+        ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha,
+                    edge_w_perm=self.edge_perm, self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+        ops.gat_src_grad(self.pull, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
+        dg.reverse_add(gext, c.hdp + c.heads)
         ops.wgrad_sgd(x, gext, wt.dwext[l], c.d_in, c.n_ext, self.V)
         if l > 0:
             ref, _ = self._consumer_epilogue(l - 1)
             ops.gemm(gext, wt.wext[l], self.g, self.V, c.d_in, c.n_ext, trans_b=True, relu_ref=ref)
-        ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.dw[l],
-                            wt.datt[l], lr)
+        if not self.defer_sgd:
+            ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.dw[l],
+                                wt.datt[l], lr)
 
     def forward(self) -> None:
         for l, c in enumerate(self.cfg):
@@ -674,6 +712,14 @@ class LayerwiseEngine(_EngineBase):
     def sgd_after_allreduce(self, lr: float) -> None:
         """Sharded runs: sum the local weight gradients over ranks, then the
         replicated SGD step (training.py:343,352-354)."""
+        wt = self.wts
+        if wt.gat:
+            for l, c in enumerate(self.cfg):
+                d_in, dh, dhp = wt.shape[l]
+                self.comm.all_reduce_sum(wt.dwext[l])
+                ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp,
+                                    wt.dw[l], wt.datt[l], lr)
+            return
         for W, dW in zip(self.wts.w, self.wts.dw):
             self.comm.all_reduce_sum(dW)
             ops.wgrad_sgd(W, W, dW, dW.shape[0], dW.shape[1], 0, accumulate=True, w=W, lr=lr)

@@ -31,9 +31,17 @@ chunks of the weight gradients).  Chunks are contiguous vertex ranges;
 aggregation over a chunk is a view of the whole CSR (row-pointer slice,
 shared edge array, global self rows), so nothing is copied per chunk.
 
+GraphSAGE-mean layers (configs[4]: IGB-shaped, 1024 features) stream the
+same way with the pair Y = X [W_root | W_nbr] in the layer buffer:
+out = act(Y_root + mean_in(Y_nbr)) (the root add fused into the
+aggregation epilogue), and in backward the gradient buffer holds
+[gp | mean_in^T gp] so the weight gradient and the input gradient are one
+GEMM each per chunk (engine.LayerwiseEngine._forward_sage/_backward_sage).
+
 Supported: GCN layers (mean_self_loop / symmetric_norm) without row
 normalisation or dropout, L >= 2, hidden layers transform-first
-(d_{l+1} <= d_l for l < L-1); the last layer either way.
+(d_{l+1} <= d_l for l < L-1); the last layer either way.  GraphSAGE-mean:
+every layer transform-first (the last one included).
 """
 
 from __future__ import annotations
@@ -54,16 +62,18 @@ __all__ = ["StreamGraph", "StreamingEngine", "streaming_supported", "register_ho
 
 def streaming_supported(model) -> str | None:
     """None if the streaming engine can train ``model``, else the reason."""
-    if model.kind != "gcn":
-        return "the streaming engine trains GCN layers"
+    if model.kind not in ("gcn", "sage"):
+        return "the streaming engine trains GCN and GraphSAGE-mean layers"
     if model.row_normalize or model.dropout_rate:
         return "the streaming engine trains without row normalisation / dropout"
     dims = model.dims
     L = len(dims) - 1
     if L < 2:
         return "the streaming engine needs at least two layers"
-    if any(dims[l + 1] > dims[l] for l in range(L - 1)):
-        return "hidden layers must be transform-first (d_out <= d_in)"
+    last = L if model.kind == "sage" else L - 1
+    if any(dims[l + 1] > dims[l] for l in range(last)):
+        return ("GraphSAGE layers must all be transform-first (d_out <= d_in)"
+                if model.kind == "sage" else "hidden layers must be transform-first (d_out <= d_in)")
     return None
 
 
@@ -201,15 +211,23 @@ class StreamingEngine:
         if self.mask_count == 0:
             raise ValueError("loss mask selects no vertices")
         last = self.cfg[-1]
+        self.sage = model.kind == "sage"
         hid = max(ld_of(d) for d in self.dims[1:self.L])
         width = max(hid, last.ld_out if last.transform_first else 0)
+        if self.sage:
+            # layer buffers hold the pair Y = [Y_root | Y_nbr] in forward and
+            # [gp | mean^T gp] in backward: twice a layer's output width
+            width = max([hid] + [2 * c.ld_out for c in self.cfg])
         # two whole-height layer buffers (zeroed once: pad columns stay 0)
         self.buf = [ops.zeros_rows(self.V, width, dev), ops.zeros_rows(self.V, width, dev)]
         # transform-first last layer: its scaled logit gradient G' is pulled
-        # whole, so it needs a third (narrow) buffer
-        self.gbuf = ops.zeros_rows(self.V, last.d_out, dev) if last.transform_first else None
+        # whole, so it needs a third (narrow) buffer; GraphSAGE keeps
+        # [G | mean^T G] there
+        gw = 2 * last.ld_out if self.sage else last.d_out
+        self.gbuf = ops.zeros_rows(self.V, gw, dev) if last.transform_first else None
         # deeper hidden layers (l >= 2) kept in pinned host memory
-        self.host_acts = {l: torch.zeros((self.V, width), dtype=torch.float32, pin_memory=True)
+        hw = hid if self.sage else width
+        self.host_acts = {l: torch.zeros((self.V, hw), dtype=torch.float32, pin_memory=True)
                           for l in range(2, self.L - 1)}
         cr = max(r1 - r0 for r0, r1 in sg.chunks)
         self.chunk_rows = cr
@@ -331,6 +349,9 @@ class StreamingEngine:
 
     # -------------------------------------------------------------- epoch --
     def epoch(self, lr: float) -> None:
+        if self.sage:
+            self._epoch_sage(lr)
+            return
         sg, cfg, L, V = self.sg, self.cfg, self.L, self.V
         W, dW = self.wts.w, self.wts.dw
         for dw in dW:
@@ -459,6 +480,98 @@ class StreamingEngine:
             self._hidden_grad(l, A[r0:r1], H, B[0], r0, r1, prev_ref_scale)
         B[0], B[1] = B[1], B[0]   # dA_{L-1} now in the buffer that held H
 
+    # ------------------------------------------------- GraphSAGE-mean --
+    # Buffer roles for the whole epoch: B1 holds layer inputs A_l (forward)
+    # and the regathered pair Y_0 (backward); B0 holds the pair Y_l in
+    # forward and [gp_l | mean^T gp_l] in backward.
+    def _sage_layer_out(self, spec, Y: torch.Tensor, out: torch.Tensor, c, r0: int | None = None,
+                        r1: int | None = None, relu: bool = True) -> None:
+        """out = act(Y_root + mean_in(Y_nbr)) over the rows of ``spec``
+        (all rows, or the chunk [r0, r1) with chunk-local output rows)."""
+        lo = c.ld_out
+        root = Y[:, :lo] if r0 is None else Y[r0:r1, :lo]
+        ops.agg_sum(spec, Y[:, lo: 2 * lo], out, c.d_out, post_div_deg=2, no_self=True,
+                    add_y=root, relu=relu)
+
+    def _sage_pull(self, G: torch.Tensor, c) -> None:
+        """G[:, lo:2lo] = mean_in^T G[:, :lo] (pull over out-edges, 1/deg_v)."""
+        lo = c.ld_out
+        ops.agg_sum(self.sg.bwd, G[:, :lo], G[:, lo: 2 * lo], c.d_out,
+                    src_scale=self.sg.scale("inv_deg"), no_self=True)
+
+    def _sage_grad(self, l: int, a: torch.Tensor, G: torch.Tensor, r0: int, r1: int) -> None:
+        """Rows [r0, r1) of layer l's backward given its input rows a:
+        dW_l += a^T [gp | H]; dA_l = relu'(a) ([gp | H] [W_root | W_nbr]^T),
+        written over the (consumed) rows of B0 (layer-wise _backward_sage)."""
+        c = self.cfg[l]
+        n = r1 - r0
+        gc = G[r0:r1, : 2 * c.ld_out]
+        ops.wgrad_sgd(a, gc, self.wts.dw[l], c.d_in, 2 * c.ld_out, n, accumulate=True)
+        if l > 0:
+            d = self.dc[:n, : c.ld_in]
+            ops.gemm(gc, self.wts.w[l], d, n, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=a)
+            self.buf[0][r0:r1, : c.ld_in].copy_(d)
+
+    def _epoch_sage(self, lr: float) -> None:
+        sg, cfg, L, V = self.sg, self.cfg, self.L, self.V
+        W, dW = self.wts.w, self.wts.dw
+        for dw in dW:
+            dw.zero_()
+        B0, B1 = self.buf
+        # ---- forward of the hidden layers: Y_l -> B0, A_{l+1} -> B1 ----
+        for l in range(L - 1):
+            c = cfg[l]
+            Y = B0[:, : 2 * c.ld_out]
+            if l == 0:
+                self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
+                    x, W[0], Y[r0:r1], r1 - r0, 2 * c.ld_out, c.d_in))
+            else:
+                ops.gemm(B1[:, : c.ld_in], W[l], Y, V, 2 * c.ld_out, c.d_in)
+            self._sage_layer_out(sg.fwd, Y, B1[:, : c.ld_out], c)
+            if l + 1 in self.host_acts:
+                self._to_host(B1, self.host_acts[l + 1])
+        # ---- last layer, loss and its backward in one chunked pass ----
+        l = L - 1
+        c = cfg[l]
+        A = B1[:, : c.ld_in]
+        Y = B0[:, : 2 * c.ld_out]
+        ops.gemm(A, W[l], Y, V, 2 * c.ld_out, c.d_in)
+        G = self.gbuf
+        C = c.d_out
+        for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
+            n = r1 - r0
+            lg = self.lc[:n]
+            self._sage_layer_out(spec, Y, lg, c, r0, r1, relu=False)
+            ops.softmax_xent(lg, n, C, self.labels[r0:r1], self.mask[r0:r1], self.mask_count,
+                             G[r0:r1, : c.ld_out], self.stats_all[i], self.partials)
+        self._sage_pull(G, c)
+        for r0, r1 in sg.chunks:
+            self._sage_grad(l, A[r0:r1], G, r0, r1)
+        # ---- hidden layers: gp_l in B0[:, :lo] ----
+        for l in reversed(range(L - 1)):
+            c = cfg[l]
+            self._sage_pull(B0, c)
+            if l == 0:
+                self._stream(self.x_src, lambda x, r0, r1: ops.wgrad_sgd(
+                    x, B0[r0:r1, : 2 * c.ld_out], dW[0], c.d_in, 2 * c.ld_out, r1 - r0,
+                    accumulate=True))
+            elif l == 1:
+                # regather A_1 = relu(Y0_root + mean(Y0_nbr)) chunk by chunk
+                c0 = cfg[0]
+                Y0 = B1[:, : 2 * c0.ld_out]
+                self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
+                    x, W[0], Y0[r0:r1], r1 - r0, 2 * c0.ld_out, c0.d_in))
+                for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
+                    a = self.ac[: r1 - r0, : c.ld_in]
+                    self._sage_layer_out(spec, Y0, a, c0, r0, r1)
+                    self._sage_grad(l, a, B0, r0, r1)
+            else:
+                self._stream(HostRows(self.host_acts[l]),
+                             lambda a, r0, r1, _l=l: self._sage_grad(_l, a, B0, r0, r1))
+        # ---- SGD (training.py:352-354) ----
+        for w, dw in zip(W, dW):
+            ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
+
     def read_stats(self) -> tuple[float, float]:
         """(loss, accuracy) of the last epoch: per-chunk sums added in chunk
         order on the host (float64)."""
@@ -494,8 +607,12 @@ def streaming_bytes(num_vertices: int, num_edges: int, model, chunk_rows: int,
     V, E = int(num_vertices), int(num_edges)
     lds = [ld_of(d) for d in model.dims]
     width = max(lds[1:-1] + ([lds[-1]] if lds[-1] <= lds[-2] else []))
+    gw = lds[-1]
+    if model.kind == "sage":
+        width = max([width] + [2 * x for x in lds[1:]])
+        gw = 2 * lds[-1]
     graph = (1 if symmetric else 2) * (8 * (V + 1) + 4 * E) + 4 * V
-    layers = 2 * 4 * V * width + (4 * V * lds[-1] if lds[-1] <= lds[-2] else 0)
+    layers = 2 * 4 * V * width + (4 * V * gw if lds[-1] <= lds[-2] else 0)
     chunks = 4 * int(chunk_rows) * (2 * max(lds) + 3 * max(lds) + 2 * lds[-1])
     return graph + layers + chunks + 4 * E * max(lds) // 64 + 16 * V
 

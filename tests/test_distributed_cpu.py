@@ -58,7 +58,21 @@ def _worker(rank, world, port, out):
     send = torch.from_numpy(sp.owned[sp.send_idx].astype(np.float32)).reshape(-1, 1).contiguous()
     recv = torch.empty((sp.halo.size, 1), dtype=torch.float32)
     comm.all_to_all_rows(recv, send, sp.recv_counts, sp.send_counts)
+    # GAT's transposed pull: partial sums over the local in-CSR's transpose,
+    # halo rows returned to their owners by the reverse exchange
+    tp, ti, tperm = sp.local_transpose()
+    srcs = np.repeat(np.arange(sp.n_local), np.diff(tp))
+    assert np.array_equal(np.repeat(np.arange(sp.n_own), np.diff(sp.in_ptr))[tperm], ti)
+    assert np.array_equal(sp.in_idx[tperm], srcs)
+    part = np.zeros(sp.n_local)
+    np.add.at(part, srcs, sp.owned[ti].astype(np.float64))
+    rsend = torch.from_numpy(part[sp.n_own:]).reshape(-1, 1).contiguous()
+    rrecv = torch.empty((sp.send_idx.size, 1), dtype=torch.float64)
+    comm.all_to_all_rows(rrecv, rsend, sp.send_counts, sp.recv_counts)
+    pulled = part[: sp.n_own].copy()
+    np.add.at(pulled, sp.send_idx, rrecv.numpy().ravel())
     np.savez(os.path.join(out, f"r{rank}.npz"), owned=sp.owned, halo=sp.halo, got=recv.numpy().ravel(),
+             pulled=pulled,
              in_ptr=sp.in_ptr, in_idx=sp.in_idx, out_ptr=sp.out_ptr, out_idx=sp.out_idx,
              recv_counts=sp.recv_counts, send_counts=sp.send_counts)
     dist.destroy_process_group()
@@ -88,6 +102,9 @@ def test_shard_plans_cover_the_graph(tmp_path, world):
             assert np.array_equal(want, have)
             outs = np.sort(g.neighbors(v))
             assert np.array_equal(outs, np.sort(local[s["out_idx"][s["out_ptr"][k]:s["out_ptr"][k + 1]]]))
+        # transposed pull + reverse exchange = sum over every out-edge
+        want = np.array([g.neighbors(u).astype(np.float64).sum() for u in s["owned"]])
+        assert np.array_equal(s["pulled"], want)
         # what r sends to t is what t receives from r
         for t, st in enumerate(shards):
             if t != r:

@@ -20,6 +20,9 @@ CASES = {
     "gcn_mean": dict(mode="mean_self_loop", F=16, H=8, C=4, L=3),      # transform-first layers
     "gcn_sym_widen": dict(mode="symmetric_norm", F=6, H=12, C=3, L=2),  # aggregate-first layer 0
     "sage": dict(mode="sage_mean", F=6, H=12, C=3, L=3),
+    # GAT: halo rows of [P | s | t], transposed pull over the local in-CSR,
+    # partial sums returned by the reverse exchange
+    "gat": dict(mode="gat", F=10, H=16, C=3, L=3),
 }
 
 

@@ -153,3 +153,60 @@ def test_streaming_from_nvme_tier(tmp_path, host_rows):
         assert abs(l1 - l2) <= 1e-5 * abs(l2)
     for i in range(3):
         assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+
+
+SAGE_CASES = [
+    # (scale, deg, F, C, L, H, directed, chunk_rows)
+    (11, 12, 48, 7, 3, 32, False, 300),     # configs[4]-like: every layer transform-first
+    (11, 12, 40, 5, 2, 24, True, 256),      # directed graph: separate backward CSR
+    (10, 16, 64, 9, 4, 32, False, 200),     # L = 4: A_2 kept on the host and streamed back
+]
+
+
+@pytest.mark.parametrize("case", SAGE_CASES)
+def test_streaming_sage_matches_resident_and_oracle(case):
+    """GraphSAGE-mean through the streaming engine: same epoch as the
+    resident layer-wise engine (1e-5) and the builder oracle (1e-4)."""
+    from oracle import sage_gat
+    scale, deg, F, C, L, H, directed, rows = case
+    g, ds, plan, model = _setup(scale, deg, F, C, L, H, "sage_mean", directed)
+    epochs, lr = 2, 0.05
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(epochs, lr, use_graph=False)
+    ss = StreamSession(ds, plan, model, chunk_rows=rows, x_cache_bytes=3 * rows * 4 * F)
+    assert ss.engine.sage and ss.engine.cache_rows == 3 * rows
+    assert any(s.n_segs for s in ss.sg.fwd_chunks)
+    if L > 3:
+        assert 2 in ss.engine.host_acts
+    m_st, tr_st = ss.train(epochs, lr)
+    for (_, l1, a1), (_, l2, a2) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+        assert abs(a1 - a2) <= 2.0 / ds.train_mask.sum()
+    W, tr_or = sage_gat.train_sage(np.asarray(ds.features, np.float64), ds.labels, ds.train_mask,
+                                   g.src_ptr, g.dst_idx, model.weights, epochs, lr)[::2]
+    for i in range(L):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+        assert rel_l2(m_st.weight_grads[i], m_ref.weight_grads[i]) < 1e-5
+        assert rel_l2(m_st.weights[i], W[i]) < 1e-4
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_or):
+        assert abs(l1 - l2) <= 1e-4 * abs(l2)
+
+
+def test_streaming_sage_from_nvme_tier(tmp_path):
+    """configs[4]'s path in small: GraphSAGE with the features in their GRIN
+    file behind HBM and host caches, read with direct I/O."""
+    from paper_2605_11517_b200.tiers import FileRows
+    g, ds, plan, model = _setup(11, 12, 64, 6, 3, 32, "sage_mean")
+    ds.save(tmp_path)
+    mm = g2.load_dataset(tmp_path, mmap_features=True)
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(2, 0.05, use_graph=False)
+    ss = StreamSession(mm, plan, model, chunk_rows=300, x_cache_bytes=600 * 64 * 4,
+                       host_cache_bytes=300 * 64 * 4)
+    assert isinstance(ss.engine.x_src, FileRows)
+    m_st, tr_st = ss.train(2, 0.05)
+    assert ss.engine.x_src.storage_bytes > 0
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+    for i in range(3):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
