@@ -810,7 +810,8 @@ extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
     if (!g.workspace || g.workspace_elems < need)
         return fail(kErrArg, "gemm: workspace needs %lld floats", (long long)need);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = grd_tc_pack_b(g.b, g.ldb, g.trans_b, g.n, g.k, g.workspace, st);
+    t.bf16 = !g.trans_a && grd_tc_bf16x3();
+    cudaError_t e = grd_tc_pack_b(g.b, g.ldb, g.trans_b, g.n, g.k, g.workspace, st, t.bf16);
     if (e == cudaSuccess) {
         t.b_packed = g.workspace;
         e = grd_tc_gemm(t, st);

@@ -19,10 +19,13 @@ struct GrdTcGemm {
     int64_t k_chunk;     // multiple of 32
     float* partial;
     const float* b_packed;   // opB pre-split by grd_tc_pack_b (then b/ldb/trans_b unused)
+    int bf16;                // bf16x3 split (row-major A, packed B); else 3xTF32
 };
 
 cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st);
 // elements needed to pack opB (n x k) into hi/lo tensor-core tiles
 int64_t grd_tc_pack_elems(int64_t n, int64_t k);
 cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,
-                          cudaStream_t st);
+                          cudaStream_t st, int bf16);
+// 1 when forward / input-gradient GEMMs use the bf16x3 split (GRD_GEMM_PREC)
+int grd_tc_bf16x3();

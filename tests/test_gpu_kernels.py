@@ -2,6 +2,9 @@
 
 from __future__ import annotations
 
+import os
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -252,3 +255,34 @@ def test_gat_kernels_match_autograd(heads, dh, scale, deg):
     assert rel_l2(dP, Pt.grad.numpy()) < 1e-6
     assert rel_l2(ge[:, hdp:hdp + heads], st.grad.numpy()) < 1e-5
     assert rel_l2(ge[:, hdp + heads:], tt.grad.numpy()) < 1e-5
+
+
+def test_gemm_bf16x3_opt_in_path():
+    """The opt-in bf16x3 forward GEMM (GRD_GEMM_PREC=bf16x3, read once per
+    process, so it runs in a child): ~4e-6 against float64 on the epilogue
+    variants; the product default stays 3xTF32 (grd_gemm_tc.cu explains why)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch
+from paper_2605_11517_b200 import ops
+rng = np.random.default_rng(3)
+dev = "cuda"
+def pad(x):
+    t = ops.zeros_rows(x.shape[0], x.shape[1], dev); t[:, :x.shape[1]] = torch.from_numpy(x).float(); return t
+worst = 0.0
+for m, n, k, tb in [(1000, 47, 13, 0), (777, 100, 300, 1), (5000, 256, 256, 0), (300, 512, 70, 0)]:
+    a = rng.normal(size=(m, k)); b = rng.normal(size=(n, k) if tb else (k, n)); c0 = rng.normal(size=(m, n))
+    rr = rng.normal(size=(m, n))
+    c = pad(c0)
+    ops.gemm(pad(a), pad(b), c, m, n, k, trans_b=bool(tb), relu_ref=pad(rr), accumulate=True)
+    want = np.where(rr > 0, c0 + a @ (b.T if tb else b), 0.0)
+    got = c[:, :n].double().cpu().numpy()
+    worst = max(worst, np.linalg.norm(got - want) / np.linalg.norm(want))
+print(worst)
+'''
+    env = dict(os.environ, GRD_GEMM_PREC="bf16x3")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd=str(Path(__file__).resolve().parents[1]), timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert float(out.stdout.strip().splitlines()[-1]) < 2e-5
