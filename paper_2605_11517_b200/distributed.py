@@ -191,16 +191,20 @@ class Communicator:
                                     group=self.group)
         return _Requests(ids=recv.cpu().numpy(), counts=rc.astype(np.int64))
 
-    def all_to_all_rows(self, recv, send, recv_counts, send_counts) -> None:
-        """Row all-to-all of contiguous 2-D tensors (rows split by rank)."""
+    def all_to_all_rows(self, recv, send, recv_counts, send_counts, async_op: bool = False):
+        """Row all-to-all of contiguous 2-D tensors (rows split by rank).
+        ``async_op``: NCCL returns the work handle (``wait()`` makes the
+        current stream wait for it); host-staged gloo completes before
+        returning (None)."""
         rs = [int(x) for x in recv_counts]
         ss = [int(x) for x in send_counts]
         if self.device_native:
-            self.dist.all_to_all_single(recv, send, rs, ss, group=self.group)
-            return
+            work = self.dist.all_to_all_single(recv, send, rs, ss, group=self.group, async_op=async_op)
+            return work if async_op else None
         r_host = recv.new_empty(recv.shape, device="cpu")
         self.dist.all_to_all_single(r_host, send.cpu(), rs, ss, group=self.group)
         recv.copy_(r_host)
+        return None
 
     def all_reduce_sum(self, t) -> None:
         if self.device_native:

@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 from . import _lib, ops
+from .distributed import _csr_rows
 from .ops import AggSpec, ld_of
 
 __all__ = ["DeviceGraph", "DevicePartition", "LayerOps", "LayerwiseEngine", "PartitionEngine",
@@ -98,6 +99,11 @@ class DeviceGraph:
         """Rows of a per-vertex host array in this device's row order."""
         return arr
 
+    def exchange_agg(self, which: str, y: torch.Tensor, out: torch.Tensor, width: int, **kw) -> None:
+        """``agg_sum`` over the ``which`` ("fwd" / "bwd") CSR reading ``y``,
+        after its halo rows are filled (sharded: overlapped, see below)."""
+        ops.agg_sum(getattr(self, which), y, out, width, **kw)
+
     def gat_pull(self):
         """(spec, edge_perm) of GAT's transposed pull: the graph's out-CSR
         with each out-edge's position in the forward in-CSR."""
@@ -157,17 +163,60 @@ class ShardDeviceGraph(DeviceGraph):
         return t[: rows * ld].view(rows, ld)
 
     def exchange(self, buf: torch.Tensor, width: int) -> None:
+        self._exchange_finish(self._exchange_start(buf, width), buf, width)
+
+    def _exchange_start(self, buf: torch.Tensor, width: int):
+        """Pack the rows other ranks need and start the all-to-all."""
         ld = ld_of(width)
         send = self._buf("send", self.n_send, ld)
         recv = self._buf("recv", self.n_recv, ld)
         if self.n_send:
             ops.gather_rows(buf, self.send_idx, send, width)
-        self.comm.all_to_all_rows(recv, send, self.shard.recv_counts, self.shard.send_counts)
+        return self.comm.all_to_all_rows(recv, send, self.shard.recv_counts, self.shard.send_counts,
+                                         async_op=True)
+
+    def _exchange_finish(self, work, buf: torch.Tensor, width: int) -> None:
+        """Wait for the all-to-all (a stream wait under NCCL) and unpack the
+        received rows into the halo block."""
+        if work is not None:
+            work.wait()
         if self.n_recv:
+            recv = self._buf("recv", self.n_recv, ld_of(width))
             ops.gather_rows(recv, self.recv_ident, buf[self.n_own:], width)
 
     def local_rows(self, arr: np.ndarray) -> np.ndarray:
         return arr[self.shard.local_ids]
+
+    def _split(self, which: str):
+        """(interior, boundary) row subsets of the fwd / bwd CSR: interior
+        rows read owned rows only, so they run while the halo is in flight."""
+        key = "_split_" + which
+        sp = getattr(self, key, None)
+        if sp is None:
+            sh = self.shard
+            ptr, idx = (sh.in_ptr, sh.in_idx) if which == "fwd" else (sh.out_ptr, sh.out_idx)
+            n = ptr.size - 1
+            rows_of = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
+            halo = np.bincount(rows_of[idx >= self.n_own], minlength=n) > 0
+            sp = []
+            for rows in (np.flatnonzero(~halo), np.flatnonzero(halo)):
+                p2, i2 = _csr_rows(ptr, idx, rows)
+                sp.append(AggSpec.build(p2, i2, self.device, out_idx=rows.astype(np.int32)))
+            sp = tuple(sp)
+            setattr(self, key, sp)
+        return sp
+
+    def exchange_agg(self, which: str, y: torch.Tensor, out: torch.Tensor, width: int, **kw) -> None:
+        """Halo exchange of ``y`` overlapped with the aggregation of the
+        interior rows (NCCL: the all-to-all runs on its own stream while the
+        interior rows aggregate; gloo: synchronous), then the boundary rows."""
+        interior, boundary = self._split(which)
+        work = self._exchange_start(y, width)
+        if interior.n_rows:
+            ops.agg_sum(interior, y, out, width, **kw)
+        self._exchange_finish(work, y, width)
+        if boundary.n_rows:
+            ops.agg_sum(boundary, y, out, width, **kw)
 
     def gat_pull(self):
         if getattr(self, "_gat_pull", None) is None:
@@ -476,18 +525,19 @@ class LayerwiseEngine(_EngineBase):
         s = dg.scale("s") if c.sym else None
         if c.transform_first:
             ops.gemm(x, W, self.t1, self.V, c.d_out, c.d_in, row_scale=s)
-            dg.exchange(self.t1, c.d_out)          # halo rows of P = X W
-            ops.agg_sum(dg.fwd, self.t1, out, c.d_out, post_div_deg=not c.sym, post_scale=s, relu=relu)
+            # halo rows of P = X W, overlapped with the interior rows
+            dg.exchange_agg("fwd", self.t1, out, c.d_out, post_div_deg=not c.sym, post_scale=s, relu=relu)
         else:
-            self._input_halo(l, x)
-            ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
+            self._input_agg(l, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
             ops.gemm(self.t1, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
 
-    def _input_halo(self, l: int, x: torch.Tensor) -> None:
+    def _input_agg(self, l: int, x: torch.Tensor, out: torch.Tensor, width: int, **kw) -> None:
         """Aggregate-first layers read the layer input's halo rows (the
         features' halo is filled once at upload)."""
         if l > 0:
-            self.dg.exchange(x, self.cfg[l].d_in)
+            self.dg.exchange_agg("fwd", x, out, width, **kw)
+        else:
+            ops.agg_sum(self.dg.fwd, x, out, width, **kw)
 
     def _w(self, W):
         """SGD target of a weight-gradient call (None: deferred past the all-reduce)."""
@@ -502,14 +552,12 @@ class LayerwiseEngine(_EngineBase):
             # Y = X [W_root | W_nbr] (one GEMM), out = Y_root + mean_in(Y_nbr)
             y = self.t1[:, : 2 * c.ld_out]
             ops.gemm(x, W, y, self.V, 2 * c.ld_out, c.d_in)
-            dg.exchange(y[:, c.ld_out:], c.d_out)   # halo rows of X W_nbr
-            ops.agg_sum(dg.fwd, y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
-                        add_y=y[:, : c.ld_out], relu=relu)
+            dg.exchange_agg("fwd", y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
+                            add_y=y[:, : c.ld_out], relu=relu)      # halo rows of X W_nbr
         else:
             # N = mean_in(X), out = X W_root + N W_nbr
             n = self.t1[:, : c.ld_in]
-            self._input_halo(l, x)
-            ops.agg_sum(dg.fwd, x, n, c.d_in, post_div_deg=2, no_self=True)
+            self._input_agg(l, x, n, c.d_in, post_div_deg=2, no_self=True)
             ops.gemm(x, W[:, : c.ld_out], out, self.V, c.d_out, c.d_in)
             ops.gemm(n, W[:, c.ld_out:], out, self.V, c.d_out, c.d_in, accumulate=True, relu_out=relu)
 
@@ -523,9 +571,8 @@ class LayerwiseEngine(_EngineBase):
         if c.transform_first:
             # [gp | H_nbr] with H_nbr = mean_in^T gp (pull over out-edges, 1/deg_v per edge)
             gcat = self.g[:, : 2 * c.ld_out]
-            dg.exchange(gcat[:, : c.ld_out], c.d_out)   # halo rows of gp
-            ops.agg_sum(dg.bwd, gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
-                        no_self=True)
+            dg.exchange_agg("bwd", gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
+                            no_self=True)                          # halo rows of gp
             if l > 0:
                 ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
             ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=self._w(W), lr=lr)
@@ -536,8 +583,7 @@ class LayerwiseEngine(_EngineBase):
             if l > 0:
                 gn = self.t2[:, : c.ld_in]
                 ops.gemm(gp, W[:, c.ld_out:], gn, self.V, c.d_in, c.d_out, trans_b=True)
-                dg.exchange(gn, c.d_in)                  # halo rows of gp W_nbr^T
-                ops.agg_sum(dg.bwd, gn, self.h, c.d_in, src_scale=inv_deg, no_self=True)
+                dg.exchange_agg("bwd", gn, self.h, c.d_in, src_scale=inv_deg, no_self=True)
                 ops.gemm(gp, W[:, : c.ld_out], self.h, self.V, c.d_in, c.d_out, trans_b=True,
                          accumulate=True, relu_ref=ref)
             ops.wgrad_sgd(x, gp, dW[:, : c.ld_out], c.d_in, c.d_out, self.V, w=self._w(W[:, : c.ld_out]),
@@ -677,8 +723,7 @@ class LayerwiseEngine(_EngineBase):
             dmask = self.dmask[l]
             if c.transform_first:
                 # H = A_hat^T (gp * pre_scale)
-                dg.exchange(self.g, c.d_out)
-                ops.agg_sum(dg.bwd, self.g, self.h, c.d_out, post_scale=s)
+                dg.exchange_agg("bwd", self.g, self.h, c.d_out, post_scale=s)
                 if l > 0:
                     ops.gemm(self.h, W, self.g, self.V, c.d_in, c.d_out, trans_b=True,
                              row_scale=prev[1], elem_mul=dmask, relu_ref=prev[0])
@@ -691,10 +736,9 @@ class LayerwiseEngine(_EngineBase):
                          row_scale=dg.scale(c.pre_scale))
                 ops.wgrad_sgd(self.t1, self.g, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
                 if l > 0:
-                    dg.exchange(self.h, c.d_in)
                     post = self._combine(s is not None, prev[1])
-                    ops.agg_sum(dg.bwd, self.h, self.g, c.d_in, post_scale=post,
-                                mask_ref=None if dmask is not None else prev[0])
+                    dg.exchange_agg("bwd", self.h, self.g, c.d_in, post_scale=post,
+                                    mask_ref=None if dmask is not None else prev[0])
                     if dmask is not None:
                         ops.mul_rows(self.g, dmask, self.g, self.V, c.d_in)
                         if prev[0] is not None:
