@@ -52,3 +52,18 @@ for (m, n, k, tb) in SHAPES:
                                       tflops=round(2 * m * n * k / ms / 1e9, 1),
                                       GBs=round(4 * (m * k + m * n) / ms / 1e6, 1))
 print(json.dumps(res, indent=1))
+
+# weight-gradient GEMMs (split-K, MN-major operands), always 3xTF32
+wg = {}
+for (m, n, k) in [(256, 512, 2097152), (100, 256, 2097152), (256, 96, 2097152), (1024, 512, 1048576)]:
+    a = torch.rand(k, (m + 3) // 4 * 4, device=dev) - 0.5
+    b = torch.rand(k, (n + 3) // 4 * 4, device=dev) - 0.5
+    dw = torch.zeros(m, (n + 3) // 4 * 4, device=dev)
+    ms = timeit(lambda: ops.wgrad_sgd(a, b, dw, m, n, k), reps=5)
+    r = min(k, 262144)
+    ops.wgrad_sgd(a[:r], b[:r], dw, m, n, r)
+    ref = a[:r, :m].double().T @ b[:r, :n].double()
+    err = float((dw[:, :n].double() - ref).norm() / ref.norm())
+    wg[f"wgrad {m}x{n} K={k}"] = dict(ms=round(ms, 4), rel_err=err,
+                                     GBs=round(4 * k * (m + n) / ms / 1e6, 1))
+print(json.dumps(wg, indent=1))
