@@ -66,6 +66,7 @@ struct Params {
     int splits;
     int stages;
     int cluster;                    // CTAs per cluster along M (1, 2, 4)
+    int pair;                       // 1: cluster of 2 = a cta_group::2 pair (M = 256)
     float* c; int64_t ldc;
     const float* row_scale;
     const float* elem_mul; int64_t ld_elem_mul;
@@ -91,10 +92,10 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // kind::tf32, D fp32, M = 128, N = bn; a/b major: 0 = K, 1 = MN.
-__device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn) {
+__device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn, int m = kBM) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
            (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(bn >> 3) << 17) |
-           (static_cast<uint32_t>(kBM >> 4) << 24);
+           (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -151,6 +152,29 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
         "h"(mask)
+        : "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// CTA-pair (cta_group::2) MMA: issued by the even CTA; A rows 0-127 / 128-255
+// and B rows [0, N/2) / [N/2, N) come from the two CTAs' shared memory at the
+// same offsets; each CTA's TMEM receives its 128 rows x N.
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
         : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -297,7 +321,7 @@ __device__ __forceinline__ void epi_store_direct(const Params& p, const float (&
 
 // Epilogue warps' loop over the tiles of this CTA (both kernels): TMEM
 // accumulator `acc` of the i-th tile with K work, drained chunk by chunk.
-template <class TileFn>
+template <bool kPair, class TileFn>
 __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
                                               int warp, int lane, int64_t t0, int64_t tstep,
                                               int64_t ntiles, TileFn tile_of) {
@@ -332,12 +356,16 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
         }
         if (has_k) {
             asm volatile("tcgen05.fence::before_thread_sync;");
-            mbar_arrive(tempty + acc);
+            if (kPair) mbar_arrive_cluster(tempty + acc, 0);
+            else mbar_arrive(tempty + acc);
             ++i;
         }
     }
 }
 
+// kPair: a kernel containing cta_group::2 instructions must be launched in
+// clusters of 2, so the CTA-pair variant is its own instantiation.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const Params p) {
@@ -345,8 +373,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int bn = p.bn;
     const int S = p.stages;
+    constexpr bool pair = kPair;
+    const int bnl = pair ? bn / 2 : bn;                      // B rows staged by this CTA
     const uint32_t a_bytes = kBM * 128u;
-    const uint32_t b_bytes = static_cast<uint32_t>(bn) * 128u;
+    const uint32_t b_bytes = static_cast<uint32_t>(bnl) * 128u;
     // stage: A hi | A lo | B hi | B lo | [A raw] | [B raw]  (raw only for MN-major)
     const uint32_t stage_bytes = 2u * (a_bytes + b_bytes);   // A hi | A lo | B hi | B lo
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
@@ -372,19 +402,31 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
 
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     if (threadIdx.x == 32) {
+        // pair: the even CTA's conv / tempty barriers collect both CTAs'
+        // converters / epilogue threads; its commits arrive on both CTAs'
+        // empty / tfull barriers
+        const uint32_t nc = pair ? 2u : 1u;
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(conv + s, kConvThreads);
-            mbar_init(empty + s, static_cast<uint32_t>(C));
+            mbar_init(conv + s, kConvThreads * nc);
+            mbar_init(empty + s, pair ? 1u : static_cast<uint32_t>(C));
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, 128 * nc);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
@@ -427,7 +469,23 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                    static_cast<int32_t>(k0), full + s);
                     }
                     uint8_t* bdst = st + 2 * a_bytes;
-                    if (p.b_mode == kPacked) {
+                    if (pair) {
+                        // this CTA's half of the B tile: rows [crank * bnl, +bnl)
+                        const int64_t nb0 = n0 + crank * bnl;
+                        if (p.b_mode == kPacked) {
+                            const int64_t nkb_all = (p.k + kBK - 1) / kBK;
+                            const float* src = p.b_packed + (ntile * nkb_all + k0 / kBK) * (2 * int64_t(bn) * kBK);
+                            bulk_copy(bdst, src + int64_t(crank) * bnl * kBK, b_bytes, full + s);
+                            bulk_copy(bdst + b_bytes, src + int64_t(bn) * kBK + int64_t(crank) * bnl * kBK, b_bytes,
+                                      full + s);
+                        } else if (p.b_mode == kKMajorTma) {
+                            tma_2d(bdst, &map_b, static_cast<int32_t>(k0), static_cast<int32_t>(nb0), full + s);
+                        } else {
+                            for (int j = 0; j < bnl / 32; ++j)
+                                tma_2d(bdst + j * 4096, &map_b, static_cast<int32_t>(nb0 + 32 * j),
+                                       static_cast<int32_t>(k0), full + s);
+                        }
+                    } else if (p.b_mode == kPacked) {
                         const int64_t kbg = (k0 / kBK);
                         const int64_t nkb_all = (p.k + kBK - 1) / kBK;
                         const float* src = p.b_packed + (ntile * nkb_all + kbg) * (2 * int64_t(bn) * kBK);
@@ -455,14 +513,14 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
     } else if (warp == 1) {
         // ------------------------------------------------- MMA issuer --
-        if (lane == 0) {
+        if (lane == 0 && (!pair || crank == 0)) {
             // K-major: SW128, advance 32 B per 8-deep MMA inside the 128 B row.
             // MN-major: SW128_32B atoms of 32 MN x 4 K rows, LBO = 4 KB between
             // 32-wide MN atoms, SBO = 512 B between 4-row K groups, advance
             // 1024 B (8 K rows) per MMA.
             const int a_mn = p.a_mode == kMNMajorTma;
             const int b_mn = p.b_mode == kMNMajorTma;
-            const uint32_t idesc = make_idesc(bn, a_mn, b_mn);
+            const uint32_t idesc = make_idesc(bn, a_mn, b_mn, pair ? 2 * kBM : kBM);
             const uint32_t a_step = a_mn ? 1024u : 32u, b_step = b_mn ? 1024u : 32u;
             const uint32_t a_lbo = a_mn ? 4096u : 16u, b_lbo = b_mn ? 4096u : 16u;
             const uint32_t a_sbo = a_mn ? 512u : 1024u, b_sbo = b_mn ? 512u : 1024u;
@@ -490,14 +548,22 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo, a_lay);
                         const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo, b_lay);
                         const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo, b_lay);
-                        mma_tf32(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-                        mma_tf32(tacc, dah, dbl, idesc, 1u);
-                        mma_tf32(tacc, dah, dbh, idesc, 1u);
+                        if constexpr (kPair) {
+                            mma_tf32_pair(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                            mma_tf32_pair(tacc, dah, dbl, idesc, 1u);
+                            mma_tf32_pair(tacc, dah, dbh, idesc, 1u);
+                        } else {
+                            mma_tf32(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                            mma_tf32(tacc, dah, dbl, idesc, 1u);
+                            mma_tf32(tacc, dah, dbh, idesc, 1u);
+                        }
                     }
-                    if (C == 1) mma_commit(empty + s);
+                    if constexpr (kPair) mma_commit_pair(empty + s);   // both CTAs' stage s
+                    else if (C == 1) mma_commit(empty + s);
                     else mma_commit_mc(empty + s, cmask);   // release the stage in every CTA
                 }
-                mma_commit(tfull + acc);
+                if constexpr (kPair) mma_commit_pair(tfull + acc);   // both CTAs' accumulators
+                else mma_commit(tfull + acc);
                 ++i;
             }
         }
@@ -516,12 +582,13 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 uint8_t* bh = st + 2 * a_bytes;
                 if (p.b_mode != kPacked) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(conv + s);
+                if (pair) mbar_arrive_cluster(conv + s, 0);     // the issuing CTA's barrier
+                else mbar_arrive(conv + s);
             }
         }
     } else {
         // ---------------------------------------------------- epilogue --
-        epilogue_loop(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles,
+        epilogue_loop<kPair>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles,
                       [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
                           z = static_cast<int>(t / (mg * nt));
                           const int64_t r = t % (mg * nt);
@@ -534,7 +601,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     __syncthreads();
     if (C > 1) cluster_sync();     // no peer still multicasts into this CTA
     if (warp == 0) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+        if constexpr (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
     }
 }
 
@@ -731,7 +801,7 @@ gemm_bf16x3_ws(const __grid_constant__ CUtensorMap map_a, const Params p) {
             }
         }
     } else {
-        epilogue_loop(p, tmem, tfull, tempty, warp, lane, blockIdx.x, gridDim.x,
+        epilogue_loop<false>(p, tmem, tfull, tempty, warp, lane, blockIdx.x, gridDim.x,
                       ntiles, [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
                           m0 = (t / nt) * kBM;
                           n0 = (t % nt) * bn;
@@ -847,6 +917,16 @@ inline int pick_bn(int64_t n) {
     if (n > 128) return static_cast<int>((n + 31) / 32 * 32);
     int bn = static_cast<int>((n + 15) / 16 * 16);
     return bn < 16 ? 16 : bn;
+}
+
+// CTA pairs (cta_group::2, M = 256 per pair): GRD_GEMM_PAIR = 1 / 0
+inline int pair_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_PAIR");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
 }
 
 // CTAs per cluster sharing the B operand (GRD_GEMM_CLUSTER = 1, 2 or 4)
@@ -978,7 +1058,13 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32, true)) return cudaErrorInvalidValue;
     }
     if (p.b_mode == kMNMajorTma) p.bn = (p.bn + 31) / 32 * 32;   // whole 32-wide TMA atoms
-    const uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.bn) * 128u);
+    const int64_t mt0 = (g.m + kBM - 1) / kBM;
+    // a CTA pair stages half of B each: halves of whole 32-row atoms
+    p.pair = (pair_pref() && p.bn % 64 == 0 && mt0 >= 2) ? 1 : 0;
+    if (p.pair && p.b_mode == kKMajorTma &&
+        !make_map(&map_b, g.b, g.n, g.k, g.ldb, 32, static_cast<uint32_t>(p.bn / 2)))
+        return cudaErrorInvalidValue;
+    const uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.pair ? p.bn / 2 : p.bn) * 128u);
     p.stages = static_cast<int>((220u * 1024u) / stage);
     if (p.stages > 4) p.stages = 4;
     if (p.stages < 2) p.stages = 2;
@@ -986,8 +1072,10 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gemm_tf32x3_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -995,12 +1083,13 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     int C = cluster_pref();
     while (C > 1 && mt < C) C >>= 1;               // at most the last group has idle CTAs
     if (p.b_mode == kKMajorTma) C = 1;
+    if (p.pair) C = 2;
     p.cluster = C;
     const int64_t tiles = ((mt + C - 1) / C) * ((g.n + p.bn - 1) / p.bn) * p.splits;
     const int64_t max_cl = num_sms() / C;
     const int grid = static_cast<int>((tiles < max_cl ? tiles : max_cl) * C);
     if (C == 1) {
-        gemm_tf32x3_ws<<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        gemm_tf32x3_ws<false><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -1015,7 +1104,8 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     attr_c[0].val.clusterDim.z = 1;
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws, map_a, map_b, p);
+    if (p.pair) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true>, map_a, map_b, p);
+    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false>, map_a, map_b, p);
 }
 
 cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,
