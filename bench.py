@@ -179,8 +179,13 @@ def run_ours(args, spec, rank, world, local_rank):
     from paper_2605_11517_b200 import ops
     from paper_2605_11517_b200.training import session_for
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # GRD_BENCH_BACKEND=gloo lets the multi-rank path run with every rank on
+    # one GPU (a functional check of this script's N > 1 logic on a 1-GPU
+    # box); production runs use NCCL with one GPU per rank
+    backend = os.environ.get("GRD_BENCH_BACKEND", "nccl")
+    gpu = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     need = spec.get("host_gb")
     if need:
         import psutil
@@ -189,7 +194,10 @@ def run_ours(args, spec, rank, world, local_rank):
             raise SystemExit(f"workload {args.workload} needs ~{need} GiB of host memory, "
                              f"{have:.0f} GiB available")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     g, ds, plan, model, prep = build_workload(spec)
     L, E = spec["L"], g.num_edges
     if spec.get("tier") == "nvme":
@@ -237,7 +245,7 @@ def run_ours(args, spec, rank, world, local_rank):
         flush_l2(flush)
         sess.run_epoch(w, LR)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -456,6 +464,10 @@ def main():
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     rank, world, local_rank = rank_info()
+    if world > 1 and os.environ.get("OMP_NUM_THREADS") == "1":
+        # torchrun pins every rank to one OpenMP thread; the native
+        # preprocessing (generator, partitioner, plan) gets its share of cores
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // world))
     spec = WORKLOADS[args.workload]
     if args.impl == "reference":
         out = run_reference(args, spec, rank, world)
