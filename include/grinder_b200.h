@@ -260,10 +260,20 @@ typedef struct grd_gat_args {
     float* delta_self;
     float* grad_ext;               /* dL/dP_ext: s and t columns written here */
     int64_t ld_gext;
+    const float* st;               /* optional compact scores [rows, ld_st] for
+                                      grd_gat_softmax: s_u in columns 0..H-1, t_v in H..2H-1
+                                      (grd_gat_pack_scores); null: p_ext's s / t columns.
+                                      The backward reads s_u beside the P_u row it gathers. */
+    int64_t ld_st;
 } grd_gat_args;
 int grd_gat_softmax(const grd_gat_args* args, void* stream);
 int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream);
 int grd_gat_src_grad(const grd_gat_args* args, void* stream);
+/* st[r, 0:2H] = p_ext[r, hdp : hdp + 2H]: the per-vertex attention scores as
+ * one 32-byte row each (H = 4), so the edge-softmax's per-edge score gathers
+ * hit a table that stays in L2 instead of one line of a wide P_ext row each. */
+int grd_gat_pack_scores(const float* p_ext, int64_t ld_ext, int64_t n_rows, int32_t heads,
+                        int32_t hdp, float* st, int64_t ld_st, void* stream);
 /* W_ext = [W | W a_src | W a_dst] (att = [a_src; a_dst], each heads x dhp). */
 int grd_gat_build_wext(const float* w, int64_t ldw, const float* att, int64_t d_in,
                        int32_t heads, int32_t dh, int32_t dhp, float* wext,

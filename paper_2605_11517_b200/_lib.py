@@ -103,6 +103,8 @@ class GrdGatArgs(ctypes.Structure):
         ("delta_self", c_vp),
         ("grad_ext", c_vp),
         ("ld_gext", c_i64),
+        ("st", c_vp),
+        ("ld_st", c_i64),
     ]
 
 
@@ -159,6 +161,7 @@ SIGNATURES = {
     "grd_gat_softmax": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
     "grd_gat_softmax_bwd": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
     "grd_gat_src_grad": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_pack_scores": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp]),
     "grd_gat_build_wext": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp]),
     "grd_gat_param_grads": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp,
                                     c_vp, c_f32, c_vp]),

@@ -123,7 +123,7 @@ __device__ __forceinline__ void unit_scores(const grd_gat_args& a, const Unit& u
     const int64_t ne = un.end - un.beg;
     const int64_t n = ne + (un.self ? 1 : 0);
     float tv[HM];
-    load_heads<HM>(a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H, H, tv);
+    load_heads<HM>(a.st ? a.st + int64_t(v) * a.ld_st + H : a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H, H, tv);
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
         const int64_t i = lane + kWarp * it;
@@ -134,7 +134,7 @@ __device__ __forceinline__ void unit_scores(const grd_gat_args& a, const Unit& u
         }
         const int32_t u = i < ne ? a.idx[un.beg + i] : v;
         float su[HM];
-        load_heads<HM>(a.p_ext + int64_t(u) * a.ld_ext + a.hdp, H, su);
+        load_heads<HM>(a.st ? a.st + int64_t(u) * a.ld_st : a.p_ext + int64_t(u) * a.ld_ext + a.hdp, H, su);
 #pragma unroll
         for (int h = 0; h < HM; ++h) z[it][h] = (i < n && h < H) ? lrelu(su[h] + tv[h], a.slope) : -INFINITY;
     }
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
         float s_my = 0.f, al_my = 0.f;
         if (mine) {
             const int32_t u = im < ne ? a.idx[un.beg + im] : v;
-            s_my = a.p_ext[int64_t(u) * a.ld_ext + a.hdp + my_h];
+            s_my = a.p_ext[int64_t(u) * a.ld_ext + a.hdp + my_h];   // beside the gathered P_u row
             al_my = im < ne ? a.alpha[(un.beg + im) * H + my_h] : a.alpha_self[int64_t(v) * H + my_h];
         }
 #pragma unroll
@@ -550,6 +550,28 @@ extern "C" int grd_gat_src_grad(const grd_gat_args* args, void* stream) {
     if (rc || args->n_heavy == 0) return rc;
     gat_heavy_sum_kernel<<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args, args->hdp);
     return launch_status("gat_heavy_sum");
+}
+
+__global__ void gat_pack_scores_kernel(const float* __restrict__ p_ext, int64_t ld_ext, int64_t n_rows, int H,
+                                       int hdp, float* __restrict__ st, int64_t ld_st) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int w = 2 * H;
+    if (i >= n_rows * w) return;
+    const int64_t r = i / w;
+    const int c = static_cast<int>(i % w);
+    st[r * ld_st + c] = p_ext[r * ld_ext + hdp + c];
+}
+
+extern "C" int grd_gat_pack_scores(const float* p_ext, int64_t ld_ext, int64_t n_rows, int32_t heads, int32_t hdp,
+                                   float* st, int64_t ld_st, void* stream) {
+    clear_error();
+    if (!p_ext || !st || heads < 1 || heads > kMaxHeads || ld_st < 2 * heads || n_rows < 0)
+        return fail(kErrArg, "gat_pack_scores: bad arguments");
+    if (n_rows == 0) return 0;
+    const int64_t n = n_rows * 2 * heads;
+    gat_pack_scores_kernel<<<blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(p_ext, ld_ext, n_rows, heads,
+                                                                                      hdp, st, ld_st);
+    return launch_status("gat_pack_scores");
 }
 
 extern "C" int grd_gat_build_wext(const float* w, int64_t ldw, const float* att, int64_t d_in, int32_t heads,

@@ -602,6 +602,9 @@ class LayerwiseEngine(_EngineBase):
         self.alpha_self = torch.zeros(self.NL * H, dtype=torch.float32, device=dev)
         self.delta_self = torch.zeros_like(self.alpha_self)
         self.pull, self.edge_perm = dg.gat_pull()
+        # compact [s | t] score table (32 B per vertex at 4 heads): the
+        # edge-softmax's per-edge score gathers stay in L2
+        self.st = ops.zeros_rows(self.NL, 2 * H, dev)
         # t2: the last layer's per-head aggregate O (kept for the backward's
         # gO.O term); t3: its per-head upstream gradient
         hdp = self.cfg[-1].hdp
@@ -618,7 +621,8 @@ class LayerwiseEngine(_EngineBase):
         pext = self.t1[:, : c.ld_ext]
         ops.gemm(x, wt.wext[l], pext, self.V, c.n_ext, c.d_in)
         dg.exchange(pext, c.n_ext)                # halo rows of [P | s | t]
-        ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self)
+        ops.gat_pack_scores(pext, self.NL, c.heads, c.dhp, self.st)
+        ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, st=self.st)
         return pext
 
     def _forward_gat(self, l: int, x: torch.Tensor, out: torch.Tensor) -> None:
@@ -643,7 +647,7 @@ class LayerwiseEngine(_EngineBase):
         pext = self._gat_transform(l, x)
         gext = self.h[:, : c.ld_ext]
         ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go, o_fwd,
-                            self.delta, self.delta_self, gext)
+                            self.delta, self.delta_self, gext)   # s_u beside the gathered P_u row
         if self.NL > self.V:
             go[self.V:].zero_()    # halo rows: no self term, no stale gradient
         # dP_u = sum_v alpha_uv gO_v and ds_u = sum_v delta_uv over u's out-edges

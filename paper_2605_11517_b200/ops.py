@@ -327,9 +327,19 @@ def _gat_args(spec: AggSpec, p_ext, heads, dhp, **kw):
     return a
 
 
-def gat_softmax(spec, p_ext, heads, dhp, alpha, alpha_self) -> None:
-    """alpha = edge softmax of LeakyReLU(s_u + t_v) over in(v) + self loop."""
-    a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self)
+def gat_pack_scores(p_ext, n_rows, heads, dhp, st) -> None:
+    """st[:, 0:2H] = [s | t] columns of P_ext (compact score table)."""
+    H = int(heads)
+    _launch("gat_params", 1, 4 * int(n_rows) * 4 * H, 0, lambda: _lib.check(_lib.lib().grd_gat_pack_scores(
+        _p(p_ext), _ld(p_ext), int(n_rows), H, H * int(dhp), _p(st), _ld(st), stream_ptr()),
+        "gat_pack_scores"))
+
+
+def gat_softmax(spec, p_ext, heads, dhp, alpha, alpha_self, st=None) -> None:
+    """alpha = edge softmax of LeakyReLU(s_u + t_v) over in(v) + self loop
+    (scores from the compact table ``st`` when given)."""
+    kw = {} if st is None else dict(st=st, ld_st=_ld(st))
+    a = _gat_args(spec, p_ext, heads, dhp, alpha=alpha, alpha_self=alpha_self, **kw)
     E, R = spec.nnz, spec.n_rows
     # idx + s_u sector per edge, t_v per row, alpha written
     nbytes = 8 * (R + 1) + 4 * E + 4 * heads * (E + R) * 2 + 4 * heads * R

@@ -222,8 +222,18 @@ class TrainSession:
                 w.copy_(s)
         torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            eng.epoch(lr)
+        # no garbage collection while capturing (a finalizer's CUDA call, e.g.
+        # cudaHostUnregister of a collected array, would invalidate the
+        # capture), and other threads' CUDA calls do not count against it
+        import gc
+        gc_was = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                eng.epoch(lr)
+        finally:
+            if gc_was:
+                gc.enable()
         self._graph, self._graph_lr = g, lr
 
     def run_epoch(self, epoch: int, lr: float, use_graph: bool = True) -> None:

@@ -193,10 +193,12 @@ def test_rownorm_kernels():
 
 @pytest.mark.parametrize("heads,dh,scale,deg", [(2, 4, 9, 8), (2, 5, 9, 8), (4, 16, 9, 8), (1, 7, 9, 8),
                                                 (4, 64, 12, 16), (8, 8, 12, 16), (3, 12, 11, 24)])
-def test_gat_kernels_match_autograd(heads, dh, scale, deg):
+@pytest.mark.parametrize("use_st", [False, True])
+def test_gat_kernels_match_autograd(heads, dh, scale, deg, use_st):
     """Edge softmax forward/backward, the weighted pulls and the score
     gradients against torch float64 autograd of the same layer (the larger
-    graphs have hub rows above the 128-edge segmentation threshold)."""
+    graphs have hub rows above the 128-edge segmentation threshold); scores
+    read from P_ext's columns or from the packed [s | t] table."""
     from paper_2605_11517_b200 import generate_kronecker
     from paper_2605_11517_b200.engine import DeviceGraph
     g = generate_kronecker(scale, deg, seed=2)
@@ -223,7 +225,14 @@ def test_gat_kernels_match_autograd(heads, dh, scale, deg):
     alpha = torch.zeros(E * heads, device=DEV)
     alpha_self = torch.zeros(n * heads, device=DEV)
     pe = _dev(pext)
-    ops.gat_softmax(dg.fwd, pe, heads, dhp, alpha, alpha_self)
+    st_tab = None
+    if use_st:
+        st_tab = ops.zeros_rows(n, 2 * heads, DEV)
+        ops.gat_pack_scores(pe, n, heads, dhp, st_tab)
+        pe[:, hdp:hdp + 2 * heads] = float("nan")   # the softmax must not read P_ext's scores
+    ops.gat_softmax(dg.fwd, pe, heads, dhp, alpha, alpha_self, st=st_tab)
+    if use_st:
+        pe[:, hdp:hdp + 2 * heads] = torch.from_numpy(pext[:, hdp:]).float().to(DEV)   # bwd reads them
     O = ops.zeros_rows(n, hdp, DEV)
     ops.agg_sum(dg.fwd, pe[:, :hdp], O, hdp, edge_w=alpha, self_w=alpha_self, heads=heads, head_ld=dhp)
     dlt, dlt_s = torch.zeros_like(alpha), torch.zeros_like(alpha_self)
