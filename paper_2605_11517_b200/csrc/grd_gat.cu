@@ -154,7 +154,25 @@ __device__ __forceinline__ void write_alpha(const grd_gat_args& a, const Unit& u
         float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
 #pragma unroll
         for (int h = 0; h < HM; ++h)
-            if (h < H) dst[h] = expf(z[it][h] - mx[h]) * inv[h];
+            if (h < H) dst[h] = __expf(z[it][h] - mx[h]) * inv[h];
+    }
+}
+
+// light rows: z already holds exp(z - max) (computed once for the sum)
+template <int HM>
+__device__ __forceinline__ void write_alpha_e(const grd_gat_args& a, const Unit& un, int32_t v, int lane,
+                                              const float (&e)[kItems][HM], const float (&inv)[HM]) {
+    const int H = a.heads;
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (un.self ? 1 : 0);
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const int64_t i = lane + kWarp * it;
+        if (i >= n) continue;
+        float* dst = i < ne ? a.alpha + (un.beg + i) * H : a.alpha_self + int64_t(v) * H;
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H) dst[h] = e[it][h] * inv[h];
     }
 }
 
@@ -181,8 +199,12 @@ __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
         mx[h] = warp_max(mx[h]);
         sm[h] = 0.f;
 #pragma unroll
-        for (int it = 0; it < kItems; ++it)
-            if (h < H && lane + kWarp * it < n) sm[h] += expf(z[it][h] - mx[h]);
+        for (int it = 0; it < kItems; ++it) {
+            // exp once (fast ex2 path); z keeps it for the normalisation below
+            const float e = (h < H && lane + kWarp * it < n) ? __expf(z[it][h] - mx[h]) : 0.f;
+            z[it][h] = e;
+            sm[h] += e;
+        }
         sm[h] = warp_sum(sm[h]);
     }
     if (un.seg >= 0) {
@@ -198,7 +220,7 @@ __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
     float inv[HM];
 #pragma unroll
     for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
-    write_alpha<HM>(a, un, v, lane, z, mx, inv);
+    write_alpha_e<HM>(a, un, v, lane, z, inv);
 }
 
 // Pass 2, one warp per heavy segment: merge the row's segment partials in a

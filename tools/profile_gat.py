@@ -18,7 +18,9 @@ ld_ext = ops.ld_of(hdp + 2 * H)
 pext = torch.randn(n, ld_ext, device=dev)
 E = dg.fwd.nnz
 alpha = torch.zeros(E * H, device=dev); aself = torch.zeros(n * H, device=dev)
-ops.gat_softmax(dg.fwd, pext, H, dhp, alpha, aself)
+st = ops.zeros_rows(n, 2 * H, dev)
+ops.gat_pack_scores(pext, n, H, dhp, st)
+ops.gat_softmax(dg.fwd, pext, H, dhp, alpha, aself, st=st)
 O = ops.zeros_rows(n, hdp, dev)
 ops.agg_sum(dg.fwd, pext[:, :hdp], O, hdp, edge_w=alpha, self_w=aself, heads=H, head_ld=dhp, relu=True)
 go = torch.randn(n, hdp, device=dev)
