@@ -351,19 +351,24 @@ class _LayerCfg:
 class _Weights:
     """fp32 device copies of W_l and dW_l, zero padded to [ld(d_in), ld(d_out)].
     GraphSAGE layers keep [W_root | W_nbr] as [ld(d_in), 2 ld(d_out)] with the
-    neighbour block starting at column ld(d_out) (16-byte aligned)."""
+    neighbour block starting at column ld(d_out) (16-byte aligned); layers in
+    ``stacked`` keep them stacked along K instead, [W_root ; W_nbr] as
+    [2 ld(d_in), ld(d_out)], for the one-GEMM form [X | mean(X)] W."""
 
-    def __init__(self, model, device):
+    def __init__(self, model, device, stacked=frozenset()):
         self.w = []
         self.dw = []
         self.blocks = 2 if model.kind == "sage" else 1
         self.gat = model.kind == "gat"
+        self.stacked = frozenset(stacked) if self.blocks == 2 else frozenset()
         if self.gat:
             self._init_gat(model, device)
             return
-        for w in model.weights:
+        for l, w in enumerate(model.weights):
             d_in, d_out = w.shape[0], w.shape[1] // self.blocks
-            t = torch.zeros((ld_of(d_in), self.blocks * ld_of(d_out)), dtype=torch.float32, device=device)
+            shape = (2 * ld_of(d_in), ld_of(d_out)) if l in self.stacked else \
+                (ld_of(d_in), self.blocks * ld_of(d_out))
+            t = torch.zeros(shape, dtype=torch.float32, device=device)
             self.w.append(t)
             self.dw.append(torch.zeros_like(t))
         self.load(model)
@@ -417,8 +422,12 @@ class _Weights:
         """Every trained device tensor (what an SGD step modifies)."""
         return self.w + (self.att if self.gat else [])
 
-    def _views(self, t: torch.Tensor, w: np.ndarray):
+    def _views(self, t: torch.Tensor, w: np.ndarray, l: int):
         d_in, d_out = w.shape[0], w.shape[1] // self.blocks
+        if l in self.stacked:
+            li = ld_of(d_in)
+            return [(t[b * li: b * li + d_in, :d_out], slice(b * d_out, (b + 1) * d_out))
+                    for b in range(self.blocks)]
         ld = ld_of(d_out)
         return [(t[:d_in, b * ld: b * ld + d_out], slice(b * d_out, (b + 1) * d_out))
                 for b in range(self.blocks)]
@@ -427,9 +436,9 @@ class _Weights:
         if self.gat:
             self._gat_load(model)
             return
-        for t, w in zip(self.w, model.weights):
+        for l, (t, w) in enumerate(zip(self.w, model.weights)):
             w32 = torch.from_numpy(np.asarray(w, dtype=np.float32))
-            for view, cols in self._views(t, w):
+            for view, cols in self._views(t, w, l):
                 view.copy_(w32[:, cols])
 
     def export(self, model) -> None:
@@ -439,14 +448,16 @@ class _Weights:
 
         def host(tensors):
             out = []
-            for t, w in zip(tensors, model.weights):
-                out.append(np.concatenate([v.double().cpu().numpy() for v, _ in self._views(t, w)],
+            for l, (t, w) in enumerate(zip(tensors, model.weights)):
+                out.append(np.concatenate([v.double().cpu().numpy() for v, _ in self._views(t, w, l)],
                                           axis=1))
             return out
         model.weights, model.weight_grads = host(self.w), host(self.dw)
 
 
 class _EngineBase:
+    _fuse_sage_root = False
+
     def __init__(self, dg: DeviceGraph, model, features: torch.Tensor, labels: np.ndarray,
                  train_mask: np.ndarray, mask_count: int | None = None):
         self.dg = dg
@@ -461,7 +472,15 @@ class _EngineBase:
         self.model = model
         self.cfg = [_LayerCfg(l, self.dims, self.mode, model.row_normalize, l == self.L - 1,
                               model.heads) for l in range(self.L)]
-        self.wts = _Weights(model, dev)
+        # GraphSAGE aggregate-first layer 0 over a features buffer with room
+        # for mean(X) beside X: out = [X | mean(X)] [W_root ; W_nbr], one GEMM
+        # (and one weight-gradient GEMM) instead of two with a read-back of out
+        c0 = self.cfg[0]
+        self.xn = None
+        if (self._fuse_sage_root and c0.sage and not c0.transform_first
+                and features.stride(0) >= 2 * c0.ld_in):
+            self.xn = torch.as_strided(features, (dg.n_local, 2 * c0.ld_in), (features.stride(0), 1))
+        self.wts = _Weights(model, dev, stacked={0} if self.xn is not None else ())
         self.acts = [features] + [ops.zeros_rows(self.NL, d, dev) for d in self.dims[1:]]
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
         self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
@@ -498,6 +517,8 @@ class _EngineBase:
 
 class LayerwiseEngine(_EngineBase):
     """Fused layer-wide epoch over an HBM-resident graph (module docstring)."""
+
+    _fuse_sage_root = True
 
     def __init__(self, dg, model, features, labels, train_mask, mask_count=None):
         super().__init__(dg, model, features, labels, train_mask, mask_count)
@@ -554,6 +575,11 @@ class LayerwiseEngine(_EngineBase):
             ops.gemm(x, W, y, self.V, 2 * c.ld_out, c.d_in)
             dg.exchange_agg("fwd", y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
                             add_y=y[:, : c.ld_out], relu=relu)      # halo rows of X W_nbr
+        elif l == 0 and self.xn is not None:
+            # N = mean_in(X) beside X, out = [X | N] [W_root ; W_nbr]
+            n = self.xn[:, c.ld_in: 2 * c.ld_in]
+            self._input_agg(l, x, n, c.d_in, post_div_deg=2, no_self=True)
+            ops.gemm(self.xn, W, out, self.V, c.d_out, 2 * c.ld_in, relu_out=relu)
         else:
             # N = mean_in(X), out = X W_root + N W_nbr
             n = self.t1[:, : c.ld_in]
@@ -576,6 +602,11 @@ class LayerwiseEngine(_EngineBase):
             if l > 0:
                 ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
             ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=self._w(W), lr=lr)
+        elif l == 0 and self.xn is not None:
+            gp = self.g[:, : c.ld_out]
+            ops.agg_sum(dg.fwd, x, self.xn[:, c.ld_in: 2 * c.ld_in], c.d_in, post_div_deg=2,
+                        no_self=True)                                           # regather
+            ops.wgrad_sgd(self.xn, gp, dW, 2 * c.ld_in, c.d_out, self.V, w=self._w(W), lr=lr)
         else:
             gp = self.g[:, : c.ld_out]
             n = self.t1[:, : c.ld_in]

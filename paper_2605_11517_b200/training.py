@@ -160,7 +160,13 @@ class TrainSession:
         self.dg = dg
         self.model = copy_model(model)
         self.dataset = dataset
-        features = ops.zeros_rows(dg.n_local, dataset.feature_dim, self.dev)
+        F = dataset.feature_dim
+        if layerwise and model.kind == "sage" and model.dims[1] > model.dims[0]:
+            # room for mean(X) beside X (engine: one [X | mean(X)] GEMM in layer 0)
+            buf = torch.zeros((dg.n_local, 2 * ops.ld_of(F)), dtype=torch.float32, device=self.dev)
+            features = buf[:, : ops.ld_of(F)]
+        else:
+            features = ops.zeros_rows(dg.n_local, F, self.dev)
         cls = LayerwiseEngine if layerwise else PartitionEngine
         own = slice(None) if comm is None else dg.shard.owned
         self.engine = cls(dg, self.model, features, np.asarray(dataset.labels)[own],
