@@ -47,8 +47,12 @@ constexpr int kBK = 32;
 constexpr int kWarps = 14;
 constexpr int kThreads = kWarps * 32;
 constexpr int kConvWarp0 = 2;
-constexpr int kConvThreads = 256;
-constexpr int kEpiWarp0 = 10;
+constexpr int kConvWarps = 4;
+constexpr int kConvThreads = kConvWarps * 32;
+constexpr int kEpiWarp0 = kConvWarp0 + kConvWarps;
+constexpr int kEpiWarps = 8;            // two per TMEM lane quarter (column halves)
+constexpr int kEpiThreads = kEpiWarps * 32;
+static_assert(kEpiWarp0 + kEpiWarps == kWarps, "warp roles");
 
 enum OpMode : int {
     kKMajorTma = 0,     // raw, K-contiguous rows, one TMA box (32 x rows)
@@ -326,6 +330,7 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
                                               int warp, int lane, int64_t t0, int64_t tstep,
                                               int64_t ntiles, TileFn tile_of) {
     const int q = warp & 3;                               // TMEM lane quarter
+    const int half = (warp - kEpiWarp0) >> 2;             // which interleaved column chunks
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const int bn = p.bn;
     int64_t i = 0;
@@ -337,12 +342,14 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
         const int acc = static_cast<int>(i & 1);
         const int64_t row0 = m0 + q * 32;
         const int64_t n_pad = (p.n + 3) / 4 * 4;
-        for (int c0 = 0; c0 < bn; c0 += 32) {
+        bool waited = false;
+        for (int c0 = 32 * half; c0 < bn; c0 += 64) {
             EpiIn in;
             epi_prefetch(p, row0 + lane, n0 + c0, in);
-            if (has_k && c0 == 0) {
+            if (has_k && !waited) {
                 mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                waited = true;
             }
             float v[32];
             if (has_k) {
@@ -355,6 +362,10 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
             epi_store_direct(p, v, row0 + lane, n0 + c0, z, in);
         }
         if (has_k) {
+            // a warp without columns in this tile (bn <= 32) still waits for
+            // the accumulator before releasing it: no arrival may run ahead
+            // into the buffer's next phase
+            if (!waited) mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
             asm volatile("tcgen05.fence::before_thread_sync;");
             if (kPair) mbar_arrive_cluster(tempty + acc, 0);
             else mbar_arrive(tempty + acc);
@@ -426,7 +437,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128 * nc);
+            mbar_init(tempty + a, kEpiThreads * nc);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
@@ -648,29 +659,35 @@ __device__ __forceinline__ void sts128u(uint32_t a, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
 }
 
-// 8 converter warps; lane = (row-in-group r4 = lane / 8, output chunk j = lane % 8)
+// kConvWarps converter warps, 4 rows per warp per pass; lane = (row-in-group
+// r4 = lane / 8, output chunk j = lane % 8); 4 passes read before any write
 __device__ __forceinline__ void split_stage_bf16(uint8_t* st, int cwarp, int lane) {
     const uint32_t base = smem_u32(st);
     const int r4 = lane >> 3, j = lane & 7;
     const uint32_t box = static_cast<uint32_t>(j >> 2) * 16384u;
     const uint32_t c0 = static_cast<uint32_t>(2 * (j & 3));
-    float4 x[4][2];
+    constexpr int kRowsPerPass = kConvWarps * 4;
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-        const uint32_t r = static_cast<uint32_t>(cwarp * 4 + r4 + 32 * it);
-        const uint32_t row = base + box + r * 128u;
-        x[it][0] = lds128(row + (((c0) ^ (r & 7u)) << 4));
-        x[it][1] = lds128(row + (((c0 + 1u) ^ (r & 7u)) << 4));
-    }
-    __syncwarp();
+    for (int g4 = 0; g4 < kBM / kRowsPerPass; g4 += 4) {
+        float4 x[4][2];
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-        const uint32_t r = static_cast<uint32_t>(cwarp * 4 + r4 + 32 * it);
-        uint4 hi, lo;
-        split8(x[it][0], x[it][1], hi, lo);
-        const uint32_t off = r * 128u + ((static_cast<uint32_t>(j) ^ (r & 7u)) << 4);
-        sts128u(base + off, hi);
-        sts128u(base + 16384u + off, lo);
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t r = static_cast<uint32_t>(cwarp * 4 + r4 + kRowsPerPass * (g4 + it));
+            const uint32_t row = base + box + r * 128u;
+            x[it][0] = lds128(row + (((c0) ^ (r & 7u)) << 4));
+            x[it][1] = lds128(row + (((c0 + 1u) ^ (r & 7u)) << 4));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t r = static_cast<uint32_t>(cwarp * 4 + r4 + kRowsPerPass * (g4 + it));
+            uint4 hi, lo;
+            split8(x[it][0], x[it][1], hi, lo);
+            const uint32_t off = r * 128u + ((static_cast<uint32_t>(j) ^ (r & 7u)) << 4);
+            sts128u(base + off, hi);
+            sts128u(base + 16384u + off, lo);
+        }
+        __syncwarp();
     }
 }
 
@@ -727,7 +744,7 @@ gemm_bf16x3_ws(const __grid_constant__ CUtensorMap map_a, const Params p) {
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, kEpiThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
