@@ -91,7 +91,8 @@ def test_agg_sum_mask_ref_and_defaults():
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
 @pytest.mark.parametrize("m,n,k", [(1000, 64, 128), (257, 10, 64), (131, 47, 100), (64, 256, 300),
-                                   (1300, 96, 64), (2000, 512, 100)])
+                                   (1300, 96, 64), (2000, 512, 100),
+                                   (1300, 256, 70)])   # CTA pairs with an odd M-tile count
 def test_gemm_matches_numpy(ta, tb, m, n, k):
     rng = np.random.default_rng(m + n + k)
     a = rng.normal(size=(k, m) if ta else (m, k))
@@ -117,7 +118,8 @@ def test_gemm_relu_out_and_accumulate():
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 131072), (64, 10, 5000), (100, 47, 1), (256, 256, 70000),
-                                   (384, 10, 20000), (512, 96, 9000)])
+                                   (384, 10, 20000), (512, 96, 9000),
+                                   (384, 128, 30000)])  # split-K on CTA pairs, odd M-tile count
 def test_wgrad_sgd(m, n, k):
     rng = np.random.default_rng(k)
     a = rng.normal(size=(k, m)).astype(np.float32)
