@@ -43,13 +43,13 @@ WORKLOADS["products_sage"] = dict(
          "generate_kronecker(21, 30): 2,097,152 V / 62,914,560 E, 100 feats, 47 classes, "
          "8 switching-aware partitions",
     scale=21, deg=30, F=100, C=47, L=3, H=256, P=8, mode="sage_mean",
-    cpu_sample=dict(scale=19, deg=30))
+    cpu_sample=dict(scale=19, deg=30), ref_sample=dict(scale=18, deg=30))
 WORKLOADS["products_gat"] = dict(
     desc="configs[2]: 3-layer GAT (4 heads x 64 concat, mean on the last layer) on the "
          "ogbn-products-shaped generate_kronecker(21, 30): 2,097,152 V / 62,914,560 E, "
          "100 feats, 47 classes, 8 switching-aware partitions",
     scale=21, deg=30, F=100, C=47, L=3, H=256, P=8, mode="gat", heads=4,
-    cpu_sample=dict(scale=16, deg=30))
+    cpu_sample=dict(scale=16, deg=30), ref_sample=dict(scale=15, deg=30))
 WORKLOADS["papers_gcn"] = dict(
     desc="configs[3] shape at 1/3.3 size (HBM-resident on one B200): 3-layer GCN hidden 128, "
          "ogbn-papers100M-shaped generate_kronecker(25, 14): 33,554,432 V / 469,762,048 E "
@@ -404,11 +404,12 @@ def oracle_epoch_seconds(spec, ds, plan, model, epochs=1):
     return (time.perf_counter() - t0) / epochs
 
 
-def cpu_sample(spec, g, ds, plan, model):
+def cpu_sample(spec, g, ds, plan, model, key="cpu_sample"):
     """The workload itself, or (for graphs the float64 oracle cannot hold in
     host memory / a bounded time) the same model on a smaller Kronecker graph
-    of the same average degree."""
-    smp = spec.get("cpu_sample")
+    of the same average degree.  ``ref_sample``: the reference arm's per-step
+    sample (smaller, so K + W steps stay within a few minutes)."""
+    smp = spec.get(key) or spec.get("cpu_sample")
     if smp is None:
         return g, ds, plan, model, "the full workload"
     sub = dict(spec, scale=smp["scale"], deg=smp["deg"])
@@ -431,7 +432,7 @@ def run_reference(args, spec, rank, world):
     if rank != 0:
         return None
     g, ds, plan, model, prep = build_workload(spec)
-    g, ds, plan, model, what = cpu_sample(spec, g, ds, plan, model)
+    g, ds, plan, model, what = cpu_sample(spec, g, ds, plan, model, key="ref_sample")
     for _ in range(args.warmup):
         oracle_epoch_seconds(spec, ds, plan, model)
     times = [oracle_epoch_seconds(spec, ds, plan, model) for _ in range(args.steps)]
