@@ -83,10 +83,24 @@ def rank_info():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def _cuda_ok() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
 def build_workload(spec):
     import paper_2605_11517_b200 as g2
     t0 = time.perf_counter()
-    g = g2.generate_kronecker(spec["scale"], spec["deg"], seed=SEED)
+    gpu_gen = spec["scale"] >= 20 and _cuda_ok()
+    if gpu_gen:   # bit-identical to the host generator (tests/test_gpu_generate.py)
+        import torch
+        g = g2.generate_kronecker(spec["scale"], spec["deg"], seed=SEED, device="cuda")
+        torch.cuda.empty_cache()
+    else:
+        g = g2.generate_kronecker(spec["scale"], spec["deg"], seed=SEED)
     t_gen = time.perf_counter() - t0
     ds = g2.make_random_dataset(g, feature_dim=spec["F"], num_classes=spec["C"], seed=SEED + 1,
                                 feature_dtype=np.dtype(spec.get("feature_dtype", "float64")))
@@ -99,7 +113,7 @@ def build_workload(spec):
     model = g2.create_model(spec["F"], spec["C"], num_layers=spec["L"], hidden_dim=spec["H"],
                             seed=SEED + 3, aggregation_mode=spec["mode"],
                             heads=spec.get("heads", 4))
-    prep = {"generate_s": round(t_gen, 3), "partition_s": round(t_part, 3),
+    prep = {"generate_s": round(t_gen, 3), "generator": "gpu" if gpu_gen else "host", "partition_s": round(t_part, 3),
             "plan_s": round(t_plan, 3), "partitioner_iterations": part.iterations}
     return g, ds, plan, model, prep
 

@@ -56,6 +56,15 @@ int grd_kronecker_generate(int32_t scale, int64_t avg_degree,
                            int64_t* src_ptr, int32_t* dst_idx,
                            int64_t dst_capacity, int64_t* num_edges_out,
                            int32_t num_threads);
+/* GPU variant of one generator round (graph.py:158-209): the `batch` vertex
+ * pairs of the round as canonical keys lo * 2^scale + hi (-1 for a self
+ * loop) into device memory `keys`.  pcg_words = {state_hi, state_lo, inc_hi,
+ * inc_lo} of the PCG64 stream at the round's start, then {mul_hi, mul_lo,
+ * add_hi, add_lo} of the LCG jump by `batch` steps; cum = the cumulative
+ * initiator (host arrays).  Deduplication / CSR build are the caller's
+ * (graph.generate_kronecker(..., device="cuda")). */
+int grd_kronecker_keys(int32_t scale, int64_t batch, const uint64_t* pcg_words,
+                       const double* cum, int64_t* keys, void* stream);
 
 /* Switching-aware partitioner, bit-exact with partition.py:254-321
  * switching_aware_partition (its numba kernels _analyze_kernel :140-200 and
