@@ -108,7 +108,8 @@ def build_workload(spec):
     part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2))
     t_part = time.perf_counter() - t1
     t2 = time.perf_counter()
-    plan = g2.build_partition_plan(g, part.labels, spec["P"])
+    # bit-identical to the host plan (tests/test_gpu_plan.py)
+    plan = g2.build_partition_plan(g, part.labels, spec["P"], device="cuda" if gpu_gen else None)
     t_plan = time.perf_counter() - t2
     model = g2.create_model(spec["F"], spec["C"], num_layers=spec["L"], hidden_dim=spec["H"],
                             seed=SEED + 3, aggregation_mode=spec["mode"],

@@ -531,7 +531,71 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
     double loss_acc = 0.0;
     double correct = 0.0;
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / kWarp);
-    for (int64_t r = int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows; r += nwarps) {
+    if (c <= 2 * kWarp) {
+        // <= 64 classes: the row lives in two registers per lane, each exp is
+        // computed once, and the next row's logits / label / mask are loaded
+        // while this one reduces (same arithmetic as the general loop below,
+        // so the same bits)
+        int64_t r = int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp;
+        auto load = [&](int64_t rr, float& a, float& b, int& yy, bool& mm) {
+            const float* row = logits + rr * ldl;
+            a = lane < c ? row[lane] : -INFINITY;
+            b = lane + kWarp < c ? row[lane + kWarp] : -INFINITY;
+            yy = labels[rr];
+            mm = mask[rr] != 0;
+        };
+        float v0 = 0.f, v1 = 0.f;
+        int y = 0;
+        bool on = false;
+        if (r < n_rows) load(r, v0, v1, y, on);
+        for (; r < n_rows; r += nwarps) {
+            float n0 = 0.f, n1 = 0.f;
+            int ny = 0;
+            bool non = false;
+            if (r + nwarps < n_rows) load(r + nwarps, n0, n1, ny, non);
+            float* grow = grad + r * ldg;
+            if (lane < c4 - c) grow[c + lane] = 0.f;
+            if (!on) {
+                if (lane < c) grow[lane] = 0.f;
+                if (lane + kWarp < c) grow[lane + kWarp] = 0.f;
+            } else {
+                float mx = v0;
+                int arg = lane < c ? lane : 0x7fffffff;
+                if (v1 > mx) { mx = v1; arg = lane + kWarp; }
+                for (int off = 16; off > 0; off >>= 1) {
+                    const float om = __shfl_xor_sync(0xffffffffu, mx, off);
+                    const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+                    if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+                }
+                const float e0 = lane < c ? expf(v0 - mx) : 0.f;
+                const float e1 = lane + kWarp < c ? expf(v1 - mx) : 0.f;
+                float sum = e0 + e1;
+                if (!(lane + kWarp < c)) sum = e0;
+                // the general loop adds j = lane first, then j = lane + 32
+                for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+                const float scale = gscale ? gscale[r] : 1.0f;
+                if (lane < c) {
+                    float pr = e0 / sum;
+                    if (lane == y) pr -= 1.0f;
+                    grow[lane] = pr * inv_count * scale;
+                }
+                if (lane + kWarp < c) {
+                    float pr = e1 / sum;
+                    if (lane + kWarp == y) pr -= 1.0f;
+                    grow[lane + kWarp] = pr * inv_count * scale;
+                }
+                const float ey = __shfl_sync(0xffffffffu, y < kWarp ? e0 : e1, y & (kWarp - 1));
+                if (lane == 0) {
+                    loss_acc -= static_cast<double>(logf(ey / sum));
+                    correct += (arg == y) ? 1.0 : 0.0;
+                }
+            }
+            v0 = n0; v1 = n1; y = ny; on = non;
+        }
+        r = n_rows;   // fall through to the block reduction
+    }
+    for (int64_t r = c <= 2 * kWarp ? n_rows : int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows;
+         r += nwarps) {
         const float* row = logits + r * ldl;
         float* grow = grad + r * ldg;
         // padding columns [c, round_up(c, 4)) are part of the 16-byte rows the

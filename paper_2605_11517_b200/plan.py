@@ -122,10 +122,68 @@ class PartitionPlan:
         return t, g, e
 
 
+def _flat_plan_gpu(graph: CsrGraph, lab32: np.ndarray, p: int, device) -> FlatPlan:
+    """The FlatPlan by device sorts (same arrays as grd_plan_create, bit for
+    bit): edges ordered by (perm row of the target, owner of the source,
+    source id) through two stable sorts of the CSR's source-ordered edge
+    list; gather maps as the sorted unique (partition, owner, id) keys of
+    every in-edge and target, whose inverse gives src_pos and self_pos."""
+    import torch
+    dev = torch.device(device)
+    n = graph.num_vertices
+    with torch.cuda.device(dev):
+        lab = torch.from_numpy(lab32).to(dev).long()
+        ptr = torch.from_numpy(np.ascontiguousarray(graph.src_ptr, dtype=np.int64)).to(dev)
+        dst = torch.from_numpy(np.ascontiguousarray(graph.dst_idx, dtype=np.int32)).to(dev).long()
+        m = dst.numel()
+        src = torch.repeat_interleave(torch.arange(n, device=dev), ptr[1:] - ptr[:-1])
+        perm = torch.sort(lab, stable=True).indices
+        rank = torch.empty_like(perm)
+        rank[perm] = torch.arange(n, device=dev)
+        part_ptr = torch.zeros(p + 1, dtype=torch.int64, device=dev)
+        part_ptr[1:] = torch.cumsum(torch.bincount(lab, minlength=p), 0)
+        in_degree = torch.bincount(dst, minlength=n)
+        # CSR edges are in source order: stable by owner(source) gives
+        # (owner, id); stable by the target's perm row groups the rows
+        o1 = torch.sort(lab[src], stable=True).indices
+        src, dst = src[o1], dst[o1]
+        del o1
+        o2 = torch.sort(rank[dst], stable=True).indices
+        src, dst = src[o2], dst[o2]
+        del o2
+        in_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        in_ptr[1:] = torch.cumsum(in_degree[perm], 0)
+        # gather maps: unique (partition, owner, id) over in-edges and targets
+        q_e = lab[dst]
+        keys = torch.cat([(q_e * p + lab[src]) * n + src, (lab * p + lab) * n + torch.arange(n, device=dev)])
+        del q_e
+        uniq, inv = torch.unique(keys, sorted=True, return_inverse=True)
+        del keys
+        gq = uniq // n // p
+        gather_ptr = torch.zeros(p + 1, dtype=torch.int64, device=dev)
+        gather_ptr[1:] = torch.cumsum(torch.bincount(gq, minlength=p), 0)
+        gather_map = (uniq % n).int()
+        del uniq, gq
+        in_src_pos = (inv[:m] - gather_ptr[lab[dst]]).int()
+        self_all = inv[m:] - gather_ptr[lab]
+        self_pos = self_all[perm].int()
+        del inv, self_all
+
+        def h(t, dt):
+            return t.to(torch.int64 if dt == np.int64 else torch.int32).cpu().numpy().astype(dt, copy=False)
+        flat = FlatPlan(part_ptr=h(part_ptr, np.int64), perm=h(perm, np.int32), in_ptr=h(in_ptr, np.int64),
+                        in_src=h(src, np.int32), in_src_pos=h(in_src_pos, np.int32),
+                        gather_ptr=h(gather_ptr, np.int64), gather_map=h(gather_map, np.int32),
+                        self_pos=h(self_pos, np.int32), in_degree=h(in_degree, np.int32))
+    torch.cuda.empty_cache()
+    return flat
+
+
 def build_partition_plan(graph: CsrGraph, labels: np.ndarray,
                          num_partitions: int | None = None,
-                         num_threads: int | None = None) -> PartitionPlan:
-    """Gather maps and local topologies for every partition (plan.py:75-136)."""
+                         num_threads: int | None = None, device=None) -> PartitionPlan:
+    """Gather maps and local topologies for every partition (plan.py:75-136).
+    ``device="cuda"`` builds the same plan with device sorts."""
     n = graph.num_vertices
     labels = np.asarray(labels)
     if labels.shape != (n,):
@@ -134,6 +192,8 @@ def build_partition_plan(graph: CsrGraph, labels: np.ndarray,
     if labels.size and (labels.min() < 0 or labels.max() >= p):
         raise ValueError("labels out of range for num_partitions")
     lab32 = np.ascontiguousarray(labels, dtype=np.int32)
+    if device is not None and str(device).startswith("cuda"):
+        return PartitionPlan(lab32, p, n, _flat_plan_gpu(graph, lab32, p, device))
     src_ptr = np.ascontiguousarray(graph.src_ptr, dtype=np.int64)
     dst_idx = np.ascontiguousarray(graph.dst_idx, dtype=np.int32)
     L = _lib.lib()

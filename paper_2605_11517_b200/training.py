@@ -21,6 +21,8 @@ sees per-partition tensors in the reference's order.
 
 from __future__ import annotations
 
+import os
+
 from pathlib import Path
 
 import numpy as np
@@ -351,11 +353,22 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
     Inside an initialised torch.distributed job with several ranks the
     session is this rank's shard of the partitions (distributed.py)."""
     comm = _communicator()
-    stream = layerwise and comm is None and _use_streaming(dataset, model)
     key = ("session", tuple(model.dims), model.aggregation_mode, model.heads, model.row_normalize,
-           model.dropout_rate, model.dropout_seed, layerwise, comm is not None, stream)
+           model.dropout_rate, model.dropout_seed, layerwise, comm is not None)
     sess = plan.device_cache.get(key)
+    # the engine choice is made once per (plan, model config): a later call
+    # must not re-decide against the HBM the cached session itself holds
+    forced = os.environ.get("GRD_ENGINE", "")
+    if sess is not None and forced in ("stream", "resident"):
+        from .stream import StreamSession
+        if isinstance(sess, StreamSession) != (forced == "stream"):
+            del plan.device_cache[key]      # release it before building the other engine
+            sess = None
+            import gc
+            gc.collect()
+            torch.cuda.empty_cache()
     if sess is None:
+        stream = layerwise and comm is None and _use_streaming(dataset, model)
         if stream:
             from .stream import StreamSession
             sess = StreamSession(dataset, plan, model)
