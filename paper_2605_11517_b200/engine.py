@@ -92,7 +92,9 @@ class DeviceGraph:
             src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(g.src_ptr))
             key_out = src * n + g.dst_idx.astype(np.int64)
             pos = order[np.searchsorted(key_in[order], key_out)]
-            self._o2i = torch.from_numpy(pos.astype(np.int32)).to(self.device)
+            # at least one element: an edgeless graph still passes a valid pointer
+            self._o2i = torch.from_numpy(np.concatenate([pos.astype(np.int32),
+                                                         np.zeros(1, np.int32)])).to(self.device)
         return self._o2i
 
     def local_rows(self, arr: np.ndarray) -> np.ndarray:
@@ -222,7 +224,7 @@ class ShardDeviceGraph(DeviceGraph):
         if getattr(self, "_gat_pull", None) is None:
             ptr, idx, perm = self.shard.local_transpose()
             self._gat_pull = (AggSpec.build(ptr, idx, self.device),
-                              torch.from_numpy(perm).to(self.device))
+                              torch.from_numpy(np.concatenate([perm, [0]]).astype(np.int32)).to(self.device))
         return self._gat_pull
 
     def reverse_add(self, buf: torch.Tensor, width: int) -> None:

@@ -1,0 +1,85 @@
+"""Degenerate inputs through the public API on the GPU, against the oracle:
+a graph without edges, a single vertex, partitions left empty, a lone
+train vertex, and one class."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from conftest import rel_l2  # noqa: E402
+from oracle import gcn, plan as oplan  # noqa: E402
+import paper_2605_11517_b200 as g2  # noqa: E402
+
+
+def _check(g, labels, P, F=6, C=3, L=2, H=4, mode="mean_self_loop", mask=None, epochs=2):
+    ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=1)
+    if mask is not None:
+        ds.train_mask = mask
+    plan = g2.build_partition_plan(g, labels, P)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=2, aggregation_mode=mode)
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=epochs, lr=0.1)
+    topos = oplan.build_plan(g.src_ptr, g.dst_idx, labels, P)
+    W, _, ref = gcn.train_partitioned(ds.features, ds.labels, ds.train_mask, topos, model.weights,
+                                      epochs, 0.1, mode=mode)
+    for (_, l1, _), (_, l2, _) in zip(trace, ref):
+        assert abs(l1 - l2) <= 1e-4 * max(abs(l2), 1e-12)
+    for a, b in zip(trained.weights, W):
+        assert rel_l2(a, b) < 1e-4
+    return trained, trace
+
+
+@pytest.mark.parametrize("mode", ["mean_self_loop", "symmetric_norm"])
+def test_graph_without_edges(mode):
+    g = g2.build_csr(np.zeros((0, 2), dtype=np.int64), 50)
+    labels = (np.arange(50) % 3).astype(np.int32)
+    _check(g, labels, 3, mode=mode)
+
+
+def test_single_vertex():
+    g = g2.build_csr(np.zeros((0, 2), dtype=np.int64), 1)
+    _check(g, np.zeros(1, dtype=np.int32), 1, mask=np.ones(1, dtype=bool))
+
+
+def test_empty_partitions_and_one_class():
+    g = g2.generate_kronecker(8, 6, seed=3)
+    labels = np.zeros(g.num_vertices, dtype=np.int32)
+    labels[::5] = 3                       # partitions 1 and 2 empty
+    _check(g, labels, 4, C=1)
+
+
+def test_one_train_vertex():
+    g = g2.generate_kronecker(8, 6, seed=4)
+    mask = np.zeros(g.num_vertices, dtype=bool)
+    mask[17] = True
+    labels = g2.random_partition(g.num_vertices, 3, 0)
+    _check(g, labels, 3, mask=mask)
+
+
+@pytest.mark.parametrize("mode", ["sage_mean", "gat"])
+def test_sage_gat_without_edges(mode):
+    from oracle import sage_gat
+    g = g2.build_csr(np.zeros((0, 2), dtype=np.int64), 40)
+    ds = g2.make_random_dataset(g, feature_dim=8, num_classes=3, seed=1)
+    plan = g2.build_partition_plan(g, (np.arange(40) % 2).astype(np.int32), 2)
+    model = g2.create_model(8, 3, num_layers=2, hidden_dim=8, seed=2, aggregation_mode=mode, heads=2)
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.1)
+    if mode == "gat":
+        W, _, ref = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                       model.weights, 2, 2, 0.1)
+    else:
+        W, _, ref = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                        model.weights, 2, 0.1)
+    for (_, l1, _), (_, l2, _) in zip(trace, ref):
+        assert abs(l1 - l2) <= 1e-4 * abs(l2)
+    for a, b in zip(trained.weights, W):
+        assert rel_l2(a, b) < 1e-4
+
+
+def test_streaming_without_edges(monkeypatch):
+    monkeypatch.setenv("GRD_ENGINE", "stream")
+    g = g2.build_csr(np.zeros((0, 2), dtype=np.int64), 64)
+    _check(g, (np.arange(64) % 4).astype(np.int32), 4, F=8, C=3, H=4)
