@@ -779,6 +779,7 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     clear_error();
     if (!args) return fail(kErrArg, "agg_sum: null args");
     const grd_agg_args& a = *args;
+    if (a.n_rows == 0 && a.width > 0) return 0;        // e.g. a rank that owns no rows
     if (a.n_rows < 0 || a.width <= 0 || a.width > 1024 || !a.row_ptr || !a.y || !a.out)
         return fail(kErrArg, "agg_sum: bad arguments (width %d)", a.width);
     if (a.ldy % 4 || a.ldo % 4 || (reinterpret_cast<uintptr_t>(a.y) & 15) ||
@@ -854,9 +855,9 @@ extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
     clear_error();
     if (!args) return fail(kErrArg, "gemm: null args");
     const grd_gemm_args& g = *args;
-    if (g.m < 0 || g.n < 0 || g.k < 0 || !g.a || !g.b || !g.c)
-        return fail(kErrArg, "gemm: bad arguments");
-    if (g.m == 0 || g.n == 0) return 0;
+    if (g.m < 0 || g.n < 0 || g.k < 0) return fail(kErrArg, "gemm: bad arguments");
+    if (g.m == 0 || g.n == 0) return 0;                 // nothing to write
+    if (!g.a || !g.b || !g.c) return fail(kErrArg, "gemm: bad arguments");
     GrdTcGemm t{};
     t.m = g.m; t.n = g.n; t.k = g.k;
     t.a = g.a; t.lda = g.lda; t.trans_a = g.trans_a;
@@ -894,12 +895,13 @@ extern "C" int grd_wgrad_sgd(int64_t m, int64_t n, int64_t k, const float* a, in
                              int64_t ldb, float* dw, int64_t lddw, int32_t accumulate, float* w, int64_t ldw,
                              float lr, float* workspace, int64_t workspace_elems, void* stream) {
     clear_error();
-    if (m <= 0 || n <= 0 || k < 0 || !a || !b || !dw || !workspace)
+    if (m <= 0 || n <= 0 || k < 0 || (k > 0 && (!a || !b)) || !dw || !workspace)
         return fail(kErrArg, "wgrad: bad arguments");
     const int64_t splits = wgrad_splits(m, n, k);
     if (workspace_elems < splits * m * ((n + 3) / 4 * 4)) return fail(kErrArg, "wgrad: workspace too small");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (lda % 4 || ldb % 4 || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+    if (k > 0 && (lda % 4 || ldb % 4 || (reinterpret_cast<uintptr_t>(a) & 15) ||
+                  (reinterpret_cast<uintptr_t>(b) & 15)))
         return fail(kErrArg, "wgrad: leading dims must be multiples of 4 and rows 16-byte aligned");
     const int64_t ldp = (n + 3) / 4 * 4;
     int64_t used = 1;
@@ -934,7 +936,8 @@ extern "C" int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t 
                                 int64_t ld_grad, const float* grad_scale, double* partials, double* stats_out,
                                 void* stream) {
     clear_error();
-    if (!logits || !labels || !mask || !grad || !partials || !stats_out || n_classes <= 0)
+    if ((n_rows > 0 && (!logits || !labels || !mask || !grad)) || !partials || !stats_out || n_classes <= 0 ||
+        n_rows < 0)
         return fail(kErrArg, "softmax_xent: bad arguments");
     if (mask_count <= 0) return fail(kErrArg, "loss mask selects no vertices");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

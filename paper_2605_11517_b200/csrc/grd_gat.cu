@@ -546,6 +546,7 @@ extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
 extern "C" int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream) {
     clear_error();
     if (int rc = check_units(args, "gat_softmax_bwd")) return rc;
+    if (args->n_rows == 0) return 0;
     if (args->hdp > 256 || args->hdp % 4 || args->dhp % 4 || !args->grad_o || !args->o_fwd ||
         args->ld_go % 4 || args->ld_o % 4 || args->ld_ext % 4)
         return fail(kErrArg, "gat_softmax_bwd: hdp <= 256, 16-byte aligned rows, grad_o and o_fwd required");
@@ -564,8 +565,8 @@ extern "C" int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream) {
 extern "C" int grd_gat_src_grad(const grd_gat_args* args, void* stream) {
     clear_error();
     if (int rc = check_units(args, "gat_src_grad")) return rc;
-    if (!args->edge_perm) return fail(kErrArg, "gat_src_grad: needs edge_perm");
     if (args->n_rows == 0) return 0;
+    if (!args->edge_perm) return fail(kErrArg, "gat_src_grad: needs edge_perm");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     gat_src_grad_kernel<<<unit_blocks(*args), 256, 0, st>>>(*args);
     int rc = launch_status("gat_src_grad");
@@ -587,9 +588,9 @@ __global__ void gat_pack_scores_kernel(const float* __restrict__ p_ext, int64_t 
 extern "C" int grd_gat_pack_scores(const float* p_ext, int64_t ld_ext, int64_t n_rows, int32_t heads, int32_t hdp,
                                    float* st, int64_t ld_st, void* stream) {
     clear_error();
+    if (n_rows == 0) return 0;
     if (!p_ext || !st || heads < 1 || heads > kMaxHeads || ld_st < 2 * heads || n_rows < 0)
         return fail(kErrArg, "gat_pack_scores: bad arguments");
-    if (n_rows == 0) return 0;
     const int64_t n = n_rows * 2 * heads;
     gat_pack_scores_kernel<<<blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(p_ext, ld_ext, n_rows, heads,
                                                                                       hdp, st, ld_st);

@@ -23,6 +23,10 @@ CASES = {
     # GAT: halo rows of [P | s | t], transposed pull over the local in-CSR,
     # partial sums returned by the reverse exchange
     "gat": dict(mode="gat", F=10, H=16, C=3, L=3),
+    # rank 0's only partition is empty: a rank that owns no rows still takes
+    # part in every exchange and all-reduce
+    "gcn_empty_rank": dict(mode="mean_self_loop", F=8, H=8, C=3, L=2, empty_first=True),
+    "gat_empty_rank": dict(mode="gat", F=8, H=16, C=3, L=2, empty_first=True),
 }
 
 
@@ -30,8 +34,11 @@ def _setup(case):
     c = CASES[case]
     g = g2.generate_kronecker(10, 8, seed=4)
     ds = g2.make_random_dataset(g, feature_dim=c["F"], num_classes=c["C"], seed=5)
-    part = g2.switching_aware_partition(g, 6, g2.PartitionerParams(seed=6))
-    plan = g2.build_partition_plan(g, part.labels, 6)
+    if c.get("empty_first"):
+        plan = g2.build_partition_plan(g, np.ones(g.num_vertices, dtype=np.int32), 2)
+    else:
+        part = g2.switching_aware_partition(g, 6, g2.PartitionerParams(seed=6))
+        plan = g2.build_partition_plan(g, part.labels, 6)
     model = g2.create_model(c["F"], c["C"], num_layers=c["L"], hidden_dim=c["H"], seed=7,
                             aggregation_mode=c["mode"])
     return ds, plan, model
