@@ -83,3 +83,24 @@ def test_streaming_without_edges(monkeypatch):
     monkeypatch.setenv("GRD_ENGINE", "stream")
     g = g2.build_csr(np.zeros((0, 2), dtype=np.int64), 64)
     _check(g, (np.arange(64) % 4).astype(np.int32), 4, F=8, C=3, H=4)
+
+
+def test_per_partition_operators_on_empty_partition():
+    """layer_forward / regather_backward / scatter_accumulate of a partition
+    with no targets return empty results of the right shapes (the
+    reference's empty-partition plans, test_training.py:91-96)."""
+    g = g2.generate_kronecker(7, 6, seed=3)
+    labels = np.zeros(g.num_vertices, dtype=np.int32)
+    labels[::2] = 2                            # partition 1 empty
+    plan = g2.build_partition_plan(g, labels, 3)
+    topo = plan.topologies[1]
+    assert topo.targets.size == 0 and topo.gather_map.size == 0
+    model = g2.create_model(5, 3, num_layers=2, hidden_dim=4, seed=1)
+    out = g2.layer_forward(0, np.zeros((0, 5)), topo, model)
+    assert out.shape == (0, 4)
+    acts = np.random.default_rng(0).normal(size=(g.num_vertices, 5))
+    ga, gw = g2.regather_backward(0, 1, np.zeros((0, 4)), np.zeros((0, 4)), acts, plan, model)
+    assert ga.shape == (0, 5) and gw.shape == (5, 4) and not gw.any()
+    glob = np.ones((g.num_vertices, 5))
+    res = g2.scatter_accumulate(ga, topo.gather_map, glob)
+    assert res is glob and np.array_equal(glob, np.ones((g.num_vertices, 5)))

@@ -58,3 +58,24 @@ def test_offloaded_per_partition_probe_matches_resident():
     for k in seen_b:
         assert np.array_equal(seen_a[k][0], seen_b[k][0])   # same kernels, same order
         assert np.array_equal(seen_a[k][1], seen_b[k][1])
+
+
+def test_offloaded_with_empty_partition():
+    """A partition with no targets (and so no gathered rows) in the host-tier
+    path: same result as the resident engine, ledger equals the simulation."""
+    g = g2.generate_kronecker(8, 6, seed=7)
+    labels = (np.arange(g.num_vertices) % 3).astype(np.int32)
+    labels[labels == 1] = 2                   # partition 1 empty
+    plan = g2.build_partition_plan(g, labels, 3)
+    ds = g2.make_random_dataset(g, feature_dim=8, num_classes=3, seed=2)
+    model = g2.create_model(8, 3, num_layers=2, hidden_dim=8, seed=4)
+    cfg = HierarchyConfig(host_capacity=10_000, bytes_per_value=4)
+    session = TierSession(plan, model.dims, "GRINNDER", cfg)
+    trained, trace, ledger = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.05, hierarchy=session)
+    sim = simulate_epoch(plan, model.dims, "GRINNDER", cfg)
+    assert ledger.events[:len(sim.events)] == sim.events
+    resident, rtrace, _ = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.05)
+    for (_, a, _), (_, b, _) in zip(trace, rtrace):
+        assert abs(a - b) <= 1e-5 * abs(b)
+    for a, b in zip(trained.weights, resident.weights):
+        assert rel_l2(a, b) < 1e-5
