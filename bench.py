@@ -349,6 +349,7 @@ def run_ours(args, spec, rank, world, local_rank):
                 r["traffic"] = tr[r["kernel"]]
                 per_launch_s = r["ms_per_epoch"] * 1e-3 / r["launches_per_epoch"]
                 r["dram_GBs_implied"] = round(r["traffic"] / per_launch_s / 1e9, 1)
+                r["dram_frac"] = round(r["dram_GBs_implied"] / hbm_peak, 4)
     edges_per_epoch = L * E
     # strong scaling: the N ranks together train ONE epoch of the whole graph,
     # so the job processes L*|E| edges per step whatever N is
