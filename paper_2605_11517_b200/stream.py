@@ -690,8 +690,11 @@ class StreamSession:
         from .model import copy_model
         eng = self.engine
         eng.set_features(feature_rows(dataset, self.sg.chunks[0][1] if self.sg.chunks else 1))
-        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)))
-        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)))
+        from .training import pinned_rows
+        eng.labels.copy_(pinned_rows(dataset, "labels", np.asarray(dataset.labels), torch.int32),
+                         non_blocking=True)
+        eng.mask.copy_(pinned_rows(dataset, "mask", np.asarray(dataset.train_mask), torch.uint8),
+                       non_blocking=True)
         eng.mask_count = int(np.count_nonzero(dataset.train_mask))
         self.model = copy_model(model)
         eng.model = self.model

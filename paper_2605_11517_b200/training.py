@@ -206,8 +206,9 @@ class TrainSession:
         eng = self.engine
         moved = self.upload_features(dataset)
         own = slice(None) if self.comm is None else self.dg.shard.owned
-        eng.labels.copy_(torch.from_numpy(np.asarray(dataset.labels, dtype=np.int32)[own]))
-        eng.mask.copy_(torch.from_numpy(np.asarray(dataset.train_mask, dtype=np.uint8)[own]))
+        lab, msk = np.asarray(dataset.labels)[own], np.asarray(dataset.train_mask)[own]
+        eng.labels.copy_(pinned_rows(dataset, "labels", lab, torch.int32), non_blocking=True)
+        eng.mask.copy_(pinned_rows(dataset, "mask", msk, torch.uint8), non_blocking=True)
         eng.mask_count = int(np.count_nonzero(dataset.train_mask))
         self.model = copy_model(model)
         eng.wts.load(self.model)
@@ -318,6 +319,19 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
     if epochs == 0:
         trained = copy_model(model)
     return trained, trace, getattr(hierarchy, "ledger", None)
+
+
+def pinned_rows(dataset: LabeledDataset, name: str, values: np.ndarray, dtype) -> torch.Tensor:
+    """``values`` converted to ``dtype`` in a page-locked staging buffer kept
+    on the dataset (refilled every call), so its H2D copy is a true async
+    DMA instead of a pageable copy."""
+    key = "_pinned_" + name
+    stage = getattr(dataset, key, None)
+    if stage is None or stage.numel() != values.size or stage.dtype != dtype:
+        stage = torch.empty(values.size, dtype=dtype).pin_memory()
+        setattr(dataset, key, stage)
+    np.copyto(stage.numpy(), values, casting="unsafe")
+    return stage
 
 
 def pinned_features(dataset: LabeledDataset) -> torch.Tensor:
