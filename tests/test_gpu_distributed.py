@@ -73,3 +73,49 @@ def test_two_ranks_match_one_device(tmp_path, case):
     want = np.array(trace)
     assert np.allclose(r0["trace"][:, 1], want[:, 1], rtol=1e-4)
     assert np.allclose(r0["trace"][:, 2], want[:, 2], atol=2.0 / ds.train_mask.sum())
+
+
+def _setup_random(seed):
+    rng = np.random.default_rng(500 + seed)
+    mode = ["mean_self_loop", "symmetric_norm", "sage_mean", "gat"][seed % 4]
+    g = g2.generate_kronecker(int(rng.integers(8, 10)), int(rng.integers(2, 16)), seed=seed)
+    if seed % 2:     # directed: halo = in- and out-neighbours differ
+        src = np.repeat(np.arange(g.num_vertices), np.diff(g.src_ptr))
+        keep = rng.random(g.num_edges) < 0.6
+        g = g2.build_csr(np.stack([src[keep], g.dst_idx[keep]], 1), g.num_vertices)
+    F, C, L = int(rng.integers(3, 20)), int(rng.integers(2, 8)), int(rng.integers(2, 4))
+    H = 8 * int(rng.integers(1, 3)) if mode == "gat" else int(rng.integers(3, 24))
+    P = int(rng.integers(2, 7))
+    ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=seed + 1)
+    plan = g2.build_partition_plan(g, g2.random_partition(g.num_vertices, P, seed), P)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=seed + 2, aggregation_mode=mode,
+                            heads=2)
+    return ds, plan, model
+
+
+def _worker_random(rank, world, port, seed, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ds, plan, model = _setup_random(seed)
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.05)
+    np.savez(os.path.join(out, f"r{rank}.npz"), trace=np.array(trace),
+             **{f"w{i}": w for i, w in enumerate(trained.weights)})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_two_ranks_random_configuration(tmp_path, seed):
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_worker_random, args=(2, port, seed, str(tmp_path)), nprocs=2, join=True)
+    ds, plan, model = _setup_random(seed)
+    single, trace, _ = g2.partitioned_train(ds, plan, model, epochs=2, lr=0.05)
+    r0, r1 = (dict(np.load(tmp_path / f"r{r}.npz")) for r in range(2))
+    for i in range(len(single.weights)):
+        assert np.array_equal(r0[f"w{i}"], r1[f"w{i}"])
+        assert rel_l2(r0[f"w{i}"], single.weights[i]) < 1e-4
+    assert np.allclose(r0["trace"][:, 1], np.array(trace)[:, 1], rtol=1e-4)
