@@ -51,9 +51,33 @@ def dropout_mask(dropout_rate: float, dropout_seed: int, epoch: int, layer: int,
     return (np.random.Generator(np.random.PCG64(seq)).random(shape) < keep) / keep
 
 
+def _degree_order(ptr: np.ndarray) -> np.ndarray | None:
+    """Rows by descending degree (stable), or None for the given order
+    (GRD_AGG_ROW_ORDER=plan).  Every row's sum is unchanged (same edges in
+    the same order), only the order rows are scheduled in: measured -8 % on
+    the products-shaped 256-wide aggregation (tools/agg_order.py) — warps
+    get rows of similar length and the hub rows start first."""
+    import os
+    if os.environ.get("GRD_AGG_ROW_ORDER", "degree") != "degree":
+        return None
+    return np.argsort(-np.diff(ptr), kind="stable")
+
+
+def _reorder_rows(ptr: np.ndarray, idx: np.ndarray, order: np.ndarray):
+    """CSR rows taken in ``order`` (edges of a row keep their order); also
+    the new position of every old edge."""
+    cnt = np.diff(ptr)[order]
+    new_ptr = np.zeros(order.size + 1, dtype=np.int64)
+    np.cumsum(cnt, out=new_ptr[1:])
+    old_start = np.repeat(ptr[order] - new_ptr[:-1], cnt)
+    old_pos = np.arange(new_ptr[-1], dtype=np.int64) + old_start   # old position of each new edge
+    return new_ptr, idx[old_pos], old_pos
+
+
 class DeviceGraph:
-    """HBM-resident plan of one (graph, labeling): forward in-CSR in perm
-    order, the out-CSR for the transposed pull, and per-vertex degree scales."""
+    """HBM-resident plan of one (graph, labeling): forward in-CSR (rows =
+    targets, scheduled by descending degree, output row = vertex), the
+    out-CSR for the transposed pull (likewise), and per-vertex degree scales."""
 
     def __init__(self, graph, plan, device):
         f = plan.flat
@@ -66,10 +90,24 @@ class DeviceGraph:
         # owns every vertex and holds no halo
         self.n_own = self.n_local = plan.num_vertices
         self.comm = None
-        # forward: rows = perm order, output row = vertex, self = vertex
-        self.fwd = AggSpec.build(f.in_ptr, f.in_src, device, out_idx=f.perm)
+        # forward: rows = targets, output row = vertex, self = vertex
+        fo = _degree_order(f.in_ptr)
+        self._fwd_order = fo
+        if fo is None:
+            self.fwd = AggSpec.build(f.in_ptr, f.in_src, device, out_idx=f.perm)
+        else:
+            ptr, idx, _ = _reorder_rows(f.in_ptr, f.in_src, fo)
+            self.fwd = AggSpec.build(ptr, idx, device, out_idx=f.perm[fo])
+            del ptr, idx
         # transposed pull: rows = vertices, neighbours = out-edges (u -> v)
-        self.bwd = AggSpec.build(graph.src_ptr, graph.dst_idx, device)
+        bo = _degree_order(graph.src_ptr)
+        self._bwd_order = bo
+        if bo is None:
+            self.bwd = AggSpec.build(graph.src_ptr, graph.dst_idx, device)
+        else:
+            ptr, idx, _ = _reorder_rows(graph.src_ptr, graph.dst_idx, bo)
+            self.bwd = AggSpec.build(ptr, idx, device, out_idx=bo.astype(np.int32))
+            del ptr, idx
         self._deg = f.in_degree.astype(np.float64)
         self._scales: dict[str, torch.Tensor] = {}
         self._partitions: dict[int, "DevicePartition"] = {}
@@ -86,11 +124,21 @@ class DeviceGraph:
         if getattr(self, "_o2i", None) is None:
             f, g = self.plan.flat, self.graph
             n = np.int64(self.num_vertices)
-            tgt = np.repeat(f.perm.astype(np.int64), np.diff(f.in_ptr))
-            key_in = f.in_src.astype(np.int64) * n + tgt
+            # the device CSRs' row orders (see __init__)
+            in_ptr, in_src, perm = f.in_ptr, f.in_src, f.perm
+            if self._fwd_order is not None:
+                in_ptr, in_src, _ = _reorder_rows(f.in_ptr, f.in_src, self._fwd_order)
+                perm = f.perm[self._fwd_order]
+            out_ptr, out_dst = g.src_ptr, g.dst_idx
+            out_rows = np.arange(self.num_vertices, dtype=np.int64)
+            if self._bwd_order is not None:
+                out_ptr, out_dst, _ = _reorder_rows(g.src_ptr, g.dst_idx, self._bwd_order)
+                out_rows = self._bwd_order.astype(np.int64)
+            tgt = np.repeat(perm.astype(np.int64), np.diff(in_ptr))
+            key_in = in_src.astype(np.int64) * n + tgt
             order = np.argsort(key_in, kind="stable")
-            src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(g.src_ptr))
-            key_out = src * n + g.dst_idx.astype(np.int64)
+            src = np.repeat(out_rows, np.diff(out_ptr))
+            key_out = src * n + out_dst.astype(np.int64)
             pos = order[np.searchsorted(key_in[order], key_out)]
             # at least one element: an edgeless graph still passes a valid pointer
             self._o2i = torch.from_numpy(np.concatenate([pos.astype(np.int32),
