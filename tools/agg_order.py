@@ -55,8 +55,14 @@ def timeit(sp, reps=10):
 
 
 rng = np.random.default_rng(0)
+lg = np.floor(np.log2(np.maximum(deg_v, 1))).astype(np.int64)
+rank = np.empty(n, np.int64)
+rank[f.perm] = np.arange(n)
 orders = {"plan (partition) order": f.perm.astype(np.int64), "vertex order": np.arange(n),
-          "random order": rng.permutation(n), "descending degree": np.argsort(-deg_v, kind="stable")}
+          "random order": rng.permutation(n), "descending degree": np.argsort(-deg_v, kind="stable"),
+          "ascending degree": np.argsort(deg_v, kind="stable"),
+          "log2-degree buckets desc, plan order inside": np.lexsort((rank, -lg)),
+          "log2-degree buckets desc, vertex order inside": np.lexsort((np.arange(n), -lg))}
 ref = None
 for name, order in orders.items():
     sp = spec_for(order)
