@@ -275,9 +275,16 @@ __global__ void __launch_bounds__(256) gat_softmax_heavy_kernel(grd_gat_args a) 
 // suffices.  Per-head dot products are reduced through shared memory.
 constexpr int kU = 4;
 
+// Per-lane partial dot products live in part[][j][.] with every head's cph
+// chunks followed by one pad slot and rows kPartStride (= 4 mod 32) apart:
+// the head sums then read 16 (edge, head) slots on distinct banks (the
+// unpadded layout made them 6.6-way bank conflicts: 85 % of the kernel's
+// shared-load wavefronts, ncu).
+constexpr int kPartStride = 100;
+
 template <int NV>
 __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
-    __shared__ float part[8][kU][kWarp * NV];
+    __shared__ float part[8][kU][kPartStride];
     __shared__ float cs[8][kMaxHeads];
     const int lane = threadIdx.x & (kWarp - 1);
     const int wib = threadIdx.x / kWarp;
@@ -288,6 +295,13 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
     const int q4 = a.hdp / 4;
     const int cph = a.dhp / 4;
     const int32_t v = vertex_of(a, un.row);
+    const int hs = cph + 1;                    // padded head slot
+    int pq[NV];                                // padded slot of chunk lane + 32 c
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = lane + c * kWarp;
+        pq[c] = (q / cph) * hs + q % cph;
+    }
     float4 g[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) {
@@ -299,12 +313,12 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
             const float4 o = *reinterpret_cast<const float4*>(a.o_fwd + int64_t(v) * a.ld_o + 4 * q);
             d = g[c].x * o.x + g[c].y * o.y + g[c].z * o.z + g[c].w * o.w;
         }
-        part[wib][0][q] = d;
+        if (q < q4) part[wib][0][pq[c]] = d;
     }
     __syncwarp();
     if (lane < H) {
         float c = 0.f;
-        for (int k = 0; k < cph; ++k) c += part[wib][0][lane * cph + k];
+        for (int k = 0; k < cph; ++k) c += part[wib][0][lane * hs + k];
         cs[wib][lane] = c;
     }
     __syncwarp();
@@ -342,12 +356,13 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
         for (int j = 0; j < kU; ++j)
 #pragma unroll
             for (int c = 0; c < NV; ++c)
-                part[wib][j][lane + c * kWarp] = g[c].x * p[j][c].x + g[c].y * p[j][c].y +
-                                                 g[c].z * p[j][c].z + g[c].w * p[j][c].w;
+                if (lane + c * kWarp < q4)
+                    part[wib][j][pq[c]] = g[c].x * p[j][c].x + g[c].y * p[j][c].y +
+                                          g[c].z * p[j][c].z + g[c].w * p[j][c].w;
         __syncwarp();
         if (mine) {
             float da = 0.f;
-            for (int k = 0; k < cph; ++k) da += part[wib][my_j][my_h * cph + k];
+            for (int k = 0; k < cph; ++k) da += part[wib][my_j][my_h * hs + k];
             const float d = al_my * (da - c_my) * lrelu_grad(s_my + t_my, a.slope);
             if (im < ne)
                 a.delta[(un.beg + im) * H + my_h] = d;
