@@ -349,6 +349,15 @@ int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t n_rows,
                      const uint8_t* mask, int64_t mask_count,
                      float* grad, int64_t ld_grad, const float* grad_scale,
                      double* partials, double* stats_out, void* stream);
+/* grd_softmax_xent that also writes grad2[r, :] = grad[r, :] * grad2_scale[r]
+ * (e.g. GraphSAGE's 1/deg source scale of the following transposed pull,
+ * applied once per row instead of once per edge). */
+int grd_softmax_xent2(const float* logits, int64_t ld_logits, int64_t n_rows,
+                      int32_t n_classes, const int32_t* labels, const uint8_t* mask,
+                      int64_t mask_count, float* grad, int64_t ld_grad,
+                      const float* grad_scale, float* grad2, int64_t ld_grad2,
+                      const float* grad2_scale, double* partials, double* stats_out,
+                      void* stream);
 
 /* Elementwise helpers. */
 /* y[i,:] = x[i,:] * m[i,:]  (dropout, training.py:178-185,297). */

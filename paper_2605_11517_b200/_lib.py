@@ -174,6 +174,8 @@ SIGNATURES = {
     "grd_loss_partials": (c_i64, [c_i64]),
     "grd_softmax_xent": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                  c_vp, c_vp, c_vp]),
+    "grd_softmax_xent2": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
+                                  c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "grd_mul_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_mask_scale_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64,
                                     c_vp]),

@@ -524,7 +524,9 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
                                                    int64_t n_rows, int c, const int32_t* __restrict__ labels,
                                                    const uint8_t* __restrict__ mask, float inv_count,
                                                    float* __restrict__ grad, int64_t ldg,
-                                                   const float* __restrict__ gscale, double* partials) {
+                                                   const float* __restrict__ gscale, double* partials,
+                                                   float* __restrict__ grad2, int64_t ldg2,
+                                                   const float* __restrict__ g2scale) {
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x / kWarp;
     const int c4 = (c + 3) / 4 * 4;
@@ -554,10 +556,19 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
             bool non = false;
             if (r + nwarps < n_rows) load(r + nwarps, n0, n1, ny, non);
             float* grow = grad + r * ldg;
-            if (lane < c4 - c) grow[c + lane] = 0.f;
+            float* grow2 = grad2 ? grad2 + r * ldg2 : nullptr;
+            const float s2 = grad2 ? g2scale[r] : 0.f;
+            if (lane < c4 - c) {
+                grow[c + lane] = 0.f;
+                if (grow2) grow2[c + lane] = 0.f;
+            }
             if (!on) {
                 if (lane < c) grow[lane] = 0.f;
                 if (lane + kWarp < c) grow[lane + kWarp] = 0.f;
+                if (grow2) {
+                    if (lane < c) grow2[lane] = 0.f;
+                    if (lane + kWarp < c) grow2[lane + kWarp] = 0.f;
+                }
             } else {
                 float mx = v0;
                 int arg = lane < c ? lane : 0x7fffffff;
@@ -577,12 +588,16 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
                 if (lane < c) {
                     float pr = e0 / sum;
                     if (lane == y) pr -= 1.0f;
-                    grow[lane] = pr * inv_count * scale;
+                    const float gv = pr * inv_count * scale;
+                    grow[lane] = gv;
+                    if (grow2) grow2[lane] = gv * s2;     // the pull's source scale, pre-applied
                 }
                 if (lane + kWarp < c) {
                     float pr = e1 / sum;
                     if (lane + kWarp == y) pr -= 1.0f;
-                    grow[lane + kWarp] = pr * inv_count * scale;
+                    const float gv = pr * inv_count * scale;
+                    grow[lane + kWarp] = gv;
+                    if (grow2) grow2[lane + kWarp] = gv * s2;
                 }
                 const float ey = __shfl_sync(0xffffffffu, y < kWarp ? e0 : e1, y & (kWarp - 1));
                 if (lane == 0) {
@@ -598,11 +613,19 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
          r += nwarps) {
         const float* row = logits + r * ldl;
         float* grow = grad + r * ldg;
+        float* grow2 = grad2 ? grad2 + r * ldg2 : nullptr;
+        const float s2 = grad2 ? g2scale[r] : 0.f;
         // padding columns [c, round_up(c, 4)) are part of the 16-byte rows the
         // aggregation kernels read: keep them zero
-        if (lane < c4 - c) grow[c + lane] = 0.f;
+        if (lane < c4 - c) {
+            grow[c + lane] = 0.f;
+            if (grow2) grow2[c + lane] = 0.f;
+        }
         if (!mask[r]) {
-            for (int j = lane; j < c; j += kWarp) grow[j] = 0.f;
+            for (int j = lane; j < c; j += kWarp) {
+                grow[j] = 0.f;
+                if (grow2) grow2[j] = 0.f;
+            }
             continue;
         }
         // max and first argmax (np.argmax semantics)
@@ -625,7 +648,9 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
         for (int j = lane; j < c; j += kWarp) {
             float p = expf(row[j] - mx) / sum;
             if (j == y) p -= 1.0f;
-            grow[j] = p * inv_count * scale;
+            const float gv = p * inv_count * scale;
+            grow[j] = gv;
+            if (grow2) grow2[j] = gv * s2;
         }
         if (lane == 0) {
             const float py = expf(row[y] - mx) / sum;
@@ -935,7 +960,16 @@ extern "C" int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t 
                                 const int32_t* labels, const uint8_t* mask, int64_t mask_count, float* grad,
                                 int64_t ld_grad, const float* grad_scale, double* partials, double* stats_out,
                                 void* stream) {
+    return grd_softmax_xent2(logits, ld_logits, n_rows, n_classes, labels, mask, mask_count, grad, ld_grad,
+                             grad_scale, nullptr, 0, nullptr, partials, stats_out, stream);
+}
+
+extern "C" int grd_softmax_xent2(const float* logits, int64_t ld_logits, int64_t n_rows, int32_t n_classes,
+                                 const int32_t* labels, const uint8_t* mask, int64_t mask_count, float* grad,
+                                 int64_t ld_grad, const float* grad_scale, float* grad2, int64_t ld_grad2,
+                                 const float* grad2_scale, double* partials, double* stats_out, void* stream) {
     clear_error();
+    if (grad2 && (!grad2_scale || ld_grad2 < n_classes)) return fail(kErrArg, "softmax_xent: grad2 needs its scale");
     if ((n_rows > 0 && (!logits || !labels || !mask || !grad)) || !partials || !stats_out || n_classes <= 0 ||
         n_rows < 0)
         return fail(kErrArg, "softmax_xent: bad arguments");
@@ -943,7 +977,7 @@ extern "C" int grd_softmax_xent(const float* logits, int64_t ld_logits, int64_t 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const float inv = static_cast<float>(1.0 / static_cast<double>(mask_count));
     xent_kernel<<<kLossBlocks, 256, 0, st>>>(logits, ld_logits, n_rows, n_classes, labels, mask, inv, grad,
-                                             ld_grad, grad_scale, partials);
+                                             ld_grad, grad_scale, partials, grad2, ld_grad2, grad2_scale);
     int rc = launch_status("softmax_xent");
     if (rc) return rc;
     xent_finalize_kernel<<<1, 1024, 0, st>>>(partials, kLossBlocks, static_cast<double>(mask_count), stats_out);

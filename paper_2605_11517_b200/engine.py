@@ -591,6 +591,11 @@ class LayerwiseEngine(_EngineBase):
             self.t2 = ops.zeros_rows(self.NL, self.maxw, dev)
         elif model.kind != "gat":
             self.t2 = None
+        # GraphSAGE, transform-first last layer: the loss also writes its
+        # gradient pre-scaled by 1/deg, the source scale of the pull that
+        # follows (once per row instead of once per edge)
+        cl = self.cfg[-1]
+        self.g2 = ops.zeros_rows(self.NL, cl.d_out, dev) if (cl.sage and cl.transform_first) else None
         # one device: SGD fused into the weight-gradient reduction; sharded:
         # local weight gradients are all-reduced first, SGD at epoch end
         self.defer_sgd = self.comm is not None
@@ -654,8 +659,12 @@ class LayerwiseEngine(_EngineBase):
         if c.transform_first:
             # [gp | H_nbr] with H_nbr = mean_in^T gp (pull over out-edges, 1/deg_v per edge)
             gcat = self.g[:, : 2 * c.ld_out]
-            dg.exchange_agg("bwd", gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
-                            no_self=True)                          # halo rows of gp
+            if c.last and getattr(self, "g2", None) is not None:
+                # the loss wrote gp / deg as well: an unscaled pull
+                dg.exchange_agg("bwd", self.g2, gcat[:, c.ld_out:], c.d_out, no_self=True)
+            else:
+                dg.exchange_agg("bwd", gcat[:, : c.ld_out], gcat[:, c.ld_out:], c.d_out, src_scale=inv_deg,
+                                no_self=True)                      # halo rows of gp
             if l > 0:
                 ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
             ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=self._w(W), lr=lr)
@@ -779,8 +788,10 @@ class LayerwiseEngine(_EngineBase):
     def loss(self) -> None:
         c = self.cfg[-1]
         _, scale = self._consumer_epilogue(self.L - 1)
+        extra = {} if getattr(self, "g2", None) is None else dict(grad2=self.g2,
+                                                                   grad2_scale=self.dg.scale("inv_deg"))
         ops.softmax_xent(self.acts[-1], self.V, c.d_out, self.labels, self.mask, self.mask_count,
-                         self.g, self.stats, self.partials, grad_scale=scale)
+                         self.g, self.stats, self.partials, grad_scale=scale, **extra)
         if self.comm is not None:
             self.comm.all_reduce_sum(self.stats)   # {loss, acc, sums}: partial / global count
 

@@ -286,13 +286,16 @@ def rownorm_bwd(pre: torch.Tensor, grad_y: torch.Tensor, grad_pre: torch.Tensor,
 
 def softmax_xent(logits: torch.Tensor, n_rows: int, n_classes: int, labels: torch.Tensor,
                  mask: torch.Tensor, mask_count: int, grad: torch.Tensor, stats: torch.Tensor,
-                 partials: torch.Tensor, grad_scale=None) -> None:
-    """stats (float64 cuda[4]) <- {loss, accuracy, loss_sum, correct}."""
+                 partials: torch.Tensor, grad_scale=None, grad2=None, grad2_scale=None) -> None:
+    """stats (float64 cuda[4]) <- {loss, accuracy, loss_sum, correct};
+    optionally grad2 = grad * grad2_scale (per row) as well."""
     n, c = int(n_rows), int(n_classes)
     nbytes = 8 * n * c + 9 * n + 4 * n * (grad_scale is not None)
-    _launch("softmax_xent", 2, nbytes, 6.0 * n * c, lambda: _lib.check(_lib.lib().grd_softmax_xent(
+    nbytes += (4 * n * c + 4 * n) * (grad2 is not None)
+    _launch("softmax_xent", 2, nbytes, 6.0 * n * c, lambda: _lib.check(_lib.lib().grd_softmax_xent2(
         _p(logits), _ld(logits), n, c, _p(labels), _p(mask), int(mask_count), _p(grad), _ld(grad),
-        _p(grad_scale), _p(partials), _p(stats), stream_ptr()), "softmax_xent"))
+        _p(grad_scale), _p(grad2), _ld(grad2) if grad2 is not None else 0, _p(grad2_scale),
+        _p(partials), _p(stats), stream_ptr()), "softmax_xent"))
 
 
 def loss_partials(n_rows: int, device) -> torch.Tensor:
