@@ -320,6 +320,8 @@ typedef struct grd_gemm_args {
     int32_t accumulate;
     float* workspace;          /* >= grd_gemm_workspace(n, k) floats */
     int64_t workspace_elems;
+    float* c2; int64_t ldc2;   /* optional: columns >= split go to c2[:, col - split] */
+    int64_t split;             /* (multiple of 4; not with accumulate / relu_ref / elem_mul) */
 } grd_gemm_args;
 int64_t grd_gemm_workspace(int64_t n, int64_t k);
 int grd_gemm(const grd_gemm_args* args, void* stream);

@@ -130,6 +130,9 @@ class GrdGemmArgs(ctypes.Structure):
         ("accumulate", c_i32),
         ("workspace", c_vp),
         ("workspace_elems", c_i64),
+        ("c2", c_vp),
+        ("ldc2", c_i64),
+        ("split", c_i64),
     ]
 
 

@@ -893,6 +893,13 @@ extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
     t.relu_ref = g.relu_ref; t.ld_relu_ref = g.ld_relu_ref;
     t.relu_out = g.relu_out; t.accumulate = g.accumulate;
     t.k_splits = 1;
+    if (g.c2) {
+        if (g.split <= 0 || g.split % 4 || g.ldc2 % 4 || g.accumulate || g.relu_ref || g.elem_mul ||
+            (reinterpret_cast<uintptr_t>(g.c2) & 15))
+            return fail(kErrArg, "gemm: split output needs split %% 4 == 0, aligned c2, no accumulate / "
+                        "relu_ref / elem_mul");
+        t.c2 = g.c2; t.ldc2 = g.ldc2; t.split = g.split;
+    }
     if (g.lda % 4 || g.ldb % 4 || g.ldc % 4 || (reinterpret_cast<uintptr_t>(g.a) & 15) ||
         (reinterpret_cast<uintptr_t>(g.c) & 15))
         return fail(kErrArg, "gemm: leading dims must be multiples of 4 and rows 16-byte aligned");

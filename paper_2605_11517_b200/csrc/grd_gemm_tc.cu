@@ -78,6 +78,7 @@ struct Params {
     int relu_out;
     int accumulate;
     float* partial; int64_t ld_partial;   // split-K: [z][m][ld_partial]
+    float* c2; int64_t ldc2; int64_t split;   // columns >= split (> 0) go to c2
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -286,6 +287,7 @@ __device__ __forceinline__ void epi_prefetch(const Params& p, int64_t row, int64
     }
 }
 
+template <bool kSplit>
 __device__ __forceinline__ void epi_store_direct(const Params& p, const float (&v)[32], int64_t row, int64_t col0,
                                                  int z, const EpiIn& in) {
     if (row >= p.m) return;
@@ -303,6 +305,9 @@ __device__ __forceinline__ void epi_store_direct(const Params& p, const float (&
     for (int j = 0; j < 32; j += 4) {
         const int64_t n = col0 + j;
         if (n >= n_pad) continue;
+        // columns >= split go to the second destination (host-checked: no
+        // accumulate / relu_ref / elem_mul operands with a split output)
+        float* dst = (kSplit && p.split > 0 && n >= p.split) ? p.c2 + row * p.ldc2 + (n - p.split) : crow + j;
         float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         const float4 oo = in.o[j / 4];
         x.x += oo.x; x.y += oo.y; x.z += oo.z; x.w += oo.w;
@@ -319,13 +324,13 @@ __device__ __forceinline__ void epi_store_direct(const Params& p, const float (&
         if (p.relu_out) {
             x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
         }
-        *reinterpret_cast<float4*>(crow + j) = x;
+        *reinterpret_cast<float4*>(dst) = x;
     }
 }
 
 // Epilogue warps' loop over the tiles of this CTA (both kernels): TMEM
 // accumulator `acc` of the i-th tile with K work, drained chunk by chunk.
-template <bool kPair, class TileFn>
+template <bool kPair, bool kSplit, class TileFn>
 __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
                                               int warp, int lane, int64_t t0, int64_t tstep,
                                               int64_t ntiles, TileFn tile_of) {
@@ -359,7 +364,7 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
                 for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
             if (row0 >= p.m || n0 + c0 >= n_pad) continue;   // warp-uniform
-            epi_store_direct(p, v, row0 + lane, n0 + c0, z, in);
+            epi_store_direct<kSplit>(p, v, row0 + lane, n0 + c0, z, in);
         }
         if (has_k) {
             // a warp without columns in this tile (bn <= 32) still waits for
@@ -376,7 +381,7 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
 
 // kPair: a kernel containing cta_group::2 instructions must be launched in
 // clusters of 2, so the CTA-pair variant is its own instantiation.
-template <bool kPair>
+template <bool kPair, bool kSplit>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const Params p) {
@@ -599,7 +604,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
     } else {
         // ---------------------------------------------------- epilogue --
-        epilogue_loop<kPair>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles,
+        epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles,
                       [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
                           z = static_cast<int>(t / (mg * nt));
                           const int64_t r = t % (mg * nt);
@@ -818,7 +823,7 @@ gemm_bf16x3_ws(const __grid_constant__ CUtensorMap map_a, const Params p) {
             }
         }
     } else {
-        epilogue_loop<false>(p, tmem, tfull, tempty, warp, lane, blockIdx.x, gridDim.x,
+        epilogue_loop<false, false>(p, tmem, tfull, tempty, warp, lane, blockIdx.x, gridDim.x,
                       ntiles, [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
                           m0 = (t / nt) * kBM;
                           n0 = (t % nt) * bn;
@@ -1011,6 +1016,9 @@ static cudaError_t gemm_bf16x3(const GrdTcGemm& g, cudaStream_t st) {
     p.relu_out = g.relu_out;
     p.accumulate = g.accumulate;
     p.b_packed = g.b_packed;
+    p.c2 = g.c2;
+    p.ldc2 = g.ldc2;
+    p.split = g.c2 ? g.split : 0;
     p.a_mode = kKMajorTma;
     p.b_mode = kPacked;
     CUtensorMap map_a{};
@@ -1054,6 +1062,9 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     p.accumulate = g.accumulate;
     p.partial = g.partial;
     p.ld_partial = (g.n + 3) / 4 * 4;
+    p.c2 = g.c2;
+    p.ldc2 = g.ldc2;
+    p.split = g.c2 ? g.split : 0;
     CUtensorMap map_a{}, map_b{};
     // A(m, k): K-major TMA when stored M x K, MN-major boxes when stored K x M.
     if (!g.trans_a) {
@@ -1089,10 +1100,11 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(gemm_tf32x3_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaSuccess;
+        for (auto fn : {gemm_tf32x3_ws<false, false>, gemm_tf32x3_ws<true, false>, gemm_tf32x3_ws<false, true>,
+                        gemm_tf32x3_ws<true, true>})
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -1106,7 +1118,8 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     const int64_t max_cl = num_sms() / C;
     const int grid = static_cast<int>((tiles < max_cl ? tiles : max_cl) * C);
     if (C == 1) {
-        gemm_tf32x3_ws<false><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        if (p.split > 0) gemm_tf32x3_ws<false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        else gemm_tf32x3_ws<false, false><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -1121,8 +1134,12 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     attr_c[0].val.clusterDim.z = 1;
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
-    if (p.pair) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true>, map_a, map_b, p);
-    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false>, map_a, map_b, p);
+    if (p.pair) {
+        if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, true>, map_a, map_b, p);
+        return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false>, map_a, map_b, p);
+    }
+    if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, true>, map_a, map_b, p);
+    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, false>, map_a, map_b, p);
 }
 
 cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,

@@ -20,6 +20,8 @@ struct GrdTcGemm {
     float* partial;
     const float* b_packed;   // opB pre-split by grd_tc_pack_b (then b/ldb/trans_b unused)
     int bf16;                // bf16x3 split (row-major A, packed B); else 3xTF32
+    float* c2; int64_t ldc2; // columns >= split (> 0) go to c2 (plain stores only)
+    int64_t split;
 };
 
 cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st);

@@ -632,11 +632,17 @@ class LayerwiseEngine(_EngineBase):
         c, dg = self.cfg[l], self.dg
         W = self.wts.w[l]
         if c.transform_first:
-            # Y = X [W_root | W_nbr] (one GEMM), out = Y_root + mean_in(Y_nbr)
-            y = self.t1[:, : 2 * c.ld_out]
-            ops.gemm(x, W, y, self.V, 2 * c.ld_out, c.d_in)
-            dg.exchange_agg("fwd", y[:, c.ld_out:], out, c.d_out, post_div_deg=2, no_self=True,
-                            add_y=y[:, : c.ld_out], relu=relu)      # halo rows of X W_nbr
+            # Y = X [W_root | W_nbr] (one GEMM, its two column halves written to
+            # two dense planes), out = Y_root + mean_in(Y_nbr): the gathered
+            # Y_nbr rows are not interleaved with Y_root (narrow rows: whole
+            # sectors instead of half-used ones)
+            lo = c.ld_out
+            plane = self.t1.view(-1)
+            yr = plane[: self.NL * lo].view(self.NL, lo)
+            yn = plane[self.NL * lo: 2 * self.NL * lo].view(self.NL, lo)
+            ops.gemm(x, W, yr, self.V, 2 * lo, c.d_in, c2=yn, split=lo)
+            dg.exchange_agg("fwd", yn, out, c.d_out, post_div_deg=2, no_self=True,
+                            add_y=yr, relu=relu)                    # halo rows of X W_nbr
         elif l == 0 and self.xn is not None:
             # N = mean_in(X) beside X, out = [X | N] [W_root ; W_nbr]
             n = self.xn[:, c.ld_in: 2 * c.ld_in]

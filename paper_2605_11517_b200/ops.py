@@ -185,8 +185,9 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
          trans_a=False, trans_b=False, row_scale=None, elem_mul=None, relu_ref=None,
-         relu_out=False, accumulate=False) -> None:
-    """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim."""
+         relu_out=False, accumulate=False, c2=None, split=0) -> None:
+    """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim;
+    with c2, columns >= split land in c2[:, col - split] instead."""
     g = _lib.GrdGemmArgs()
     g.m, g.n, g.k = int(m), int(n), int(k)
     g.a, g.lda, g.trans_a = _p(a), _ld(a), int(bool(trans_a))
@@ -199,6 +200,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: i
     g.ld_relu_ref = _ld(relu_ref) if relu_ref is not None else 0
     g.relu_out = int(bool(relu_out))
     g.accumulate = int(bool(accumulate))
+    g.c2 = _p(c2)
+    g.ldc2 = _ld(c2) if c2 is not None else 0
+    g.split = int(split) if c2 is not None else 0
     m, n, k = int(m), int(n), int(k)
     need = int(_lib.lib().grd_gemm_workspace(n, k))
     ws = _workspace(("pack", c.device), need)

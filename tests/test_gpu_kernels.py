@@ -297,3 +297,21 @@ print(worst)
                          cwd=str(Path(__file__).resolve().parents[1]), timeout=300)
     assert out.returncode == 0, out.stderr
     assert float(out.stdout.strip().splitlines()[-1]) < 2e-5
+
+
+@pytest.mark.parametrize("m,n2,k", [(1000, 48, 100), (2000, 256, 96), (300, 12, 7)])
+def test_gemm_split_output(m, n2, k):
+    """Columns >= split of one GEMM land in a second dense matrix (the
+    GraphSAGE [Y_root | Y_nbr] planes)."""
+    rng = np.random.default_rng(m + n2)
+    a = rng.normal(size=(m, k))
+    b = rng.normal(size=(k, 2 * n2))
+    c1 = ops.zeros_rows(m, n2, DEV)
+    c2 = ops.zeros_rows(m, n2, DEV)
+    ldb = (n2 + 3) // 4 * 4
+    bp = np.zeros((k, 2 * ldb))
+    bp[:, :n2], bp[:, ldb:ldb + n2] = b[:, :n2], b[:, n2:]
+    ops.gemm(_dev(a), _dev(bp), c1, m, 2 * ldb, k, c2=c2, split=ldb, relu_out=True)
+    full = np.maximum(a @ b, 0)
+    assert rel_l2(_host(c1, n2), full[:, :n2]) < 5e-6
+    assert rel_l2(_host(c2, n2), full[:, n2:]) < 5e-6
