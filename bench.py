@@ -373,7 +373,7 @@ def run_ours(args, spec, rank, world, local_rank):
             "num_edges": E, "layers": L, "hidden": spec["H"], "features": spec["F"],
             "classes": spec["C"], "partitions": spec["P"], "aggregation": spec["mode"],
             "parallelism": "single" if world == 1 else
-            f"partition-parallel x{world} (halo all-to-all + grad all-reduce over NCCL)",
+            f"partition-parallel x{world} (halo all-to-all + grad all-reduce over {backend.upper()})",
             "l2": "flushed (512 MiB write) before every timed step", "lr": LR,
             "preprocess": prep, "loss_last_step": loss, "acc_last_step": acc,
             "storage_read_bytes_per_epoch": storage_bytes if streaming else None,
