@@ -350,6 +350,9 @@ def run_ours(args, spec, rank, world, local_rank):
                 per_launch_s = r["ms_per_epoch"] * 1e-3 / r["launches_per_epoch"]
                 r["dram_GBs_implied"] = round(r["traffic"] / per_launch_s / 1e9, 1)
                 r["dram_frac"] = round(r["dram_GBs_implied"] / hbm_peak, 4)
+                r["note"] = ("achieved/frac count algorithmic bytes (SURVEY 8(d) per-edge streaming "
+                             "model); 43-69 % of the row gathers hit L2, so DRAM moves less: "
+                             "traffic / dram_frac are the ncu DRAM side")
     edges_per_epoch = L * E
     # strong scaling: the N ranks together train ONE epoch of the whole graph,
     # so the job processes L*|E| edges per step whatever N is
