@@ -297,22 +297,28 @@ __device__ __forceinline__ void cp_wait() {
 
 constexpr int kAsyncWarps = 4;   // warps per block of the staged kernel
 
-template <int NV, int G, int K, bool SCALED>
+// MODE: 0 unweighted, 1 source-scaled (src_scale[j]), 2 GAT per-edge
+// per-head weights (edge_w[perm(e), head(chunk)], self_w for the self item),
+// each lane copying the NV weights of its own chunks.
+template <int NV, int G, int K, int MODE>
 __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_agg_args a, int64_t light_warps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool SCALED = MODE == 1;
+    constexpr bool WE = MODE == 2;
     constexpr int kSlots = G * K;                     // rows in flight per warp
+    constexpr int kWN = WE ? NV : (SCALED ? 1 : 0);   // weights per slot and lane
     const int lane = threadIdx.x & (kWarp - 1);
     const int wib = threadIdx.x / kWarp;
     float4* ring = reinterpret_cast<float4*>(smem_raw) + size_t(wib) * kSlots * NV * kWarp;
     float* wring = reinterpret_cast<float*>(reinterpret_cast<float4*>(smem_raw) +
                                             size_t(kAsyncWarps) * kSlots * NV * kWarp) +
-                   size_t(wib) * kSlots * kWarp;
+                   size_t(wib) * kSlots * kWN * kWarp;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
     const int w4 = (a.width + 3) / 4;
     const int ldp = 4 * w4;
     int hd[NV];
 #pragma unroll
-    for (int c = 0; c < NV; ++c) hd[c] = 0;
+    for (int c = 0; c < NV; ++c) hd[c] = WE ? min((4 * (lane + c * kWarp)) / a.head_ld, a.heads - 1) : 0;
 
     int64_t r, beg, end, seg = -1;
     if (warp < light_warps) {
@@ -338,10 +344,19 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_a
         const int64_t i = m * kWarp + lane;
         return i < ne ? __ldg(a.idx + beg + i) : srow;
     };
-    // SCALED: the windows' per-source scales, gathered one window ahead too
-    auto scales = [&](int32_t j) -> float { return (SCALED && j >= 0) ? __ldg(a.src_scale + j) : 0.f; };
+    // SCALED: the windows' per-source scales, gathered one window ahead too;
+    // WE: the windows' weight rows (edge ids through edge_w_perm)
+    auto scales = [&](int64_t m, int32_t j) -> float {
+        if constexpr (SCALED) return j >= 0 ? __ldg(a.src_scale + j) : 0.f;
+        if constexpr (WE) {
+            const int64_t i = m * kWarp + lane;
+            if (!a.edge_w_perm) return __int_as_float(static_cast<int>(i));
+            return __int_as_float(i < ne ? __ldg(a.edge_w_perm + beg + i) : 0);
+        }
+        return 0.f;
+    };
     int32_t wa = window(0), wb = n > kWarp ? window(1) : 0;
-    float sa = scales(wa), sb = n > kWarp ? scales(wb) : 0.f;
+    float sa = scales(0, wa), sb = n > kWarp ? scales(1, wb) : 0.f;
     int64_t ma = 0;
     // group g = rows 4g .. 4g+G-1 (G divides 32: a group never straddles a window)
     auto issue = [&](int64_t g) {
@@ -354,7 +369,7 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_a
                 ma = m;
                 if ((m + 1) * kWarp < n) {
                     wb = window(m + 1);
-                    sb = scales(wb);
+                    sb = scales(m + 1, wb);
                 }
             }
             const int slot0 = static_cast<int>(g % K) * G;
@@ -362,6 +377,7 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_a
             for (int u = 0; u < G; ++u) {
                 const int64_t p = p0 + u;
                 const int32_t j = __shfl_sync(0xffffffffu, wa, static_cast<int>(p & (kWarp - 1)));
+                const float sv = (SCALED || WE) ? __shfl_sync(0xffffffffu, sa, static_cast<int>(p & (kWarp - 1))) : 0.f;
                 if (p < n) {
                     const float* row = a.y + int64_t(j) * a.ldy;
 #pragma unroll
@@ -370,8 +386,14 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_a
                         if (q < w4) cp_async16(smem_u32(ring + ((slot0 + u) * NV + c) * kWarp + lane), row + 4 * q);
                     }
                     if constexpr (SCALED)   // after the row copies: the scale load may still be in flight
-                        wring[(slot0 + u) * kWarp + lane] =
-                            __shfl_sync(0xffffffffu, sa, static_cast<int>(p & (kWarp - 1)));
+                        wring[(slot0 + u) * kWarp + lane] = sv;
+                    if constexpr (WE) {
+                        const float* wrow = p < ne ? a.edge_w + (a.edge_w_perm ? int64_t(__float_as_int(sv)) : beg + p) * a.heads
+                                                   : a.self_w + int64_t(orow) * a.heads;
+#pragma unroll
+                        for (int c = 0; c < NV; ++c)
+                            cp_async4(smem_u32(wring + ((slot0 + u) * NV + c) * kWarp + lane), wrow + hd[c]);
+                    }
                 }
             }
         }
@@ -393,39 +415,42 @@ __global__ void __launch_bounds__(kAsyncWarps * 32) agg_async_kernel(const grd_a
             if (g * G + u >= n) break;
 #pragma unroll
             for (int c = 0; c < NV; ++c) {
-                const float w = SCALED ? wring[(slot0 + u) * kWarp + lane] : 1.f;
+                const float w = WE ? wring[((slot0 + u) * NV + c) * kWarp + lane]
+                                   : (SCALED ? wring[(slot0 + u) * kWarp + lane] : 1.f);
                 acc[c] = f4_fma(w, ring[((slot0 + u) * NV + c) * kWarp + lane], acc[c]);
             }
         }
     }
     cp_wait<0>();
     if (seg < 0) {
-        agg_finish<32, NV, false>(a, r, ne, lane, w4, hd, acc, /*add_self=*/false);
+        agg_finish<32, NV, WE>(a, r, ne, lane, w4, hd, acc, /*add_self=*/false);
         return;
     }
-    heavy_tail<32, NV, false>(a, seg, lane, lane, w4, ldp, hd, acc);
+    heavy_tail<32, NV, WE>(a, seg, lane, lane, w4, ldp, hd, acc);
 }
 
-template <int NV, int G, int K, bool SCALED>
+template <int NV, int G, int K, int MODE>
 int launch_async_t(const grd_agg_args& a, cudaStream_t st) {
     const int64_t warps = a.n_rows + a.n_segs;
     if (warps == 0) return 0;
-    const size_t smem = size_t(kAsyncWarps) * G * K * kWarp * (16 * NV + (SCALED ? 4 : 0));
+    const int wn = MODE == 2 ? NV : (MODE == 1 ? 1 : 0);
+    const size_t smem = size_t(kAsyncWarps) * G * K * kWarp * (16 * NV + 4 * wn);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(agg_async_kernel<NV, G, K, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(agg_async_kernel<NV, G, K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         attr = true;
     }
     const int64_t blocks = (warps + kAsyncWarps - 1) / kAsyncWarps;
-    agg_async_kernel<NV, G, K, SCALED><<<static_cast<unsigned>(blocks), kAsyncWarps * kWarp, smem, st>>>(a, a.n_rows);
+    agg_async_kernel<NV, G, K, MODE><<<static_cast<unsigned>(blocks), kAsyncWarps * kWarp, smem, st>>>(a, a.n_rows);
     return launch_status("agg_sum(staged)");
 }
 
 template <int NV, int G, int K>
 int launch_async(const grd_agg_args& a, cudaStream_t st) {
-    if (a.src_scale) return launch_async_t<NV, G, K, true>(a, st);
-    return launch_async_t<NV, G, K, false>(a, st);
+    if (a.edge_w) return launch_async_t<NV, G, K, 2>(a, st);
+    if (a.src_scale) return launch_async_t<NV, G, K, 1>(a, st);
+    return launch_async_t<NV, G, K, 0>(a, st);
 }
 
 template <int LPR, int NV, int U, bool WE>
@@ -829,6 +854,12 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     const char* mid_env = getenv("GRD_AGG_MID");
     const bool mid_override = mid_env && atoi(mid_env) > 0;
     if (async_on && !mid_override && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64)
+        return w4 <= 32 ? launch_async<1, 2, 2>(a, st) : launch_async<2, 2, 2>(a, st);
+    // GAT weighted rows: staged variant opt-in (GRD_AGG_ASYNC_WE=1; parity-
+    // green, but 157 vs 135 ms per products_gat epoch on B200: the NV 4-byte
+    // weight copies per row cost more than the staging hides)
+    const char* we_env = getenv("GRD_AGG_ASYNC_WE");
+    if (a.edge_w && we_env && atoi(we_env) > 0 && cc >= a.width && w4 > 16 && w4 <= 64)
         return w4 <= 32 ? launch_async<1, 2, 2>(a, st) : launch_async<2, 2, 2>(a, st);
     // rows in flight per warp: 8 for the 17..32-chunk rows (measured +15% at
     // width 100), 4 above
