@@ -274,6 +274,12 @@ typedef struct grd_gat_args {
                                       (grd_gat_pack_scores); null: p_ext's s / t columns.
                                       The backward reads s_u beside the P_u row it gathers. */
     int64_t ld_st;
+    int64_t n_small;               /* grd_gat_softmax, grd_gat_src_grad: the last n_small rows have at most
+                                      3 in-edges each (caller's guarantee, e.g. the
+                                      low-degree tail of a degree-sorted CSR; 0 = none):
+                                      4 lanes per row instead of a warp */
+    int64_t n_mid;                 /* the n_mid rows before those have at most 15
+                                      in-edges each: 16 lanes per row (0 = none) */
 } grd_gat_args;
 int grd_gat_softmax(const grd_gat_args* args, void* stream);
 int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream);

@@ -105,6 +105,8 @@ class GrdGatArgs(ctypes.Structure):
         ("ld_gext", c_i64),
         ("st", c_vp),
         ("ld_st", c_i64),
+        ("n_small", c_i64),
+        ("n_mid", c_i64),
     ]
 
 

@@ -184,8 +184,9 @@ template <int HM>
 __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
     const int lane = threadIdx.x & (kWarp - 1);
     const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const int64_t nl = a.n_rows - a.n_small - a.n_mid;   // rows of this kernel; segments follow
     Unit un;
-    if (!unit_of(a, w, un)) return;
+    if (!unit_of(a, w < nl ? w : a.n_rows + (w - nl), un)) return;
     const int H = a.heads;
     const int32_t v = vertex_of(a, un.row);
     const int64_t n = un.end - un.beg + (un.self ? 1 : 0);
@@ -221,6 +222,82 @@ __global__ void __launch_bounds__(256) gat_softmax_kernel(grd_gat_args a) {
 #pragma unroll
     for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
     write_alpha_e<HM>(a, un, v, lane, z, inv);
+}
+
+// The low-degree tail (the last n_small rows, <= 3 in-edges each: 66 % of
+// the rows of the products-shaped Kronecker graph, 40 % with none) at
+// kSmallLanes lanes per row, one item (edge or self loop) per lane: a warp
+// per such row left 28+ lanes idle and made the launch warp-count bound.
+// Rows longer than promised still come out right (items strided by
+// kSmallLanes, online (max, sum) merge, scores recomputed).
+constexpr int kSmallLanes = 4;
+constexpr int kMidLanes = 16;   // the n_mid rows before them (<= 15 in-edges)
+
+template <int HM>
+__device__ __forceinline__ void small_scores(const grd_gat_args& a, int64_t b, int64_t ne, int32_t v,
+                                             int64_t i, const float (&tv)[HM], float (&z)[HM]) {
+    const int32_t u = i < ne ? a.idx[b + i] : v;
+    float su[HM];
+    load_heads<HM>(a.st ? a.st + int64_t(u) * a.ld_st : a.p_ext + int64_t(u) * a.ld_ext + a.hdp, a.heads, su);
+#pragma unroll
+    for (int h = 0; h < HM; ++h) z[h] = h < a.heads ? lrelu(su[h] + tv[h], a.slope) : -INFINITY;
+}
+
+template <int HM, int L>
+__global__ void __launch_bounds__(256) gat_softmax_small_kernel(grd_gat_args a, int64_t r0, int64_t r1) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int sub = threadIdx.x & (L - 1);
+    const int64_t row = r0 + t / L;
+    const int H = a.heads;
+    int64_t b = 0, ne = -1;
+    int32_t v = 0;
+    float tv[HM];
+    if (row < r1) {
+        b = a.row_ptr[row];
+        ne = a.row_ptr[row + 1] - b;
+        v = vertex_of(a, row);
+        load_heads<HM>(a.st ? a.st + int64_t(v) * a.ld_st + H : a.p_ext + int64_t(v) * a.ld_ext + a.hdp + H, H, tv);
+    }
+    float z0[HM], mx[HM], sm[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        z0[h] = -INFINITY;
+        mx[h] = -INFINITY;
+        sm[h] = 0.f;
+    }
+    for (int64_t i = sub; i <= ne; i += L) {   // items 0..ne-1 edges, ne the self loop
+        float z[HM];
+        small_scores<HM>(a, b, ne, v, i, tv, z);
+#pragma unroll
+        for (int h = 0; h < HM; ++h) {
+            if (i == sub) z0[h] = z[h];
+            lse_merge(mx[h], sm[h], z[h], 1.f);
+        }
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int h = 0; h < HM; ++h) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, mx[h], o);
+            const float d2 = __shfl_xor_sync(0xffffffffu, sm[h], o);
+            lse_merge(mx[h], sm[h], m2, d2);
+        }
+    float inv[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
+    for (int64_t i = sub; i <= ne; i += L) {
+        float z[HM];
+        if (i == sub) {
+#pragma unroll
+            for (int h = 0; h < HM; ++h) z[h] = z0[h];
+        } else {
+            small_scores<HM>(a, b, ne, v, i, tv, z);
+        }
+        float* dst = i < ne ? a.alpha + (b + i) * H : a.alpha_self + int64_t(v) * H;
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H) dst[h] = __expf(z[h] - mx[h]) * inv[h];
+    }
 }
 
 // Pass 2, one warp per heavy segment: merge the row's segment partials in a
@@ -385,35 +462,60 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
 }
 
 // Source score gradient ds_u,h = sum over u's out-edges of delta (edges
-// addressed through the transposed CSR's permutation) + the self loop; one
-// warp per unit of the out-edge CSR.
-__global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
-    Unit un;
-    if (!unit_of(a, w, un)) return;
+// addressed through the transposed CSR's permutation) + the self loop.
+// L lanes per unit of the out-edge CSR: a warp (L = 32) for rows [r0, r1)
+// and then every heavy segment, 16 / 4 lanes for the low-degree rows
+// (AggSpec.n_mid / n_small, the same split as the edge softmax).
+template <int L, int HM>
+__global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a, int64_t r0, int64_t r1) {
+    const int sub = threadIdx.x & (L - 1);
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+    Unit un{0, 0, 0, -1, false};
+    bool ok;
+    if (w < r1 - r0)
+        ok = unit_of(a, r0 + w, un);
+    else
+        ok = L == kWarp && unit_of(a, a.n_rows + (w - (r1 - r0)), un);
+    if (L == kWarp && !ok) return;   // warp-uniform
     const int H = a.heads;
-    float ds[kMaxHeads];
+    float ds[HM];
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) ds[h] = 0.f;
-    for (int64_t i = un.beg + lane; i < un.end; i += kWarp) {
-        const float* de = a.delta + int64_t(a.edge_perm[i]) * H;
+    for (int h = 0; h < HM; ++h) ds[h] = 0.f;
+    if (ok)
+        for (int64_t i = un.beg + sub; i < un.end; i += L) {
+            const float* de = a.delta + int64_t(a.edge_perm[i]) * H;
 #pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) ds[h] += de[h];
-    }
+            for (int h = 0; h < HM; ++h)
+                if (h < H) ds[h] += de[h];
+        }
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) ds[h] = warp_sum(ds[h]);
+    for (int h = 0; h < HM; ++h)
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) ds[h] += __shfl_xor_sync(0xffffffffu, ds[h], o);
+    if (!ok) return;
     const int32_t r = vertex_of(a, un.row);
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) {
-        if (h >= H || lane != h) continue;
+    for (int h = 0; h < HM; ++h) {
+        if (h >= H || (h % L) != sub) continue;
         const float t = ds[h] + (un.self ? a.delta_self[int64_t(r) * H + h] : 0.f);
         if (un.seg < 0)
             a.grad_ext[int64_t(r) * a.ld_gext + a.hdp + h] = t;
         else
             a.seg_scratch[un.seg * H + h] = t;
     }
+}
+
+template <int HM>
+void launch_src_grad(const grd_gat_args& a, cudaStream_t st) {
+    const int64_t r_small = a.n_rows - a.n_small, r_mid = r_small - a.n_mid;
+    const int64_t units = r_mid + a.n_segs;
+    if (units > 0) gat_src_grad_kernel<kWarp, HM><<<static_cast<unsigned>((units * kWarp + 255) / 256), 256, 0, st>>>(a, 0, r_mid);
+    if (a.n_mid > 0)
+        gat_src_grad_kernel<kMidLanes, HM><<<static_cast<unsigned>((a.n_mid * kMidLanes + 255) / 256), 256, 0, st>>>(
+            a, r_mid, r_small);
+    if (a.n_small > 0)
+        gat_src_grad_kernel<kSmallLanes, HM>
+            <<<static_cast<unsigned>((a.n_small * kSmallLanes + 255) / 256), 256, 0, st>>>(a, r_small, a.n_rows);
 }
 
 // Heavy rows of the two backward passes: one warp per heavy row sums its
@@ -537,14 +639,44 @@ extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
     if (args->n_rows == 0) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int H = args->heads;
-    if (H == 1)
-        gat_softmax_kernel<1><<<unit_blocks(*args), 256, 0, st>>>(*args);
-    else if (H == 2)
-        gat_softmax_kernel<2><<<unit_blocks(*args), 256, 0, st>>>(*args);
-    else if (H <= 4)
-        gat_softmax_kernel<4><<<unit_blocks(*args), 256, 0, st>>>(*args);
-    else
-        gat_softmax_kernel<8><<<unit_blocks(*args), 256, 0, st>>>(*args);
+    if (args->n_small < 0 || args->n_mid < 0 || args->n_small + args->n_mid > args->n_rows)
+        return fail(kErrArg, "gat_softmax: n_small %lld + n_mid %lld outside [0, n_rows]",
+                    (long long)args->n_small, (long long)args->n_mid);
+    const int64_t r_mid = args->n_rows - args->n_small - args->n_mid, r_small = args->n_rows - args->n_small;
+    const unsigned nb = warps_blocks(r_mid + args->n_segs);
+    if (nb > 0) {
+        if (H == 1)
+            gat_softmax_kernel<1><<<nb, 256, 0, st>>>(*args);
+        else if (H == 2)
+            gat_softmax_kernel<2><<<nb, 256, 0, st>>>(*args);
+        else if (H <= 4)
+            gat_softmax_kernel<4><<<nb, 256, 0, st>>>(*args);
+        else
+            gat_softmax_kernel<8><<<nb, 256, 0, st>>>(*args);
+    }
+    if (args->n_mid > 0) {
+        const unsigned sb = static_cast<unsigned>((args->n_mid * kMidLanes + 255) / 256);
+        if (H == 1)
+            gat_softmax_small_kernel<1, kMidLanes><<<sb, 256, 0, st>>>(*args, r_mid, r_small);
+        else if (H == 2)
+            gat_softmax_small_kernel<2, kMidLanes><<<sb, 256, 0, st>>>(*args, r_mid, r_small);
+        else if (H <= 4)
+            gat_softmax_small_kernel<4, kMidLanes><<<sb, 256, 0, st>>>(*args, r_mid, r_small);
+        else
+            gat_softmax_small_kernel<8, kMidLanes><<<sb, 256, 0, st>>>(*args, r_mid, r_small);
+    }
+    if (args->n_small > 0) {
+        const unsigned sb = static_cast<unsigned>((args->n_small * kSmallLanes + 255) / 256);
+        const int64_t r1 = args->n_rows;
+        if (H == 1)
+            gat_softmax_small_kernel<1, kSmallLanes><<<sb, 256, 0, st>>>(*args, r_small, r1);
+        else if (H == 2)
+            gat_softmax_small_kernel<2, kSmallLanes><<<sb, 256, 0, st>>>(*args, r_small, r1);
+        else if (H <= 4)
+            gat_softmax_small_kernel<4, kSmallLanes><<<sb, 256, 0, st>>>(*args, r_small, r1);
+        else
+            gat_softmax_small_kernel<8, kSmallLanes><<<sb, 256, 0, st>>>(*args, r_small, r1);
+    }
     int rc = launch_status("gat_softmax");
     if (rc || args->n_segs == 0) return rc;
     if (H == 1)
@@ -583,7 +715,17 @@ extern "C" int grd_gat_src_grad(const grd_gat_args* args, void* stream) {
     if (args->n_rows == 0) return 0;
     if (!args->edge_perm) return fail(kErrArg, "gat_src_grad: needs edge_perm");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    gat_src_grad_kernel<<<unit_blocks(*args), 256, 0, st>>>(*args);
+    if (args->n_small < 0 || args->n_mid < 0 || args->n_small + args->n_mid > args->n_rows)
+        return fail(kErrArg, "gat_src_grad: bad n_small / n_mid");
+    const int H = args->heads;
+    if (H == 1)
+        launch_src_grad<1>(*args, st);
+    else if (H == 2)
+        launch_src_grad<2>(*args, st);
+    else if (H <= 4)
+        launch_src_grad<4>(*args, st);
+    else
+        launch_src_grad<8>(*args, st);
     int rc = launch_status("gat_src_grad");
     if (rc || args->n_heavy == 0) return rc;
     gat_heavy_sum_kernel<<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args, args->hdp);

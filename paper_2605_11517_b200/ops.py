@@ -76,6 +76,17 @@ def _ld(t: torch.Tensor) -> int:
     return int(t.stride(0))
 
 
+SMALL_EDGES = 3   # grd_gat_args.n_small: rows the GAT softmax runs at 4 lanes per row
+MID_EDGES = 15    # grd_gat_args.n_mid: at 16 lanes per row
+
+
+def _small_tail(deg: np.ndarray, limit: int) -> int:
+    """Length of the trailing run of rows with <= limit edges (the
+    low-degree tail of the degree-sorted device CSRs)."""
+    big = np.flatnonzero(deg > limit)
+    return int(deg.size - (big[-1] + 1 if big.size else 0))
+
+
 @dataclass
 class AggSpec:
     """A static CSR over which rows are sum-aggregated, uploaded once, with
@@ -94,6 +105,8 @@ class AggSpec:
     n_segs: int
     nnz: int
     _partial: torch.Tensor | None = None
+    n_small: int = 0                 # trailing rows with <= SMALL_EDGES edges
+    n_mid: int = 0                   # rows before them with <= MID_EDGES edges
 
     @classmethod
     def build(cls, row_ptr: np.ndarray, idx: np.ndarray, device, out_idx=None, self_idx=None,
@@ -122,6 +135,8 @@ class AggSpec:
             heavy_counter=torch.zeros(16 * max(heavy.size, 1), dtype=torch.int32, device=device)
             if has_heavy else None,
             n_heavy=int(heavy.size), n_segs=int(seg_heavy.size), nnz=int(row_ptr[-1]),
+            n_small=_small_tail(deg, SMALL_EDGES),
+            n_mid=_small_tail(deg, MID_EDGES) - _small_tail(deg, SMALL_EDGES),
         )
 
     def partial(self, width: int) -> torch.Tensor | None:
@@ -326,6 +341,8 @@ def _gat_args(spec: AggSpec, p_ext, heads, dhp, **kw):
     a.seg_heavy = _p(spec.seg_heavy)
     a.n_segs = spec.n_segs
     a.seg_scratch = _p(spec.partial(2 * int(heads)))
+    a.n_small = spec.n_small
+    a.n_mid = spec.n_mid
     for k, v in kw.items():
         if k.startswith("ld_"):
             setattr(a, k, int(v))

@@ -315,3 +315,91 @@ def test_gemm_split_output(m, n2, k):
     full = np.maximum(a @ b, 0)
     assert rel_l2(_host(c1, n2), full[:, :n2]) < 5e-6
     assert rel_l2(_host(c2, n2), full[:, n2:]) < 5e-6
+
+
+@pytest.mark.parametrize("heads", [1, 2, 4, 8])
+def test_gat_softmax_small_tail(heads):
+    """The low-degree tail at 4 lanes per row (AggSpec.n_small) gives the
+    same attention as the warp-per-row kernel, also when forced onto rows
+    longer than it is meant for (hub rows included)."""
+    from paper_2605_11517_b200 import generate_kronecker, build_partition_plan, random_partition
+    from paper_2605_11517_b200.engine import DeviceGraph
+    g = generate_kronecker(12, 16, seed=5)
+    n = g.num_vertices
+    dg = DeviceGraph(g, build_partition_plan(g, random_partition(n, 2, 1), 2), DEV)
+    spec = dg.fwd
+    assert 0 < spec.n_small < spec.n_rows
+    dhp = 4
+    hdp = heads * dhp
+    rng = np.random.default_rng(heads)
+    pe = _dev(rng.normal(size=(n, hdp + 2 * heads)))
+    E = spec.nnz
+    out = {}
+    default = (spec.n_small, spec.n_mid)
+    assert spec.n_mid > 0
+    cases = {"warp": (0, 0), "default": default, "small_all": (spec.n_rows, 0),
+             "mid_all": (0, spec.n_rows), "split": (spec.n_rows // 2, spec.n_rows - spec.n_rows // 2)}
+    for name, (ks, km) in cases.items():
+        spec.n_small, spec.n_mid = ks, km
+        alpha = torch.zeros(E * heads, device=DEV)
+        alpha_self = torch.zeros(n * heads, device=DEV)
+        ops.gat_softmax(spec, pe, heads, dhp, alpha, alpha_self)
+        out[name] = (alpha.cpu(), alpha_self.cpu())
+    spec.n_small, spec.n_mid = default
+    for name in cases:
+        assert torch.allclose(out[name][0], out["warp"][0], rtol=1e-5, atol=1e-7), name
+        assert torch.allclose(out[name][1], out["warp"][1], rtol=1e-5, atol=1e-7), name
+    # every row's attention sums to one
+    s = out["small_all"][1].view(n, heads).double()
+    ptr = spec.row_ptr.cpu().numpy()
+    oi = spec.out_idx.cpu().numpy() if spec.out_idx is not None else np.arange(n)
+    a = out["small_all"][0].view(E, heads).double().numpy()
+    rs = np.add.reduceat(np.vstack([a, np.zeros((1, heads))]), ptr[:-1], axis=0)[:n]
+    rs[ptr[1:] == ptr[:-1]] = 0.0
+    tot = s.numpy()[oi] + rs
+    assert np.allclose(tot, 1.0, atol=1e-5)
+
+
+@pytest.mark.parametrize("heads", [1, 4, 8])
+def test_gat_src_grad_lane_groups(heads):
+    """ds_u from the lane-grouped low-degree rows equals the warp-per-row
+    sums (any split of the rows between the tiers) and a float64 reference."""
+    from paper_2605_11517_b200 import generate_kronecker, build_partition_plan, random_partition
+    from paper_2605_11517_b200.engine import DeviceGraph
+    g = generate_kronecker(12, 16, seed=7)
+    n = g.num_vertices
+    dg = DeviceGraph(g, build_partition_plan(g, random_partition(n, 2, 1), 2), DEV)
+    spec = dg.bwd
+    assert spec.n_small > 0 and spec.n_mid > 0
+    dhp = 4
+    hdp = heads * dhp
+    E = spec.nnz
+    rng = np.random.default_rng(heads)
+    delta = rng.normal(size=(E, heads))
+    dself = rng.normal(size=(n, heads))
+    d_t = torch.from_numpy(delta).float().reshape(-1).to(DEV)
+    ds_t = torch.from_numpy(dself).float().reshape(-1).to(DEV)
+    perm = dg.out_to_in_perm()
+    default = (spec.n_small, spec.n_mid)
+    cases = {"warp": (0, 0), "default": default, "small_all": (spec.n_rows, 0),
+             "mid_all": (0, spec.n_rows)}
+    res = {}
+    for name, (ks, km) in cases.items():
+        spec.n_small, spec.n_mid = ks, km
+        gext = ops.zeros_rows(n, hdp + 2 * heads, DEV)
+        ops.gat_src_grad(spec, heads, dhp, perm, d_t, ds_t, gext)
+        res[name] = gext[:, hdp:hdp + heads].cpu().double().numpy()
+    spec.n_small, spec.n_mid = default
+    # float64 reference: ds_u = sum over out-edges of delta + self
+    # float64 host sums over the transposed CSR (perm: its edges -> delta rows)
+    ptr = spec.row_ptr.cpu().numpy()
+    pm = perm.cpu().numpy()[:E].astype(np.int64)
+    rows = np.repeat(np.arange(spec.n_rows), np.diff(ptr))
+    per_row = np.zeros((spec.n_rows, heads))
+    np.add.at(per_row, rows, delta[pm])
+    oi = spec.out_idx.cpu().numpy() if spec.out_idx is not None else np.arange(n)
+    ref = dself.copy()
+    ref[oi] += per_row
+    for name in cases:
+        assert np.allclose(res[name], res["warp"], rtol=1e-5, atol=1e-5), name
+        assert np.allclose(res[name], ref, rtol=1e-4, atol=1e-4), name
