@@ -18,8 +18,10 @@ dev = "cuda"
 in_deg = np.diff(f.in_ptr)          # per perm row
 deg_v = np.empty(n, np.int64)
 deg_v[f.perm] = in_deg
-y = torch.randn(n, 256, device=dev)
-out = torch.zeros(n, 256, device=dev)
+import os  # noqa: E402
+W = int(os.environ.get("AGG_ORDER_WIDTH", "256"))
+y = torch.randn(n, W, device=dev)
+out = torch.zeros(n, W, device=dev)
 flush = torch.zeros(128 * 1024 * 1024, device=dev)
 
 
@@ -37,7 +39,7 @@ def spec_for(order):
     rep = np.repeat(starts - ptr[:-1], cnt)
     idx = f.in_src[np.arange(ptr[-1]) + rep]
     sp = AggSpec.build(ptr, idx, dev, out_idx=order.astype(np.int32))
-    sp.partial(256)
+    sp.partial(W)
     return sp
 
 
@@ -47,7 +49,7 @@ def timeit(sp, reps=10):
         flush.add_(1.0)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        ops.agg_sum(sp, y, out, 256, post_div_deg=2, no_self=True, relu=True)
+        ops.agg_sum(sp, y, out, W, post_div_deg=2, no_self=True, relu=True)
         e.record()
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
@@ -62,7 +64,8 @@ orders = {"plan (partition) order": f.perm.astype(np.int64), "vertex order": np.
           "random order": rng.permutation(n), "descending degree": np.argsort(-deg_v, kind="stable"),
           "ascending degree": np.argsort(deg_v, kind="stable"),
           "log2-degree buckets desc, plan order inside": np.lexsort((rank, -lg)),
-          "log2-degree buckets desc, vertex order inside": np.lexsort((np.arange(n), -lg))}
+          "log2-degree buckets desc, vertex order inside": np.lexsort((np.arange(n), -lg)),
+          "partition-major, descending degree inside": np.lexsort((-deg_v, plan.labels if hasattr(plan, "labels") else rank * 8 // n))}
 ref = None
 for name, order in orders.items():
     sp = spec_for(order)
