@@ -483,18 +483,21 @@ int agg_chunk_cols(int width) {
 }
 
 // ------------------------------------------------------------ K1 / K9 --
-template <bool kAdd>
+// LPR lanes per row (rows of w4 <= LPR chunks: a narrow row, e.g. GAT's
+// 16-byte per-edge attention rows, no longer idles 31 lanes of a warp)
+template <bool kAdd, int LPR>
 __global__ void __launch_bounds__(256) row_copy_kernel(const float* __restrict__ src, int64_t lds,
                                                        const int32_t* __restrict__ idx, int64_t n_rows,
                                                        int w4, float* __restrict__ dst, int64_t ldd) {
-    const int lane = threadIdx.x & (kWarp - 1);
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int sub = static_cast<int>(t & (LPR - 1));
+    const int64_t r = t / LPR;
     if (r >= n_rows) return;
     const int32_t j = idx[r];
     if (kAdd) {
         const float* s = src + r * lds;
         float* d = dst + int64_t(j) * ldd;
-        for (int q = lane; q < w4; q += kWarp) {
+        for (int q = sub; q < w4; q += LPR) {
             float4 v = *reinterpret_cast<float4*>(d + 4 * q);
             v = f4_add(v, ld_nc_f4(s + 4 * q));
             *reinterpret_cast<float4*>(d + 4 * q) = v;
@@ -502,9 +505,23 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const float* __restrict__
     } else {
         const float* s = src + int64_t(j) * lds;
         float* d = dst + r * ldd;
-        for (int q = lane; q < w4; q += kWarp)
+        for (int q = sub; q < w4; q += LPR)
             *reinterpret_cast<float4*>(d + 4 * q) = ld_nc_f4(s + 4 * q);
     }
+}
+
+template <bool kAdd>
+void launch_row_copy(const float* src, int64_t lds, const int32_t* idx, int64_t n_rows, int w4, float* dst,
+                     int64_t ldd, cudaStream_t st) {
+#define GRD_ROW_COPY(L)                                                                              \
+    row_copy_kernel<kAdd, L><<<static_cast<unsigned>((n_rows * L + 255) / 256), 256, 0, st>>>(src, lds, idx, n_rows, w4, dst, ldd)
+    if (w4 <= 1) GRD_ROW_COPY(1);
+    else if (w4 <= 2) GRD_ROW_COPY(2);
+    else if (w4 <= 4) GRD_ROW_COPY(4);
+    else if (w4 <= 8) GRD_ROW_COPY(8);
+    else if (w4 <= 16) GRD_ROW_COPY(16);
+    else GRD_ROW_COPY(32);
+#undef GRD_ROW_COPY
 }
 
 // ----------------------------------------------------------- K6 reduce --
@@ -809,8 +826,7 @@ extern "C" int grd_gather_rows(const float* src, int64_t ld_src, const int32_t* 
     if (n_rows == 0) return 0;
     if (!src || !idx || !dst || width <= 0 || ld_src % 4 || ld_dst % 4)
         return fail(kErrArg, "gather_rows: bad arguments");
-    row_copy_kernel<false><<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst);
+    launch_row_copy<false>(src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst, static_cast<cudaStream_t>(stream));
     return launch_status("gather_rows");
 }
 
@@ -820,8 +836,7 @@ extern "C" int grd_scatter_add_rows(const float* src, int64_t ld_src, const int3
     if (n_rows == 0) return 0;
     if (!src || !idx || !dst || width <= 0 || ld_src % 4 || ld_dst % 4)
         return fail(kErrArg, "scatter_add_rows: bad arguments");
-    row_copy_kernel<true><<<blocks_for(n_rows * kWarp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst);
+    launch_row_copy<true>(src, ld_src, idx, n_rows, (width + 3) / 4, dst, ld_dst, static_cast<cudaStream_t>(stream));
     return launch_status("scatter_add_rows");
 }
 

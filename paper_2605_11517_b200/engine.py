@@ -705,6 +705,14 @@ class LayerwiseEngine(_EngineBase):
         self.alpha_self = torch.zeros(self.NL * H, dtype=torch.float32, device=dev)
         self.delta_self = torch.zeros_like(self.alpha_self)
         self.pull, self.edge_perm = dg.gat_pull()
+        # the transposed pull reads alpha in its own edge order: one permuting
+        # row gather per layer (16-byte rows at 4 heads) instead of a
+        # dependent edge_perm load per edge inside the pull (GRD_GAT_ALPHA_T=0
+        # keeps the permuted addressing)
+        import os
+        self.alpha_t = None
+        if H % 4 == 0 and self.pull.nnz > 0 and E > 0 and os.environ.get("GRD_GAT_ALPHA_T", "1") != "0":
+            self.alpha_t = torch.zeros(self.pull.nnz * H, dtype=torch.float32, device=dev)
         # compact [s | t] score table (32 B per vertex at 4 heads): the
         # edge-softmax's per-edge score gathers stay in L2
         self.st = ops.zeros_rows(self.NL, 2 * H, dev)
@@ -755,8 +763,15 @@ class LayerwiseEngine(_EngineBase):
             go[self.V:].zero_()    # halo rows: no self term, no stale gradient
         # dP_u = sum_v alpha_uv gO_v and ds_u = sum_v delta_uv over u's out-edges
         # (sharded: owned targets only; halo rows are partials for their owners)
-        ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha,
-                    edge_w_perm=self.edge_perm, self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+        if self.alpha_t is not None:
+            ne = self.pull.nnz
+            ops.gather_rows(self.alpha.view(-1, c.heads), self.edge_perm[:ne],
+                            self.alpha_t.view(ne, c.heads), c.heads)
+            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha_t,
+                        self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+        else:
+            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha,
+                        edge_w_perm=self.edge_perm, self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
         ops.gat_src_grad(self.pull, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
         dg.reverse_add(gext, c.hdp + c.heads)
         ops.wgrad_sgd(x, gext, wt.dwext[l], c.d_in, c.n_ext, self.V)
