@@ -30,6 +30,8 @@ Two execution paths share the same kernels (ops.py -> libgrinder_b200.so):
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -709,7 +711,6 @@ class LayerwiseEngine(_EngineBase):
         # row gather per layer (16-byte rows at 4 heads) instead of a
         # dependent edge_perm load per edge inside the pull (GRD_GAT_ALPHA_T=0
         # keeps the permuted addressing)
-        import os
         self.alpha_t = None
         if H % 4 == 0 and self.pull.nnz > 0 and E > 0 and os.environ.get("GRD_GAT_ALPHA_T", "1") != "0":
             self.alpha_t = torch.zeros(self.pull.nnz * H, dtype=torch.float32, device=dev)
@@ -721,26 +722,50 @@ class LayerwiseEngine(_EngineBase):
         hdp = self.cfg[-1].hdp
         self.t2 = ops.zeros_rows(self.NL, hdp, dev)
         self.t3 = ops.zeros_rows(self.NL, hdp, dev)
+        # Hidden layers' [P | s | t] and attention kept from the forward when
+        # they fit (a few GB at the products shape): the backward then skips
+        # the regather (transform GEMM + edge softmax).  The last layer's are
+        # still in t1 / alpha when its backward runs.  GRD_GAT_KEEP=0, or too
+        # little free HBM, recomputes them as the reference's regather does.
+        self.gat_kept = {}
+        self.gat_keep_on = os.environ.get("GRD_GAT_KEEP", "1") != "0"
+        if self.gat_keep_on and str(dev).startswith("cuda"):
+            hidden = [l for l, c in enumerate(self.cfg) if c.gat and not c.last]
+            need = sum(self.NL * ops.ld_of(self.cfg[l].ld_ext) * 4 + (max(E, 1) + self.NL) * H * 4
+                       for l in hidden)
+            free = torch.cuda.mem_get_info(torch.device(dev))[0]
+            if need + (4 << 30) < free:
+                for l in hidden:
+                    self.gat_kept[l] = (ops.zeros_rows(self.NL, self.cfg[l].ld_ext, dev),
+                                        torch.zeros_like(self.alpha), torch.zeros_like(self.alpha_self))
 
-    def _gat_transform(self, l: int, x: torch.Tensor) -> torch.Tensor:
+    def _gat_bufs(self, l: int):
+        """(P_ext, alpha, alpha_self) buffers of layer l: kept per layer, or
+        the shared ones (t1 / alpha) that the backward recomputes."""
+        kept = self.gat_kept.get(l)
+        if kept is not None:
+            return kept[0][:, : self.cfg[l].ld_ext], kept[1], kept[2]
+        return self.t1[:, : self.cfg[l].ld_ext], self.alpha, self.alpha_self
+
+    def _gat_transform(self, l: int, x: torch.Tensor):
         """P_ext = X [W | W a_src | W a_dst] and the attention (forward, and
-        recomputed in backward: the regather)."""
+        recomputed in backward when not kept: the regather)."""
         c, dg = self.cfg[l], self.dg
         wt = self.wts
         d_in, dh, dhp = wt.shape[l]
+        pext, alpha, alpha_self = self._gat_bufs(l)
         ops.gat_build_wext(wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.wext[l])
-        pext = self.t1[:, : c.ld_ext]
         ops.gemm(x, wt.wext[l], pext, self.V, c.n_ext, c.d_in)
         dg.exchange(pext, c.n_ext)                # halo rows of [P | s | t]
         ops.gat_pack_scores(pext, self.NL, c.heads, c.dhp, self.st)
-        ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, st=self.st)
-        return pext
+        ops.gat_softmax(dg.fwd, pext, c.heads, c.dhp, alpha, alpha_self, st=self.st)
+        return pext, alpha, alpha_self
 
     def _forward_gat(self, l: int, x: torch.Tensor, out: torch.Tensor) -> None:
         c, dg = self.cfg[l], self.dg
-        pext = self._gat_transform(l, x)
+        pext, alpha, alpha_self = self._gat_transform(l, x)
         dst = self.t2[:, : c.hdp] if c.last else out
-        ops.agg_sum(dg.fwd, pext[:, : c.hdp], dst, c.hdp, edge_w=self.alpha, self_w=self.alpha_self,
+        ops.agg_sum(dg.fwd, pext[:, : c.hdp], dst, c.hdp, edge_w=alpha, self_w=alpha_self,
                     heads=c.heads, head_ld=c.dhp, relu=not c.last)
         if c.last:
             ops.head_mean(dst, self.V, c.heads, c.dh, c.dhp, out)
@@ -755,9 +780,14 @@ class LayerwiseEngine(_EngineBase):
         else:
             # ReLU mask applied by the producer, so gO.relu(O) = gO.O
             go, o_fwd = self.g[:, : c.hdp], self.acts[l + 1]
-        pext = self._gat_transform(l, x)
+        if l in self.gat_kept or (c.last and self.gat_keep_on):
+            # kept from the forward (the last layer's still sit in t1 / alpha,
+            # and wext[l] is the forward's)
+            pext, alpha, alpha_self = self._gat_bufs(l)
+        else:
+            pext, alpha, alpha_self = self._gat_transform(l, x)
         gext = self.h[:, : c.ld_ext]
-        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, self.alpha, self.alpha_self, go, o_fwd,
+        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, alpha, alpha_self, go, o_fwd,
                             self.delta, self.delta_self, gext)   # s_u beside the gathered P_u row
         if self.NL > self.V:
             go[self.V:].zero_()    # halo rows: no self term, no stale gradient
@@ -765,13 +795,13 @@ class LayerwiseEngine(_EngineBase):
         # (sharded: owned targets only; halo rows are partials for their owners)
         if self.alpha_t is not None:
             ne = self.pull.nnz
-            ops.gather_rows(self.alpha.view(-1, c.heads), self.edge_perm[:ne],
+            ops.gather_rows(alpha.view(-1, c.heads), self.edge_perm[:ne],
                             self.alpha_t.view(ne, c.heads), c.heads)
             ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha_t,
-                        self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+                        self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
         else:
-            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha,
-                        edge_w_perm=self.edge_perm, self_w=self.alpha_self, heads=c.heads, head_ld=c.dhp)
+            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=alpha,
+                        edge_w_perm=self.edge_perm, self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
         ops.gat_src_grad(self.pull, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
         dg.reverse_add(gext, c.hdp + c.heads)
         ops.wgrad_sgd(x, gext, wt.dwext[l], c.d_in, c.n_ext, self.V)

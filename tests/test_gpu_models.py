@@ -110,3 +110,24 @@ def test_gat_hub_rows():
     assert abs(tr[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
     for a, b in zip(one.weight_grads, grads):
         assert rel_l2(a, b) < TOL
+
+
+@pytest.mark.parametrize("keep", ["0", "1"])
+def test_gat_kept_vs_regathered(keep, monkeypatch):
+    """Hidden GAT layers' [P | s | t] and attention kept from the forward
+    (default) or recomputed in the backward (GRD_GAT_KEEP=0, the regather):
+    both match the float64 oracle."""
+    monkeypatch.setenv("GRD_GAT_KEEP", keep)
+    g = g2.generate_kronecker(11, 12, seed=8)
+    ds = g2.make_random_dataset(g, feature_dim=12, num_classes=5, seed=9)
+    plan = g2.build_partition_plan(g, g2.random_partition(g.num_vertices, 3, 5), 3)
+    model = g2.create_model(12, 5, num_layers=3, hidden_dim=16, seed=10, aggregation_mode="gat", heads=4)
+    one, tr, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    sess = g2.training.session_for(ds, plan, model) if hasattr(g2, "training") else None
+    if sess is not None:
+        assert bool(sess.engine.gat_kept) == (keep == "1")
+    _, grads, ref = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                       model.weights, 4, 1, 0.05)
+    assert abs(tr[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
+    for a, b in zip(one.weight_grads, grads):
+        assert rel_l2(a, b) < TOL
