@@ -677,9 +677,9 @@ class LayerwiseEngine(_EngineBase):
                 ops.gemm(gcat, W, self.h, self.V, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=ref)
             ops.wgrad_sgd(x, gcat, dW, c.d_in, 2 * c.ld_out, self.V, w=self._w(W), lr=lr)
         elif l == 0 and self.xn is not None:
+            # N = mean_in(X) is still beside X in the features buffer (nothing
+            # else writes those columns): no regather
             gp = self.g[:, : c.ld_out]
-            ops.agg_sum(dg.fwd, x, self.xn[:, c.ld_in: 2 * c.ld_in], c.d_in, post_div_deg=2,
-                        no_self=True)                                           # regather
             ops.wgrad_sgd(self.xn, gp, dW, 2 * c.ld_in, c.d_out, self.V, w=self._w(W), lr=lr)
         else:
             gp = self.g[:, : c.ld_out]
