@@ -587,6 +587,17 @@ class LayerwiseEngine(_EngineBase):
             wide = max([self.maxw] + [c.ld_ext for c in self.cfg])
             self._gat_buffers(dg, model)
         self.t1 = ops.zeros_rows(self.NL, wide, dev)
+        # aggregate-first GCN layers: the forward's normalised aggregate N is
+        # kept for the backward's dW = N^T gp when it fits, instead of the
+        # reference's regather (GRD_KEEP_AGG=0 regathers)
+        self.keep_on = os.environ.get("GRD_KEEP_AGG", "1") != "0"
+        self.n_kept = {}
+        if self.keep_on and str(dev).startswith("cuda"):
+            hidden = [l for l, c in enumerate(self.cfg)
+                      if not (c.transform_first or c.sage or c.gat or c.rownorm or c.last)]
+            need = sum(self.NL * ld_of(self.cfg[l].d_in) * 4 for l in hidden)
+            if hidden and need + (4 << 30) < torch.cuda.mem_get_info(torch.device(dev))[0]:
+                self.n_kept = {l: ops.zeros_rows(self.NL, self.cfg[l].d_in, dev) for l in hidden}
         self.g = ops.zeros_rows(self.NL, wide, dev)
         self.h = ops.zeros_rows(self.NL, wide, dev)
         if model.kind == "sage":
@@ -613,8 +624,9 @@ class LayerwiseEngine(_EngineBase):
             # halo rows of P = X W, overlapped with the interior rows
             dg.exchange_agg("fwd", self.t1, out, c.d_out, post_div_deg=not c.sym, post_scale=s, relu=relu)
         else:
-            self._input_agg(l, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
-            ops.gemm(self.t1, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
+            n = self.n_kept.get(l, self.t1)
+            self._input_agg(l, x, n, c.d_in, src_scale=s, post_div_deg=not c.sym, post_scale=s)
+            ops.gemm(n, W, out, self.V, c.d_out, c.d_in, relu_out=relu)
 
     def _input_agg(self, l: int, x: torch.Tensor, out: torch.Tensor, width: int, **kw) -> None:
         """Aggregate-first layers read the layer input's halo rows (the
@@ -883,12 +895,16 @@ class LayerwiseEngine(_EngineBase):
                              row_scale=prev[1], elem_mul=dmask, relu_ref=prev[0])
                 ops.wgrad_sgd(x, self.h, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
             else:
-                if not have_n:   # regather: recompute the normalised aggregate
-                    ops.agg_sum(dg.fwd, x, self.t1, c.d_in, src_scale=s, post_div_deg=not c.sym,
+                n = self.n_kept.get(l, self.t1)
+                # the forward's aggregate is kept (hidden layers, when it fits)
+                # or still in t1 (the last layer: only the loss ran since)
+                kept = l in self.n_kept or (c.last and self.keep_on)
+                if not have_n and not kept:   # regather: recompute the normalised aggregate
+                    ops.agg_sum(dg.fwd, x, n, c.d_in, src_scale=s, post_div_deg=not c.sym,
                                 post_scale=s)
                 ops.gemm(self.g, W, self.h, self.V, c.d_in, c.d_out, trans_b=True,
                          row_scale=dg.scale(c.pre_scale))
-                ops.wgrad_sgd(self.t1, self.g, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
+                ops.wgrad_sgd(n, self.g, dW, c.d_in, c.d_out, self.V, w=self._w(W), lr=lr)
                 if l > 0:
                     post = self._combine(s is not None, prev[1])
                     dg.exchange_agg("bwd", self.h, self.g, c.d_in, post_scale=post,

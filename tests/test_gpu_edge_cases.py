@@ -104,3 +104,16 @@ def test_per_partition_operators_on_empty_partition():
     glob = np.ones((g.num_vertices, 5))
     res = g2.scatter_accumulate(ga, topo.gather_map, glob)
     assert res is glob and np.array_equal(glob, np.ones((g.num_vertices, 5)))
+
+
+@pytest.mark.parametrize("keep", ["0", "1"])
+@pytest.mark.parametrize("mode", ["mean_self_loop", "symmetric_norm"])
+@pytest.mark.parametrize("F,C,L,H", [(6, 3, 3, 12), (12, 20, 2, 8), (5, 9, 3, 7)])
+def test_aggregate_first_kept_vs_regathered(keep, mode, F, C, L, H, monkeypatch):
+    """Aggregate-first GCN layers (hidden: N kept from the forward; last: N
+    still in place) and the regather (GRD_KEEP_AGG=0) both match the oracle
+    over two epochs."""
+    monkeypatch.setenv("GRD_KEEP_AGG", keep)
+    g = g2.generate_kronecker(9, 6, seed=4)
+    labels = g2.random_partition(g.num_vertices, 3, 2)
+    _check(g, labels, 3, F=F, C=C, L=L, H=H, mode=mode)
