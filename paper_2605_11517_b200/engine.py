@@ -592,12 +592,14 @@ class LayerwiseEngine(_EngineBase):
         # reference's regather (GRD_KEEP_AGG=0 regathers)
         self.keep_on = os.environ.get("GRD_KEEP_AGG", "1") != "0"
         self.n_kept = {}
-        if self.keep_on and str(dev).startswith("cuda"):
+        if self.keep_on:
             hidden = [l for l, c in enumerate(self.cfg)
                       if not (c.transform_first or c.sage or c.gat or c.rownorm or c.last)]
             need = sum(self.NL * ld_of(self.cfg[l].d_in) * 4 for l in hidden)
-            if hidden and need + (4 << 30) < torch.cuda.mem_get_info(torch.device(dev))[0]:
+            if hidden and self._keep_fits(need):
                 self.n_kept = {l: ops.zeros_rows(self.NL, self.cfg[l].d_in, dev) for l in hidden}
+        if model.kind == "gat":
+            self._alloc_gat_kept(model)
         self.g = ops.zeros_rows(self.NL, wide, dev)
         self.h = ops.zeros_rows(self.NL, wide, dev)
         if model.kind == "sage":
@@ -734,22 +736,35 @@ class LayerwiseEngine(_EngineBase):
         hdp = self.cfg[-1].hdp
         self.t2 = ops.zeros_rows(self.NL, hdp, dev)
         self.t3 = ops.zeros_rows(self.NL, hdp, dev)
-        # Hidden layers' [P | s | t] and attention kept from the forward when
-        # they fit (a few GB at the products shape): the backward then skips
-        # the regather (transform GEMM + edge softmax).  The last layer's are
-        # still in t1 / alpha when its backward runs.  GRD_GAT_KEEP=0, or too
-        # little free HBM, recomputes them as the reference's regather does.
         self.gat_kept = {}
         self.gat_keep_on = os.environ.get("GRD_GAT_KEEP", "1") != "0"
-        if self.gat_keep_on and str(dev).startswith("cuda"):
-            hidden = [l for l, c in enumerate(self.cfg) if c.gat and not c.last]
-            need = sum(self.NL * ops.ld_of(self.cfg[l].ld_ext) * 4 + (max(E, 1) + self.NL) * H * 4
-                       for l in hidden)
-            free = torch.cuda.mem_get_info(torch.device(dev))[0]
-            if need + (4 << 30) < free:
-                for l in hidden:
-                    self.gat_kept[l] = (ops.zeros_rows(self.NL, self.cfg[l].ld_ext, dev),
-                                        torch.zeros_like(self.alpha), torch.zeros_like(self.alpha_self))
+
+    def _keep_fits(self, need: int) -> bool:
+        """Whether `need` more bytes of kept forward state leave a margin of
+        free HBM (max(4 GB, 10 % of the device)) for the lazily allocated
+        scratch (heavy-row partials, exchange buffers, graph capture)."""
+        if not str(self.device).startswith("cuda"):
+            return False
+        free, total = torch.cuda.mem_get_info(torch.device(self.device))
+        return need + max(4 << 30, total // 10) < free
+
+    def _alloc_gat_kept(self, model) -> None:
+        """Hidden layers' [P | s | t] and attention kept from the forward when
+        they fit (a few GB at the products shape): the backward then skips the
+        regather (transform GEMM + edge softmax).  The last layer's are still
+        in t1 / alpha when its backward runs.  GRD_GAT_KEEP=0, or too little
+        free HBM, recomputes them as the reference's regather does."""
+        if not self.gat_keep_on:
+            return
+        H = model.heads
+        E = self.dg.fwd.nnz
+        hidden = [l for l, c in enumerate(self.cfg) if c.gat and not c.last]
+        need = sum(self.NL * ops.ld_of(self.cfg[l].ld_ext) * 4 + (max(E, 1) + self.NL) * H * 4
+                   for l in hidden)
+        if hidden and self._keep_fits(need):
+            for l in hidden:
+                self.gat_kept[l] = (ops.zeros_rows(self.NL, self.cfg[l].ld_ext, self.device),
+                                    torch.zeros_like(self.alpha), torch.zeros_like(self.alpha_self))
 
     def _gat_bufs(self, l: int):
         """(P_ext, alpha, alpha_self) buffers of layer l: kept per layer, or
