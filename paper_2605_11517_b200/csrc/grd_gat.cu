@@ -300,6 +300,47 @@ __global__ void __launch_bounds__(256) gat_softmax_small_kernel(grd_gat_args a, 
     }
 }
 
+// Pass 1b, one warp per heavy row: merge the row's segment partials in a
+// fixed order (lane-strided, then a butterfly) into the first segment's slot.
+// Once per row: every segment warp merging all of its row's partials was
+// quadratic in the segment count of a hub row.
+template <int HM>
+__global__ void __launch_bounds__(256) gat_softmax_merge_kernel(grd_gat_args a) {
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int64_t hr = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (hr >= a.n_heavy) return;
+    const int H = a.heads;
+    const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
+    float mx[HM], sm[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        mx[h] = -INFINITY;
+        sm[h] = 0.f;
+    }
+    for (int64_t j = s0 + lane; j < s1; j += kWarp) {
+        const float* part = a.seg_scratch + j * 2 * H;
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+            if (h < H) lse_merge(mx[h], sm[h], part[h], part[H + h]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int h = 0; h < HM; ++h) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, mx[h], o);
+            const float d2 = __shfl_xor_sync(0xffffffffu, sm[h], o);
+            lse_merge(mx[h], sm[h], m2, d2);
+        }
+    __syncwarp();   // every lane has read the partials before lane h overwrites slot s0
+    float* out = a.seg_scratch + s0 * 2 * H;
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+        if (h < H && lane == h) {
+            out[h] = mx[h];
+            out[H + h] = sm[h];
+        }
+}
+
 // Pass 2, one warp per heavy segment: merge the row's segment partials in a
 // fixed order (every warp of the row gets bit-identical statistics), then
 // normalise this segment's scores (recomputed, loads issued up front).
@@ -313,28 +354,16 @@ __global__ void __launch_bounds__(256) gat_softmax_heavy_kernel(grd_gat_args a) 
     const int32_t v = vertex_of(a, un.row);
     float z[kItems][HM];
     unit_scores<HM>(a, un, v, lane, z);
+    // the row's merged statistics (gat_softmax_merge_kernel) sit in the slot
+    // of its first segment
     const int64_t hr = a.seg_heavy[s];
-    const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
+    const float* stat = a.seg_scratch + a.heavy_seg_ptr[hr] * 2 * H;
     float mx[HM], sm[HM];
 #pragma unroll
     for (int h = 0; h < HM; ++h) {
-        mx[h] = -INFINITY;
-        sm[h] = 0.f;
+        mx[h] = h < H ? __ldg(stat + h) : -INFINITY;
+        sm[h] = h < H ? __ldg(stat + H + h) : 1.f;
     }
-    for (int64_t j = s0 + lane; j < s1; j += kWarp) {
-        const float* part = a.seg_scratch + j * 2 * H;
-#pragma unroll
-        for (int h = 0; h < HM; ++h)
-            if (h < H) lse_merge(mx[h], sm[h], __ldg(part + h), __ldg(part + H + h));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int h = 0; h < HM; ++h) {
-            const float m2 = __shfl_xor_sync(0xffffffffu, mx[h], o);
-            const float d2 = __shfl_xor_sync(0xffffffffu, sm[h], o);
-            lse_merge(mx[h], sm[h], m2, d2);
-        }
     float inv[HM];
 #pragma unroll
     for (int h = 0; h < HM; ++h) inv[h] = 1.f / sm[h];
@@ -679,6 +708,15 @@ extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
     }
     int rc = launch_status("gat_softmax");
     if (rc || args->n_segs == 0) return rc;
+    if (H == 1)
+        gat_softmax_merge_kernel<1><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    else if (H == 2)
+        gat_softmax_merge_kernel<2><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    else if (H <= 4)
+        gat_softmax_merge_kernel<4><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    else
+        gat_softmax_merge_kernel<8><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    if ((rc = launch_status("gat_softmax_merge"))) return rc;
     if (H == 1)
         gat_softmax_heavy_kernel<1><<<warps_blocks(args->n_segs), 256, 0, st>>>(*args);
     else if (H == 2)

@@ -367,7 +367,8 @@ def gat_softmax(spec, p_ext, heads, dhp, alpha, alpha_self, st=None) -> None:
     E, R = spec.nnz, spec.n_rows
     # idx + s_u sector per edge, t_v per row, alpha written
     nbytes = 8 * (R + 1) + 4 * E + 4 * heads * (E + R) * 2 + 4 * heads * R
-    _launch("gat_softmax", 1 + (spec.n_segs > 0), nbytes, 8.0 * heads * (E + R),
+    launches = 1 + (spec.n_mid > 0) + (spec.n_small > 0) + 2 * (spec.n_segs > 0)
+    _launch("gat_softmax", launches, nbytes, 8.0 * heads * (E + R),
             lambda: _lib.check(_lib.lib().grd_gat_softmax(ctypes.byref(a), stream_ptr()), "gat_softmax"))
 
 
@@ -389,7 +390,7 @@ def gat_src_grad(spec, heads, dhp, edge_perm, delta, delta_self, grad_ext) -> No
     a = _gat_args(spec, grad_ext, heads, dhp, edge_perm=edge_perm, delta=delta, delta_self=delta_self,
                   grad_ext=grad_ext, ld_gext=_ld(grad_ext))
     E, R = spec.nnz, spec.n_rows
-    _launch("gat_src_grad", 1 + (spec.n_heavy > 0), 8 * E + 4 * heads * (E + 2 * R), heads * E,
+    _launch("gat_src_grad", 1 + (spec.n_mid > 0) + (spec.n_small > 0) + (spec.n_heavy > 0), 8 * E + 4 * heads * (E + 2 * R), heads * E,
             lambda: _lib.check(_lib.lib().grd_gat_src_grad(ctypes.byref(a), stream_ptr()),
                                "gat_src_grad"))
 
