@@ -3,15 +3,23 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
 A step is one full-graph training epoch (forward over every partition, loss,
-regather backward, SGD) of the named synthetic workload.  Prints ONE JSON
-line (rank 0).  Metric (BASELINE.json): aggregated edges/s = L*|E| per epoch
-over all GPUs, plus epoch time; ``roofline`` covers the dominant kernel and
-``agg_roofline`` the aggregation kernels (north star: >= 60% of HBM peak).
+regather backward, SGD) of the named synthetic workload.  The default is
+``papers_full``: configs[3] at full size (3-layer GCN, F=H=128, C=172 on a
+134 M-vertex / 1.61 B-edge papers-shaped Kronecker graph, 16 switching-aware
+partitions), the north-star target.  Prints ONE JSON line (rank 0).  Metric
+(BASELINE.json): aggregated edges/s = L*|E| per epoch over all GPUs, plus
+epoch time; ``roofline`` is the dominant kernel's DRAM-side HBM fraction
+(ncu DRAM bytes per launch over the live launch time) with the SURVEY 8(d)
+per-edge streaming-model figure beside it; ``engines`` times the other
+engines (kept-state / regather layer-wise, per-partition with the K1 gather,
+streaming) on the largest papers-shaped instance the reference itself
+trained for the golden fixtures.
 
 --impl reference times the reference algorithm's CPU implementation — the
-float64 numpy port in oracle/ (the reference is pure Python and cannot be
-shipped to the GPU box; oracle/ is pinned to its golden vectors) — on the
-host cores, on the same workload.
+float64 numpy restatement in oracle/ (pinned to the reference's golden
+vectors; the reference package itself is not installed on the GPU box) —
+on the host cores, on a bounded sample of the same workload built by the
+oracle alone (oracle/workload.py: no product code, no native library).
 """
 
 from __future__ import annotations
@@ -36,14 +44,15 @@ WORKLOADS = {
     "config1": dict(
         desc="configs[0]: 2-layer GCN hidden 64, generate_kronecker(17, 8): 131,072 V / "
              "1,048,576 E, 128 feats, 10 classes, 8 switching-aware partitions",
-        scale=17, deg=8, F=128, C=10, L=2, H=64, P=8, mode="mean_self_loop"),
+        scale=17, deg=8, F=128, C=10, L=2, H=64, P=8, mode="mean_self_loop",
+    ref_sample=dict(scale=15, deg=8)),
 }
 WORKLOADS["products_sage"] = dict(
     desc="configs[1]: 3-layer GraphSAGE-mean hidden 256, ogbn-products-shaped "
          "generate_kronecker(21, 30): 2,097,152 V / 62,914,560 E, 100 feats, 47 classes, "
          "8 switching-aware partitions",
     scale=21, deg=30, F=100, C=47, L=3, H=256, P=8, mode="sage_mean",
-    cpu_sample=dict(scale=19, deg=30), ref_sample=dict(scale=18, deg=30))
+    cpu_sample=dict(scale=18, deg=30), ref_sample=dict(scale=17, deg=30))
 WORKLOADS["products_gat"] = dict(
     desc="configs[2]: 3-layer GAT (4 heads x 64 concat, mean on the last layer) on the "
          "ogbn-products-shaped generate_kronecker(21, 30): 2,097,152 V / 62,914,560 E, "
@@ -55,7 +64,7 @@ WORKLOADS["papers_gcn"] = dict(
          "ogbn-papers100M-shaped generate_kronecker(25, 14): 33,554,432 V / 469,762,048 E "
          "(papers100M average degree), 128 feats, 172 classes, 16 switching-aware partitions",
     scale=25, deg=14, F=128, C=172, L=3, H=128, P=16, mode="mean_self_loop",
-    cpu_sample=dict(scale=17, deg=14))
+    cpu_sample=dict(scale=16, deg=14), ref_sample=dict(scale=15, deg=14))
 WORKLOADS["papers_full"] = dict(
     desc="configs[3] at full size: 3-layer GCN hidden 128 on an ogbn-papers100M-shaped "
          "generate_kronecker(27, 12): 134,217,728 V / 1,610,612,736 E (1.6 B edges, papers "
@@ -63,7 +72,8 @@ WORKLOADS["papers_full"] = dict(
          "not fit HBM, so the streaming engine keeps two layer buffers + the graph in HBM and "
          "streams the host-resident features (stream.py)",
     scale=27, deg=12, F=128, C=172, L=3, H=128, P=16, mode="mean_self_loop",
-    feature_dtype="float32", host_gb=150, cpu_sample=dict(scale=17, deg=12))
+    feature_dtype="float32", host_gb=150, cpu_sample=dict(scale=16, deg=12),
+    ref_sample=dict(scale=15, deg=12))
 WORKLOADS["igb_nvme"] = dict(
     desc="configs[4] model and tiers at 1/24 of its size: 3-layer GraphSAGE-mean hidden 256 on "
          "IGB-shaped 1024-wide features, generate_kronecker(22, 12) (4,194,304 V / 50,331,648 E), "
@@ -73,7 +83,7 @@ WORKLOADS["igb_nvme"] = dict(
     scale=22, deg=12, F=1024, C=19, L=3, H=256, P=8, mode="sage_mean",
     feature_dtype="float32", tier="nvme", x_cache_gb=4, host_cache_gb=4,
     cpu_sample=dict(scale=14, deg=12))
-DEFAULT_WORKLOAD = "products_sage"
+DEFAULT_WORKLOAD = "papers_full"
 LR = 0.01
 SEED = 0
 
@@ -187,6 +197,84 @@ def flush_l2(buf):
     buf.add_(1.0)   # 512 MiB write evicts the 126 MB L2 between timed steps
 
 
+# the papers-shaped instance the reference itself trained for the golden
+# fixtures (tests/golden/papers_s22.npz): configs[3]'s model on
+# generate_kronecker(22, 12)
+ENGINE_SPEC = dict(desc="configs[3]'s model (3-layer GCN, F=H=128, C=172, P=16) on "
+                        "generate_kronecker(22, 12): 4,194,304 V / 50,331,648 E",
+                   scale=22, deg=12, F=128, C=172, L=3, H=128, P=16, mode="mean_self_loop",
+                   feature_dtype="float32")
+
+
+def engine_table(reps: int = 3):
+    """Epoch time of each engine on ENGINE_SPEC, so every subsystem of the
+    north star is timed: the layer-wise engine keeping the forward state
+    (the default when HBM allows), the same engine regathering in the
+    backward (GRD_KEEP_AGG=0: the reference's regather schedule), the
+    per-partition engine (K1 gather of GA_p per (layer, partition),
+    regather backward, scatter — the schedule observers see) and the
+    layer-streaming engine (stream.py).  CUDA events on the current stream,
+    L2 flushed before every epoch."""
+    import gc
+    import torch
+    from paper_2605_11517_b200.stream import StreamSession
+    from paper_2605_11517_b200.training import TrainSession
+    g, ds, plan, model, _ = build_workload(ENGINE_SPEC)
+    edges = ENGINE_SPEC["L"] * g.num_edges
+    flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    out = {"workload": ENGINE_SPEC["desc"], "reps": reps}
+
+    def timed(run):
+        for w in range(2):
+            run(w)
+        ms = []
+        for k in range(reps):
+            flush_l2(flush)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            run(k)
+            e.record()
+            torch.cuda.synchronize()
+            ms.append(s.elapsed_time(e))
+        return min(ms)
+
+    def record(name, ms, loss, note):
+        out[name] = {"ms_per_epoch": round(ms, 3), "edges_per_s": round(edges / (ms * 1e-3), 1),
+                     "loss": loss, "note": note}
+
+    prev = os.environ.get("GRD_KEEP_AGG")
+    for name, keep, note in (("layerwise_kept", "1", "HBM-resident layer-wise, forward "
+                              "aggregates kept for the weight gradient"),
+                             ("layerwise_regather", "0", "HBM-resident layer-wise, backward "
+                              "regathers (GRD_KEEP_AGG=0)")):
+        os.environ["GRD_KEEP_AGG"] = keep
+        sess = TrainSession(ds, plan, model)
+        ms = timed(lambda k: sess.run_epoch(k, LR))
+        record(name, ms, sess.read_stats()[0], note)
+        del sess
+        gc.collect()
+    if prev is None:
+        os.environ.pop("GRD_KEEP_AGG", None)
+    else:
+        os.environ["GRD_KEEP_AGG"] = prev
+    sess = TrainSession(ds, plan, model, layerwise=False)
+    ms = timed(lambda k: sess.train(1, LR, use_graph=False))
+    record("per_partition", ms, sess.read_stats()[0],
+           "per-(layer, partition) schedule: K1 gather of GA_p, aggregate, transform; "
+           "regather backward; ascending-pid scatter (eager, includes the weight export)")
+    del sess
+    gc.collect()
+    sess = StreamSession(ds, plan, model)
+    ms = timed(lambda k: sess.run_epoch(k, LR))
+    record("streaming", ms, sess.read_stats()[0], "layer-streaming engine (stream.py), "
+           "features in the HBM cache")
+    del sess, flush
+    plan.device_cache.clear()
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, spec, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -213,6 +301,7 @@ def run_ours(args, spec, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    engines = engine_table() if world == 1 and not args.no_engines else None
     g, ds, plan, model, prep = build_workload(spec)
     L, E = spec["L"], g.num_edges
     if spec.get("tier") == "nvme":
@@ -328,31 +417,38 @@ def run_ours(args, spec, rank, world, local_rank):
     dom = max(per_kernel, key=lambda n: per_kernel[n]["ms"])
     epoch_ms_instr = sum(k["ms"] for k in per_kernel.values())
 
-    def roof(name):
-        k = per_kernel[name]
-        gbs = k["bytes"] / (k["ms"] * 1e-3) / 1e9
-        return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None,
-                "peak_source": peak_kind, "launches_per_epoch": k["launches"],
-                "ms_per_epoch": round(k["ms"], 4),
-                "algorithmic_bytes_per_launch": int(k["bytes"] / k["launches"]),
-                "share_of_epoch": round(k["ms"] / epoch_ms_instr, 4)}
+    traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()) \
+        if (ROOT / "profiles" / "traffic.json").exists() else {}
+    tr = traffic.get(args.workload, {})
 
-    traffic_file = ROOT / "profiles" / "traffic.json"
+    def roof(name):
+        """HBM roofline of one kernel: DRAM bytes per launch (one ncu capture
+        of this workload, profiles/traffic.json) over the live average launch
+        time; the SURVEY 8(d) per-edge streaming model (no cache reuse
+        credited, so it can exceed the peak when hub rows hit L2) beside it."""
+        k = per_kernel[name]
+        per_launch_s = k["ms"] * 1e-3 / k["launches"]
+        model_gbs = k["bytes"] / k["launches"] / per_launch_s / 1e9
+        r = {"kernel": name, "bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
+             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json copy bandwidth, burst)",
+             "launches_per_epoch": k["launches"], "ms_per_epoch": round(k["ms"], 4),
+             "share_of_epoch": round(k["ms"] / epoch_ms_instr, 4),
+             "algorithmic_bytes_per_launch": int(k["bytes"] / k["launches"]),
+             "streaming_model_GBs": round(model_gbs, 1),
+             "streaming_model_frac": round(model_gbs / hbm_peak, 4)}
+        if name in tr:
+            dram = float(tr[name])
+            gbs = dram / per_launch_s / 1e9
+            r.update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4), traffic=int(dram),
+                     basis="ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                           f"({tr.get('_source', 'profiles/traffic.json')}) / live launch time")
+        else:
+            r.update(achieved=round(model_gbs, 1), frac=round(model_gbs / hbm_peak, 4),
+                     traffic=None, basis="streaming model (no ncu DRAM capture of this workload)")
+        return r
+
     roofline = roof(dom)
-    agg_roof = roof("agg_sum")
-    if traffic_file.exists():
-        tr = json.loads(traffic_file.read_text()).get(args.workload, {})
-        for r in (roofline, agg_roof):
-            if r["kernel"] in tr:
-                # DRAM bytes per launch (ncu) and the DRAM-side rate they imply
-                r["traffic"] = tr[r["kernel"]]
-                per_launch_s = r["ms_per_epoch"] * 1e-3 / r["launches_per_epoch"]
-                r["dram_GBs_implied"] = round(r["traffic"] / per_launch_s / 1e9, 1)
-                r["dram_frac"] = round(r["dram_GBs_implied"] / hbm_peak, 4)
-                r["note"] = ("achieved/frac count algorithmic bytes (SURVEY 8(d) per-edge streaming "
-                             "model); 43-69 % of the row gathers hit L2, so DRAM moves less: "
-                             "traffic / dram_frac are the ncu DRAM side")
+    agg_roof = roof("agg_sum") if "agg_sum" in per_kernel else None
     edges_per_epoch = L * E
     # strong scaling: the N ranks together train ONE epoch of the whole graph,
     # so the job processes L*|E| edges per step whatever N is
@@ -399,72 +495,69 @@ def run_ours(args, spec, rank, world, local_rank):
         "clocks": clock,
         "gpu_launches": launches_per_epoch * args.steps,
     }
+    if engines is not None:
+        out["engines"] = engines
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(spec, g, ds, plan, model)
+        out["cpu_baseline"] = cpu_baseline(spec)
     if world > 1:
         dist.destroy_process_group()
     return out
 
 
-def oracle_epoch_seconds(spec, ds, plan, model, epochs=1):
-    t0 = time.perf_counter()
-    if spec["mode"] == "sage_mean":
-        from oracle import sage_gat
-        sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, ds.graph.src_ptr, ds.graph.dst_idx,
-                            model.weights, epochs, LR)
-    elif spec["mode"] == "gat":
-        from oracle import sage_gat
-        sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, ds.graph.src_ptr, ds.graph.dst_idx,
-                           model.weights, model.heads, epochs, LR)
-    else:
-        from oracle import gcn
-        gcn.train_partitioned(ds.features, ds.labels, ds.train_mask, plan.topologies, model.weights,
-                              epochs, LR, mode=spec["mode"])
-    return (time.perf_counter() - t0) / epochs
+def oracle_sample(spec, key):
+    """The bounded CPU sample of the workload, built by the oracle alone
+    (oracle/workload.py): the same model on generate_kronecker(scale, deg)
+    of the same average degree, or the workload itself when it is small."""
+    from oracle import workload
+    smp = spec.get(key) or spec.get("cpu_sample") or dict(scale=spec["scale"], deg=spec["deg"])
+    s = workload.build(smp["scale"], smp["deg"], spec["F"], spec["C"], spec["L"], spec["H"],
+                       spec["P"], mode=spec["mode"], heads=spec.get("heads", 4), seed=SEED)
+    whole = smp["scale"] == spec["scale"] and smp["deg"] == spec["deg"]
+    what = (f"generate_kronecker({smp['scale']}, {smp['deg']}) ({s.num_vertices} V / "
+            f"{s.num_edges} E){' (the whole workload)' if whole else ', same model'}")
+    return s, what
 
 
-def cpu_sample(spec, g, ds, plan, model, key="cpu_sample"):
-    """The workload itself, or (for graphs the float64 oracle cannot hold in
-    host memory / a bounded time) the same model on a smaller Kronecker graph
-    of the same average degree.  ``ref_sample``: the reference arm's per-step
-    sample (smaller, so K + W steps stay within a few minutes)."""
-    smp = spec.get(key) or spec.get("cpu_sample")
-    if smp is None:
-        return g, ds, plan, model, "the full workload"
-    sub = dict(spec, scale=smp["scale"], deg=smp["deg"])
-    g2_, ds2, plan2, model2, _ = build_workload(sub)
-    return g2_, ds2, plan2, model2, (f"generate_kronecker({smp['scale']}, {smp['deg']}) "
-                                     f"({g2_.num_vertices} V / {g2_.num_edges} E), same model")
+def _oracle_name(spec):
+    return ("oracle/sage_gat.py (torch float64 CPU, builder-defined layer)"
+            if spec["mode"] in ("sage_mean", "gat") else
+            "oracle/gcn.py (float64 numpy restatement of the reference's partitioned_train, "
+            "pinned to its golden vectors)")
 
 
-def cpu_baseline(spec, g, ds, plan, model):
-    g, ds, plan, model, what = cpu_sample(spec, g, ds, plan, model)
-    secs = oracle_epoch_seconds(spec, ds, plan, model)
-    oracle = "oracle/sage_gat.py (torch float64 CPU)" if spec["mode"] in ("sage_mean", "gat") else \
-        "oracle/gcn.py (float64 numpy restatement of the reference, pinned to its golden vectors)"
-    return {"value": round(spec["L"] * g.num_edges / secs, 1), "unit": "edges/s",
+def cpu_baseline(spec):
+    from oracle import workload
+    s, what = oracle_sample(spec, "cpu_sample")
+    secs = workload.epoch_seconds(s, LR)
+    return {"value": round(spec["L"] * s.num_edges / secs, 1), "unit": "edges/s",
             "cores": os.cpu_count(), "kind": "port",
-            "sample": f"one epoch of {what} in {oracle}, all host threads: {secs:.2f} s"}
+            "sample": f"one epoch of {what} in {_oracle_name(spec)}, all host threads "
+                      f"(OpenBLAS; numpy gathers / reduceat single-threaded): {secs:.2f} s"}
 
 
 def run_reference(args, spec, rank, world):
+    """The reference arm: the pinned CPU restatement of the reference's
+    path on the box's host cores; rank 0 only (the others exit 0)."""
     if rank != 0:
         return None
-    g, ds, plan, model, prep = build_workload(spec)
-    g, ds, plan, model, what = cpu_sample(spec, g, ds, plan, model, key="ref_sample")
+    from oracle import workload
+    s, what = oracle_sample(spec, "ref_sample")
     for _ in range(args.warmup):
-        oracle_epoch_seconds(spec, ds, plan, model)
-    times = [oracle_epoch_seconds(spec, ds, plan, model) for _ in range(args.steps)]
+        workload.epoch_seconds(s, LR)
+    times = [workload.epoch_seconds(s, LR) for _ in range(args.steps)]
     secs = sum(times) / len(times)
-    value = spec["L"] * g.num_edges / secs
+    value = spec["L"] * s.num_edges / secs
     return {
         "impl": "reference",
         "metric": "aggregated edges/s (L*|E| per full-graph training epoch)",
         "value": round(value, 1), "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 3), "epoch_s": round(secs, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload, "desc": spec["desc"],
-                                        "num_edges": g.num_edges, "preprocess": prep},
+        "data": "synthetic (oracle-built: reference generator / dataset / partitioner / plan "
+                "restated)",
+        "config": {"workload": args.workload, "desc": spec["desc"], "sample": what,
+                   "sample_num_edges": s.num_edges, "sample_build_s": round(s.build_s, 2),
+                   "implementation": _oracle_name(spec)},
         "cpu_baseline": {"value": round(value, 1), "unit": "edges/s", "cores": os.cpu_count(),
                          "kind": "port", "sample": f"one epoch of {what} per step"},
         "e2e": {"value": round(value, 1), "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -480,6 +573,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-engines", action="store_true",
+                    help="skip the per-engine epoch table (ENGINE_SPEC)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -214,5 +214,14 @@ class Communicator:
         self.dist.all_reduce(h, group=self.group)
         t.copy_(h)
 
+    def all_reduce_min(self, t) -> None:
+        op = self.dist.ReduceOp.MIN
+        if self.device_native:
+            self.dist.all_reduce(t, op=op, group=self.group)
+            return
+        h = t.cpu()
+        self.dist.all_reduce(h, op=op, group=self.group)
+        t.copy_(h)
+
     def barrier(self) -> None:
         self.dist.barrier(group=self.group)

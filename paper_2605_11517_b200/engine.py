@@ -214,7 +214,9 @@ class ShardDeviceGraph(DeviceGraph):
     def _buf(self, key: str, rows: int, ld: int) -> torch.Tensor:
         t = self._bufs.get(key)
         if t is None or t.numel() < max(rows * ld, 1):
-            t = torch.empty(max(rows * ld, 1), dtype=torch.float32, device=self.device)
+            # zeroed once: padding columns of packed rows stay 0 (a halo row
+            # received in place carries the sender's padding into the block)
+            t = torch.zeros(max(rows * ld, 1), dtype=torch.float32, device=self.device)
             self._bufs[key] = t
         return t[: rows * ld].view(rows, ld)
 
@@ -222,21 +224,29 @@ class ShardDeviceGraph(DeviceGraph):
         self._exchange_finish(self._exchange_start(buf, width), buf, width)
 
     def _exchange_start(self, buf: torch.Tensor, width: int):
-        """Pack the rows other ranks need and start the all-to-all."""
+        """Pack the rows other ranks need and start the all-to-all.  When
+        ``buf``'s rows are exactly ld(width) wide the halo block
+        ``buf[n_own:]`` is contiguous and receives the rows in place;
+        otherwise they land in a scratch buffer and are unpacked."""
         ld = ld_of(width)
         send = self._buf("send", self.n_send, ld)
-        recv = self._buf("recv", self.n_recv, ld)
+        direct = buf.dim() == 2 and buf.shape[1] == ld and buf.stride(0) == ld \
+            and buf.stride(1) == 1
+        recv = buf[self.n_own:self.n_own + self.n_recv] if direct else \
+            self._buf("recv", self.n_recv, ld)
         if self.n_send:
             ops.gather_rows(buf, self.send_idx, send, width)
-        return self.comm.all_to_all_rows(recv, send, self.shard.recv_counts, self.shard.send_counts,
-                                         async_op=True)
+        work = self.comm.all_to_all_rows(recv, send, self.shard.recv_counts,
+                                         self.shard.send_counts, async_op=True)
+        return work, direct
 
-    def _exchange_finish(self, work, buf: torch.Tensor, width: int) -> None:
-        """Wait for the all-to-all (a stream wait under NCCL) and unpack the
-        received rows into the halo block."""
+    def _exchange_finish(self, started, buf: torch.Tensor, width: int) -> None:
+        """Wait for the all-to-all (a stream wait under NCCL) and, when the
+        rows went to the scratch buffer, unpack them into the halo block."""
+        work, direct = started
         if work is not None:
             work.wait()
-        if self.n_recv:
+        if self.n_recv and not direct:
             recv = self._buf("recv", self.n_recv, ld_of(width))
             ops.gather_rows(recv, self.recv_ident, buf[self.n_own:], width)
 
@@ -423,14 +433,26 @@ class _Weights:
         if self.gat:
             self._init_gat(model, device)
             return
+        shapes = []
         for l, w in enumerate(model.weights):
             d_in, d_out = w.shape[0], w.shape[1] // self.blocks
             shape = (2 * ld_of(d_in), ld_of(d_out)) if l in self.stacked else \
                 (ld_of(d_in), self.blocks * ld_of(d_out))
-            t = torch.zeros(shape, dtype=torch.float32, device=device)
-            self.w.append(t)
-            self.dw.append(torch.zeros_like(t))
+            self.w.append(torch.zeros(shape, dtype=torch.float32, device=device))
+            shapes.append(shape)
+        self.dw = self._bucket(shapes, device)
         self.load(model)
+
+    def _bucket(self, shapes, device) -> list[torch.Tensor]:
+        """Weight-gradient tensors as views of one flat buffer (``grad_bucket``),
+        so a sharded run sums every layer's gradient with one all-reduce."""
+        sizes = [a * b for a, b in shapes]
+        self.grad_bucket = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
+        out, off = [], 0
+        for (a, b), n in zip(shapes, sizes):
+            out.append(self.grad_bucket[off:off + n].view(a, b))
+            off += n
+        return out
 
     # GAT: W per head padded to dhp columns [ld(d_in), H*dhp]; att = [a_src; a_dst]
     # as [2, H, dhp]; the fused transform matrix W_ext [ld(d_in), ld_ext] is
@@ -439,7 +461,6 @@ class _Weights:
         H = model.heads
         self.heads = H
         self.att, self.datt, self.wext, self.dwext, self.shape = [], [], [], [], []
-        L = len(model.weights)
         for l, wp in enumerate(model.weights):
             d_in = wp.shape[0] - 2
             dh = wp.shape[1] // H
@@ -451,7 +472,8 @@ class _Weights:
             self.att.append(torch.zeros((2, H, dhp), dtype=torch.float32, device=device))
             self.datt.append(torch.zeros_like(self.att[-1]))
             self.wext.append(torch.zeros((ld_of(d_in), ld_of(n_ext)), dtype=torch.float32, device=device))
-            self.dwext.append(torch.zeros_like(self.wext[-1]))
+        # the fused [W | W a_src | W a_dst] gradient is what ranks sum
+        self.dwext = self._bucket([tuple(t.shape) for t in self.wext], device)
         self.load(model)
 
     def _gat_load(self, model) -> None:
@@ -746,7 +768,15 @@ class LayerwiseEngine(_EngineBase):
         if not str(self.device).startswith("cuda"):
             return False
         free, total = torch.cuda.mem_get_info(torch.device(self.device))
-        return need + max(4 << 30, total // 10) < free
+        fits = need + max(4 << 30, total // 10) < free
+        if self.comm is not None:
+            # the kept and the regathering backward issue different
+            # exchanges: every rank must make the same choice (all keep or
+            # none), or the all-to-alls pair up wrongly
+            flag = torch.tensor([1.0 if fits else 0.0], dtype=torch.float32, device=self.device)
+            self.comm.all_reduce_min(flag)
+            fits = bool(flag.item() > 0.5)
+        return fits
 
     def _alloc_gat_kept(self, model) -> None:
         """Hidden layers' [P | s | t] and attention kept from the forward when
@@ -942,15 +972,14 @@ class LayerwiseEngine(_EngineBase):
         """Sharded runs: sum the local weight gradients over ranks, then the
         replicated SGD step (training.py:343,352-354)."""
         wt = self.wts
+        self.comm.all_reduce_sum(wt.grad_bucket)     # every layer in one all-reduce
         if wt.gat:
             for l, c in enumerate(self.cfg):
                 d_in, dh, dhp = wt.shape[l]
-                self.comm.all_reduce_sum(wt.dwext[l])
                 ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp,
                                     wt.dw[l], wt.datt[l], lr)
             return
         for W, dW in zip(self.wts.w, self.wts.dw):
-            self.comm.all_reduce_sum(dW)
             ops.wgrad_sgd(W, W, dW, dW.shape[0], dW.shape[1], 0, accumulate=True, w=W, lr=lr)
 
     def epoch(self, lr: float) -> None:

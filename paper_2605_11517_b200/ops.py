@@ -9,6 +9,7 @@ zero padding columns (see include/grinder_b200.h).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,7 @@ class Recorder:
 
     def __init__(self):
         self.launches = 0
+        self.calls = 0
         self.timing = False
         self.records: list = []
 
@@ -42,8 +44,26 @@ class Recorder:
 RECORDER = Recorder()
 
 
+# GRD_NVTX=1: every op is an NVTX range "<op>#<n>" (n counts op calls), so
+# `ncu --nvtx --print-nvtx-rename kernel` attributes each CUDA kernel to the
+# op invocation that launched it (tools/dram_traffic.py)
+_NVTX = os.environ.get("GRD_NVTX", "0") == "1"
+
+
 def _launch(name: str, nlaunch: int, nbytes: float, flops: float, fn) -> None:
     RECORDER.launches += nlaunch
+    if _NVTX:
+        RECORDER.calls += 1
+        torch.cuda.nvtx.range_push(f"{name}#{RECORDER.calls}")
+        try:
+            _launch_inner(name, nbytes, flops, fn)
+        finally:
+            torch.cuda.nvtx.range_pop()
+        return
+    _launch_inner(name, nbytes, flops, fn)
+
+
+def _launch_inner(name: str, nbytes: float, flops: float, fn) -> None:
     if not RECORDER.timing:
         fn()
         return

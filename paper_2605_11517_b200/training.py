@@ -209,7 +209,14 @@ class TrainSession:
         lab, msk = np.asarray(dataset.labels)[own], np.asarray(dataset.train_mask)[own]
         eng.labels.copy_(pinned_rows(dataset, "labels", lab, torch.int32), non_blocking=True)
         eng.mask.copy_(pinned_rows(dataset, "mask", msk, torch.uint8), non_blocking=True)
-        eng.mask_count = int(np.count_nonzero(dataset.train_mask))
+        count = int(np.count_nonzero(dataset.train_mask))
+        if count != eng.mask_count:
+            # the loss kernel takes 1/|mask| by value: a captured epoch graph
+            # holds the old count, so it is re-captured on the next epoch
+            eng.mask_count = count
+            self._graph = None
+        if count == 0:
+            raise ValueError("train_mask selects no vertices")
         self.model = copy_model(model)
         eng.wts.load(self.model)
         self.dataset = dataset

@@ -135,7 +135,7 @@ def main() -> None:
         print(f, (OUT / f).stat().st_size, "bytes")
 
 
-if __name__ == "__main__" and "--ledger" not in sys.argv:
+if __name__ == "__main__" and not {"--ledger", "--papers", "--products"} & set(sys.argv):
     main()
 
 
@@ -173,3 +173,82 @@ def ledger_cases() -> dict:
 
 if __name__ == "__main__" and "--ledger" in sys.argv:
     np.savez_compressed(OUT / "ledger_cases.npz", **ledger_cases())
+
+
+def _integer_artifacts(g, ds, res, plan) -> dict:
+    out = {
+        "graph_digest": np.array(digest(g.src_ptr, g.dst_idx)),
+        "num_vertices": np.array(g.num_vertices),
+        "num_edges": np.array(g.num_edges),
+        "sa_labels_digest": np.array(digest(res.labels)),
+        "sa_sizes": np.bincount(res.labels, minlength=plan.num_partitions).astype(np.int64),
+        "sa_objective_trace": np.array(res.objective_trace),
+        "sa_initial_objective": np.array(res.initial_objective),
+        "sa_iterations": np.array(res.iterations),
+        "sa_converged": np.array(res.converged),
+        "sa_max_sizes": np.array(res.max_size_per_iteration),
+        "gather_rows": np.array([t.gather_map.size for t in plan.topologies], dtype=np.int64),
+    }
+    if ds is not None:
+        out["features_digest"] = np.array(digest(ds.features))
+        out["labels_digest"] = np.array(digest(ds.labels, ds.train_mask))
+    for q, t in enumerate(plan.topologies):
+        out[f"plan_digest_{q}"] = np.array(digest(t.targets, t.gather_map, t.tgt_ptr, t.src_pos,
+                                                  t.edge_local_target, t.self_pos, t.target_indeg,
+                                                  t.gather_indeg))
+    return out
+
+
+def papers_small() -> dict:
+    """configs[3]'s model (3-layer GCN, F=H=128, C=172, P=16 switching-aware,
+    CLI seeds 0/1/2/3, lr 0.01) on the largest papers-shaped (average degree
+    12) Kronecker graph the reference finishes here: generate_kronecker(22, 12)."""
+    scale, deg, F, C, L, H, P = PAPERS_SHAPE
+    t0 = time.time()
+    g = generate_kronecker(scale, deg, seed=0)
+    print(f"papers generate {time.time() - t0:.1f}s", flush=True)
+    ds = make_random_dataset(g, feature_dim=F, num_classes=C, seed=1)
+    t0 = time.time()
+    res = switching_aware_partition(g, P, PartitionerParams(seed=2))
+    print(f"papers partition {time.time() - t0:.1f}s", flush=True)
+    t0 = time.time()
+    plan = build_partition_plan(g, res.labels, P)
+    print(f"papers plan {time.time() - t0:.1f}s", flush=True)
+    model = create_model(F, C, num_layers=L, hidden_dim=H, seed=3)
+    out = _integer_artifacts(g, ds, res, plan)
+    del g
+    t0 = time.time()
+    trained, trace, _ = partitioned_train(ds, plan, model, epochs=1, lr=0.01)
+    print(f"papers reference epoch {time.time() - t0:.1f}s", flush=True)
+    out["spec"] = np.array(PAPERS_SHAPE, dtype=np.int64)
+    out["loss"] = np.array(trace[0][1])
+    out["acc"] = np.array(trace[0][2])
+    for i, w in enumerate(trained.weights):
+        out[f"w_final_{i}"] = w
+        out[f"wgrad_{i}"] = trained.weight_grads[i]
+    return out
+
+
+def products_integers() -> dict:
+    """configs[1]/[2]'s graph generate_kronecker(21, 30, 0) with P=8
+    switching-aware partitions (seed 2) and its plan: integer artefacts only
+    (the reference has no GraphSAGE / GAT to train)."""
+    t0 = time.time()
+    g = generate_kronecker(21, 30, seed=0)
+    print(f"products generate {time.time() - t0:.1f}s", flush=True)
+    t0 = time.time()
+    res = switching_aware_partition(g, 8, PartitionerParams(seed=2))
+    print(f"products partition {time.time() - t0:.1f}s", flush=True)
+    t0 = time.time()
+    plan = build_partition_plan(g, res.labels, 8)
+    print(f"products plan {time.time() - t0:.1f}s", flush=True)
+    return _integer_artifacts(g, None, res, plan)
+
+
+# (scale, avg degree, F, C, layers, hidden, partitions)
+PAPERS_SHAPE = (22, 12, 128, 172, 3, 128, 16)
+
+if __name__ == "__main__" and "--papers" in sys.argv:
+    np.savez_compressed(OUT / "papers_s22.npz", **papers_small())
+if __name__ == "__main__" and "--products" in sys.argv:
+    np.savez_compressed(OUT / "products_s21.npz", **products_integers())
