@@ -157,6 +157,14 @@ int grd_direct_read(int32_t fd, int64_t offset, int64_t nbytes, void* dst, int32
 int grd_direct_write(int32_t fd, int64_t offset, int64_t nbytes, const void* src,
                      int32_t num_threads);
 
+/* Row-run I/O of the SSO manager's tier files (hierarchy.py): run i is
+ * records [first[i], first[i] + count[i]) of `record` bytes at file offset
+ * first[i] * record, packed back to back in buf; write != 0 writes buf to
+ * the file, else reads (past the end of the file reads zeros).  Buffered
+ * pread / pwrite spread over num_threads threads by bytes. */
+int grd_file_runs(int32_t fd, int32_t write, int64_t record, const int64_t* first,
+                  const int64_t* count, int64_t nruns, void* buf, int32_t num_threads);
+
 /* ------------------------------------------------------------------------
  * Device kernels (sm_100a).  All take `stream` = cudaStream_t.
  * --------------------------------------------------------------------- */
@@ -166,6 +174,13 @@ int grd_direct_write(int32_t fd, int64_t offset, int64_t nbytes, const void* src
 int grd_gather_rows(const float* src, int64_t ld_src, const int32_t* idx,
                     int64_t n_rows, int32_t width, float* dst, int64_t ld_dst,
                     void* stream);
+
+/* Strided 2-D copy (cudaMemcpy2DAsync, cudaMemcpyDefault) between device
+ * and/or page-locked host memory: `rows` rows of `width_bytes` bytes, row
+ * pitches in bytes.  The SSO tiers keep unpadded rows; device matrices are
+ * padded — the host link moves exactly rows * width_bytes. */
+int grd_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                 int64_t width_bytes, int64_t rows, void* stream);
 
 /* K9 — row scatter-add: dst[idx[i],:] += src[i,:] (training.py:166-175
  * scatter_accumulate; idx is duplicate-free). */

@@ -10,6 +10,9 @@ and bit-exact with the reference.
 
 from .dataset import LabeledDataset, load_dataset, make_random_dataset
 from .graph import CsrGraph, build_csr, generate_kronecker
+from .hierarchy import (CACHE_GRANULARITIES, POLICY_KINDS, HierarchyConfig, IoLedger, PolicySpec,
+                        TierSession, ledger_summary, modeled_time, schedule_partitions,
+                        simulate_epoch)
 from .model import ModelState, create_model, softmax_cross_entropy_loss, train_accuracy
 from .partition import (PartitionerParams, PartitionQuality, PartitionResult, expansion_ratio,
                         partition_objective, random_partition, switching_aware_partition)
@@ -19,7 +22,17 @@ from .training import (TrainSession, compute_gradients, layer_forward, partition
                        write_trace_csv)
 
 __all__ = [
+    "CACHE_GRANULARITIES",
     "CsrGraph",
+    "HierarchyConfig",
+    "IoLedger",
+    "POLICY_KINDS",
+    "PolicySpec",
+    "TierSession",
+    "ledger_summary",
+    "modeled_time",
+    "schedule_partitions",
+    "simulate_epoch",
     "LabeledDataset",
     "ModelState",
     "PartitionPlan",

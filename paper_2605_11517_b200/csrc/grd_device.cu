@@ -830,6 +830,24 @@ extern "C" int grd_gather_rows(const float* src, int64_t ld_src, const int32_t* 
     return launch_status("gather_rows");
 }
 
+// Strided 2-D copy between any two of {device, page-locked host} memory
+// (cudaMemcpyDefault under UVA): `rows` rows of `width_bytes`, pitches in
+// bytes.  The SSO tiers keep rows unpadded (d values) while device matrices
+// are padded to ld = round_up(d, 4); the copy engine moves exactly
+// rows * width_bytes over the host link, the pitch change is free.
+extern "C" int grd_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                            int64_t width_bytes, int64_t rows, void* stream) {
+    clear_error();
+    if (rows == 0 || width_bytes == 0) return 0;
+    if (!dst || !src || width_bytes < 0 || rows < 0 || dpitch < width_bytes || spitch < width_bytes)
+        return fail(kErrArg, "memcpy2d: bad arguments");
+    const cudaError_t e = cudaMemcpy2DAsync(dst, static_cast<size_t>(dpitch), src, static_cast<size_t>(spitch),
+                                            static_cast<size_t>(width_bytes), static_cast<size_t>(rows),
+                                            cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "memcpy2d: %s", cudaGetErrorString(e));
+    return 0;
+}
+
 extern "C" int grd_scatter_add_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n_rows,
                                     int32_t width, float* dst, int64_t ld_dst, void* stream) {
     clear_error();

@@ -15,6 +15,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cerrno>
 #include <cstdint>
 #include <cstring>
@@ -143,5 +144,59 @@ extern "C" int grd_direct_write(int32_t fd, int64_t offset, int64_t nbytes, cons
         return 0;
     });
     if (e) return fail(kErrState, "direct_write: %s", std::strerror(e));
+    return 0;
+}
+
+// Row-run I/O of the SSO manager's tier files (buffered pread / pwrite: runs
+// start at arbitrary record offsets).  Run i covers records
+// [first[i], first[i] + count[i]) of `record` bytes each, at file offset
+// first[i] * record; the runs are packed back to back in `buf`.  Threads
+// take whole runs (contiguous ranges of the run list, balanced by bytes).
+extern "C" int grd_file_runs(int32_t fd, int32_t write, int64_t record, const int64_t* first,
+                             const int64_t* count, int64_t nruns, void* buf, int32_t num_threads) {
+    clear_error();
+    if (nruns == 0) return 0;
+    if (fd < 0 || record <= 0 || !first || !count || !buf || nruns < 0)
+        return fail(kErrArg, "file_runs: bad arguments");
+    std::vector<int64_t> at(static_cast<size_t>(nruns) + 1, 0);
+    for (int64_t i = 0; i < nruns; ++i) {
+        if (first[i] < 0 || count[i] < 0) return fail(kErrArg, "file_runs: negative run");
+        at[i + 1] = at[i] + count[i] * record;
+    }
+    const int64_t total = at[nruns];
+    int nt = num_threads > 0 ? num_threads : 1;
+    if (total < (int64_t{4} << 20)) nt = 1;
+    char* base = static_cast<char*>(buf);
+    std::vector<int> err(static_cast<size_t>(nt), 0);
+    auto worker = [&](int t) {
+        // runs whose packed start falls in this thread's byte share
+        const int64_t lo = total * t / nt, hi = total * (t + 1) / nt;
+        int64_t i = std::lower_bound(at.begin(), at.end() - 1, lo) - at.begin();
+        for (; i < nruns && at[i] < hi && !err[t]; ++i) {
+            const int64_t len = at[i + 1] - at[i];
+            const off_t off = static_cast<off_t>(first[i] * record);
+            int64_t done = 0;
+            while (done < len) {
+                const ssize_t r = write ? ::pwrite(fd, base + at[i] + done, static_cast<size_t>(len - done), off + done)
+                                        : ::pread(fd, base + at[i] + done, static_cast<size_t>(len - done), off + done);
+                if (r < 0) {
+                    if (errno == EINTR) continue;
+                    err[t] = errno;
+                    break;
+                }
+                if (r == 0) {   // read past the end of the file: zeros
+                    std::memset(base + at[i] + done, 0, static_cast<size_t>(len - done));
+                    break;
+                }
+                done += r;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (auto& th : pool) th.join();
+    for (int e : err)
+        if (e) return fail(kErrState, "file_runs: %s", std::strerror(e));
     return 0;
 }

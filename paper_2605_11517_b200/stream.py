@@ -418,7 +418,8 @@ class StreamingEngine:
         d = self.dc[:n, : c.ld_in]
         ops.gemm(Hc, self.wts.w[l], d, n, c.d_in, c.d_out, trans_b=True,
                  row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
-        out[r0:r1, : c.ld_in].copy_(d)    # dA_l rows replace H rows (consumed)
+        # dA_l rows replace the (consumed) H rows: row copy kernel (K1, identity rows)
+        ops.gather_rows(d, self.sg.self_ids[:n], out[r0:r1], c.ld_in)
 
     def _backward_first(self, D: torch.Tensor, s) -> None:
         """Layer 0: dW_0 = X^T (A_hat^T D), chunk by chunk with X streamed."""
@@ -510,7 +511,7 @@ class StreamingEngine:
         if l > 0:
             d = self.dc[:n, : c.ld_in]
             ops.gemm(gc, self.wts.w[l], d, n, c.d_in, 2 * c.ld_out, trans_b=True, relu_ref=a)
-            self.buf[0][r0:r1, : c.ld_in].copy_(d)
+            ops.gather_rows(d, self.sg.self_ids[:n], self.buf[0][r0:r1], c.ld_in)
 
     def _epoch_sage(self, lr: float) -> None:
         sg, cfg, L, V = self.sg, self.cfg, self.L, self.V

@@ -135,7 +135,7 @@ def main() -> None:
         print(f, (OUT / f).stat().st_size, "bytes")
 
 
-if __name__ == "__main__" and not {"--ledger", "--papers", "--products"} & set(sys.argv):
+if __name__ == "__main__" and not {"--ledger", "--ledger4", "--papers", "--products"} & set(sys.argv):
     main()
 
 
@@ -159,6 +159,12 @@ def ledger_cases() -> dict:
         "no_bypass": dict(host_capacity=3 * n * 6 * 8, bytes_per_value=8),
         "tight": dict(host_capacity=n * 6 * 8 + 100, bytes_per_value=8),
     }
+    if FP32_LEDGERS:
+        # every case at 4 bytes per value: what an executing (fp32) session
+        # moves, so its recorded ledger is compared with the reference's
+        cases["no_bypass"] = dict(host_capacity=3 * n * 6 * 4, bytes_per_value=4)
+        cases["tight"] = dict(host_capacity=n * 6 * 4 + 100, bytes_per_value=4)
+        cases["tiny_pages"] = dict(host_capacity=0, bytes_per_value=4, page_size=16)
     for name, kw in cases.items():
         bypass = name != "no_bypass"
         from grinder.hierarchy import PolicySpec
@@ -171,8 +177,12 @@ def ledger_cases() -> dict:
     return out
 
 
+FP32_LEDGERS = "--ledger4" in sys.argv
+
 if __name__ == "__main__" and "--ledger" in sys.argv:
     np.savez_compressed(OUT / "ledger_cases.npz", **ledger_cases())
+if __name__ == "__main__" and "--ledger4" in sys.argv:
+    np.savez_compressed(OUT / "ledger_cases_fp32.npz", **ledger_cases())
 
 
 def _integer_artifacts(g, ds, res, plan) -> dict:

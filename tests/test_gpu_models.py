@@ -131,3 +131,30 @@ def test_gat_kept_vs_regathered(keep, monkeypatch):
     assert abs(tr[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
     for a, b in zip(one.weight_grads, grads):
         assert rel_l2(a, b) < TOL
+
+
+@pytest.mark.parametrize("mode,keep", [("sage_mean", "1"), ("sage_mean", "0"), ("gat", "1"),
+                                       ("gat", "0")])
+def test_baseline_widths_match_oracle(mode, keep, monkeypatch):
+    """configs[1] / configs[2] at their real widths (F = 100, hidden 256 —
+    GAT 4 heads x 64 concatenated, mean over heads on the last layer —
+    C = 47, L = 3, P = 8 switching-aware partitions) on a scale-14
+    average-degree-30 Kronecker graph (the products degree), kept forward
+    state and regather backward: one epoch's loss, weight gradients and
+    trained weights against the float64 oracle."""
+    monkeypatch.setenv("GRD_KEEP_AGG", keep)
+    monkeypatch.setenv("GRD_GAT_KEEP", keep)
+    g, ds, plan, model = _setup(14, 30, 100, 47, 3, 256, 8, mode)
+    trained, trace, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.01)
+    if mode == "gat":
+        W, grads, ref = sage_gat.train_gat(ds.features, ds.labels, ds.train_mask, g.src_ptr,
+                                           g.dst_idx, model.weights, 4, 1, 0.01)
+    else:
+        W, grads, ref = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr,
+                                            g.dst_idx, model.weights, 1, 0.01)
+    assert abs(trace[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
+    for a, b in zip(trained.weight_grads, grads):
+        assert a.shape == b.shape and rel_l2(a, b) < TOL
+    for a, b in zip(trained.weights, W):
+        assert rel_l2(a, b) < TOL
+    plan.device_cache.clear()

@@ -73,3 +73,51 @@ def test_policy_and_config_validation():
         TierSession(plan, [2, 2], "NAIVE", HierarchyConfig())
     with pytest.raises(ValueError):
         TierSession(plan, [2], "GRINNDER", HierarchyConfig())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_manager_dry_run_equals_oracle_byte_model(seed):
+    """The manager's non-executing run and the oracle's restatement of the
+    reference byte model (oracle/ledger.py) agree on random plans, widths,
+    host capacities, page sizes and bypass settings."""
+    from oracle import ledger as oled
+    rng = np.random.default_rng(seed)
+    g = g2.generate_kronecker(int(rng.integers(6, 9)), int(rng.integers(3, 9)), seed=seed)
+    P = int(rng.integers(1, 6))
+    plan = g2.build_partition_plan(g, g2.random_partition(g.num_vertices, P, seed), P)
+    dims = [int(x) for x in rng.integers(1, 9, size=int(rng.integers(2, 5)))]
+    n = g.num_vertices
+    kw = dict(host_capacity=int(rng.choice([0, 64, n * 4, n * 4 * max(dims) * 3])),
+              bytes_per_value=int(rng.choice([4, 8])), page_size=int(rng.choice([16, 64, 4096])))
+    bypass = bool(rng.integers(0, 2))
+    ours = simulate_epoch(plan, dims, PolicySpec("GRINNDER", bypass_enabled=bypass),
+                          HierarchyConfig(**kw), epochs=2)
+    ref = oled.simulate_epoch(plan, dims, oled.PolicySpec("GRINNDER", bypass_enabled=bypass),
+                              oled.HierarchyConfig(**kw), epochs=2)
+    assert ours.events == ref.events
+    assert ledger_summary(ours) == oled.ledger_summary(ref)
+    assert ours.stage_table(2) == ref.stage_table(2)
+
+
+def test_storage_tier_row_runs_round_trip(tmp_path):
+    """grd_file_runs: packed row runs written at record offsets read back
+    bit for bit (and untouched regions of the file read as zeros)."""
+    import torch
+    from paper_2605_11517_b200.hierarchy import StorageTier
+    levels = []
+    st = StorageTier(1 << 30, str(tmp_path), True, levels.append)
+    rows = torch.arange(7 * 5, dtype=torch.float32).reshape(7, 5)
+    first, count = np.array([2, 10, 11 + 1]), np.array([3, 1, 3])
+    st.io(("act", 1), True, 5 * 4, first, count, rows, create=True)
+    st.grow(("act", 1), rows.numel() * 4)
+    back = torch.empty_like(rows)
+    st.io(("act", 1), False, 5 * 4, first, count, back)
+    assert torch.equal(back, rows)
+    whole = torch.empty((15, 5), dtype=torch.float32)
+    st.io(("act", 1), False, 5 * 4 * 15, [0], [1], whole)
+    assert torch.equal(whole[2:5], rows[:3]) and torch.equal(whole[10], rows[3])
+    assert not whole[5:10].any()
+    assert levels[-1] == rows.numel() * 4
+    st.delete(("act", 1))
+    assert st.level == 0 and not (tmp_path / "act_1.bin").exists()
+    st.close()
