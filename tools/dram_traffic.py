@@ -35,7 +35,11 @@ def main():
         per_launch[(r["ID"], r["Kernel Name"])][r["Metric Name"]] = v
     ops = collections.OrderedDict()
     for (_, name), m in per_launch.items():
+        # renamed kernels read "<op>#<call>/<kernel signature>"
         op, _, call = name.partition("#")
+        call = call.split("/", 1)[0]
+        if not call:                  # a kernel outside any op range
+            op = "(outside ops) " + name.split("(")[0][:60]
         o = ops.setdefault(op, dict(calls=set(), kernels=0, dram=0.0, s=0.0))
         o["calls"].add(call)
         o["kernels"] += 1
