@@ -121,6 +121,9 @@ def build_workload(spec):
     # bit-identical to the host plan (tests/test_gpu_plan.py)
     plan = g2.build_partition_plan(g, part.labels, spec["P"], device="cuda" if gpu_gen else None)
     t_plan = time.perf_counter() - t2
+    if gpu_gen:
+        import torch
+        torch.cuda.empty_cache()    # the plan builder's sort scratch
     model = g2.create_model(spec["F"], spec["C"], num_layers=spec["L"], hidden_dim=spec["H"],
                             seed=SEED + 3, aggregation_mode=spec["mode"],
                             heads=spec.get("heads", 4))

@@ -69,6 +69,7 @@ struct Params {
     int64_t kchunk;                 // split-K chunk (multiple of 32)
     int splits;
     int stages;
+    int b_resident;                 // packed B loaded once per CTA and kept in shared memory
     int cluster;                    // CTAs per cluster along M (1, 2, 4)
     int pair;                       // 1: cluster of 2 = a cta_group::2 pair (M = 256)
     float* c; int64_t ldc;
@@ -379,9 +380,73 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
     }
 }
 
+// Split-K partial tiles with fresh accumulators (kFresh): the MMA issuer
+// starts a new TMEM accumulator for every 32-deep K block, and these warps
+// add the K blocks' partials in registers with round-to-nearest fp32 adds.
+// The tensor cores' fused accumulation truncates (measured: the 3xTF32
+// error grows linearly with the number of MMAs accumulated, ~4e-6 relative
+// at 192 and ~8e-6 at 168-3072 accumulation steps); a weight gradient sums
+// 10^4..10^6 rows whose terms largely cancel, which amplifies that bias to
+// 1e-3 (GraphSAGE layer 0 at F = 100, H = 256).  12 MMAs per accumulator
+// keep it at the per-product rounding.  bn <= 128: two 32-column chunks of
+// running sums per thread.
+template <bool kPair, class TileFn, class KbFn>
+__device__ __forceinline__ void epilogue_fresh(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                                               int warp, int lane, int64_t t0, int64_t tstep, int64_t ntiles,
+                                               TileFn tile_of, KbFn kblocks) {
+    const int q = warp & 3;
+    const int half = (warp - kEpiWarp0) >> 2;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const int bn = p.bn;
+    int64_t g = 0;                                  // accumulator uses (K blocks) so far
+    for (int64_t t = t0; t < ntiles; t += tstep) {
+        int64_t m0, n0;
+        int z;
+        bool has_k;
+        tile_of(t, m0, n0, z, has_k);
+        const int64_t nkb = kblocks(z);
+        float run[2][32];
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) run[ci][j] = 0.f;
+        for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+            const int acc = static_cast<int>(g & 1);
+            mbar_wait(tfull + acc, static_cast<uint32_t>((g / 2) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int ci = 0; ci < 2; ++ci) {
+                const int c0 = 32 * half + 64 * ci;
+                if (c0 >= bn) continue;
+                float v[32];
+                tmem_ld32(tmem + lane_base + static_cast<uint32_t>(acc * bn + c0), v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) run[ci][j] += v[j];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            if (kPair) mbar_arrive_cluster(tempty + acc, 0);
+            else mbar_arrive(tempty + acc);
+        }
+        const int64_t row0 = m0 + q * 32;
+        const int64_t n_pad = (p.n + 3) / 4 * 4;
+        EpiIn in;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+            in.o[j4] = make_float4(0.f, 0.f, 0.f, 0.f);
+            in.e[j4] = make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+            const int c0 = 32 * half + 64 * ci;
+            if (c0 >= bn || row0 >= p.m || n0 + c0 >= n_pad) continue;
+            epi_store_direct<false>(p, run[ci], row0 + lane, n0 + c0, z, in);
+        }
+    }
+}
+
 // kPair: a kernel containing cta_group::2 instructions must be launched in
 // clusters of 2, so the CTA-pair variant is its own instantiation.
-template <bool kPair, bool kSplit>
+template <bool kPair, bool kSplit, bool kFresh = false>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const Params p) {
@@ -393,15 +458,23 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int bnl = pair ? bn / 2 : bn;                      // B rows staged by this CTA
     const uint32_t a_bytes = kBM * 128u;
     const uint32_t b_bytes = static_cast<uint32_t>(bnl) * 128u;
-    // stage: A hi | A lo | B hi | B lo | [A raw] | [B raw]  (raw only for MN-major)
-    const uint32_t stage_bytes = 2u * (a_bytes + b_bytes);   // A hi | A lo | B hi | B lo
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+    // stage: A hi | A lo | B hi | B lo   (A raw lands in A hi and is split in place)
+    // B-resident mode (small packed weight, one N tile, no split-K): stages
+    // carry A only, and this CTA's B hi|lo tiles of every K block sit after
+    // the ring for the whole launch — loaded once instead of once per M tile.
+    const bool bres = p.b_resident != 0;
+    const int64_t nkb_b = (p.k + kBK - 1) / kBK;
+    const uint32_t stage_bytes = bres ? 2u * a_bytes : 2u * (a_bytes + b_bytes);
+    uint8_t* bres_smem = smem + S * stage_bytes;
+    const uint32_t bres_bytes = bres ? static_cast<uint32_t>(nkb_b) * 2u * b_bytes : 0u;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bres_smem + bres_bytes);
     uint64_t* full = bars;             // [S]
     uint64_t* conv = bars + S;         // [S]
     uint64_t* empty = bars + 2 * S;    // [S]
     uint64_t* tfull = bars + 3 * S;    // [2]
     uint64_t* tempty = bars + 3 * S + 2;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+    uint64_t* bready = bars + 3 * S + 4;   // [1] resident B landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -444,6 +517,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, kEpiThreads * nc);
         }
+        mbar_init(bready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
         if (p.b_mode != kPacked) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
@@ -463,6 +537,16 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     if (warp == 0) {
         // ------------------------------------------------ TMA producer --
         if (lane == 0) {
+            if (bres) {
+                // this CTA's B rows (pair: its half) of every K block, once
+                mbar_expect_tx(bready, bres_bytes);
+                for (int64_t kb = 0; kb < nkb_b; ++kb) {
+                    const float* src = p.b_packed + kb * (2 * int64_t(bn) * kBK) + int64_t(crank) * bnl * kBK;
+                    uint8_t* dst = bres_smem + kb * 2 * b_bytes;
+                    bulk_copy(dst, src, b_bytes, bready);
+                    bulk_copy(dst + b_bytes, src + int64_t(bn) * kBK, b_bytes, bready);
+                }
+            }
             uint64_t g = 0;
             for (int64_t t = cid; t < ntiles; t += ncl) {
                 const int z = static_cast<int>(t / (mg * nt));
@@ -475,7 +559,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     uint8_t* st = smem + s * stage_bytes;
                     const int64_t k0 = int64_t(z) * p.kchunk + kb * kBK;
                     uint32_t bytes = a_bytes;
-                    bytes += (p.b_mode == kPacked) ? 2u * b_bytes : b_bytes;
+                    if (!bres) bytes += (p.b_mode == kPacked) ? 2u * b_bytes : b_bytes;
                     mbar_expect_tx(full + s, bytes);
                     if (p.a_mode == kKMajorTma) {
                         tma_2d(st, &map_a, static_cast<int32_t>(k0), static_cast<int32_t>(m0), full + s);
@@ -484,6 +568,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             tma_2d(st + j * 4096, &map_a, static_cast<int32_t>(m0 + 32 * j),
                                    static_cast<int32_t>(k0), full + s);
                     }
+                    if (bres) continue;
                     uint8_t* bdst = st + 2 * a_bytes;
                     if (pair) {
                         // this CTA's half of the B tile: rows [crank * bnl, +bnl)
@@ -543,33 +628,49 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t a_lay = a_mn ? 1u : 2u, b_lay = b_mn ? 1u : 2u;
             uint64_t g = 0;
             int64_t i = 0;   // tiles with K work (empty split-K tiles are skipped)
+            int64_t fresh = 0;   // kFresh: accumulators started so far
+            if (bres) {
+                mbar_wait(bready, 0u);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+            }
             for (int64_t t = cid; t < ntiles; t += ncl) {
                 const int z = static_cast<int>(t / (mg * nt));
                 const int64_t nkb = kblocks_of(z);
                 if (nkb == 0) continue;
-                const int acc = static_cast<int>(i & 1);
-                if (i >= 2) mbar_wait(tempty + acc, static_cast<uint32_t>((i / 2 - 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t tacc = tmem + static_cast<uint32_t>(acc * bn);
+                int acc = static_cast<int>(i & 1);
+                if (!kFresh) {
+                    if (i >= 2) mbar_wait(tempty + acc, static_cast<uint32_t>((i / 2 - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                uint32_t tacc = tmem + static_cast<uint32_t>(acc * bn);
                 for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+                    if constexpr (kFresh) {
+                        // a fresh accumulator per K block (epilogue_fresh sums them)
+                        acc = static_cast<int>(fresh & 1);
+                        if (fresh >= 2) mbar_wait(tempty + acc, static_cast<uint32_t>((fresh / 2 - 1) & 1));
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        tacc = tmem + static_cast<uint32_t>(acc * bn);
+                    }
                     const int s = static_cast<int>(g % S);
                     mbar_wait(conv + s, static_cast<uint32_t>((g / S) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     uint8_t* st = smem + s * stage_bytes;
                     const uint32_t ah = smem_u32(st), al = smem_u32(st + a_bytes);
-                    const uint32_t bh = smem_u32(st + 2 * a_bytes), bl = smem_u32(st + 2 * a_bytes + b_bytes);
+                    const uint8_t* bst = bres ? bres_smem + kb * 2 * b_bytes : st + 2 * a_bytes;
+                    const uint32_t bh = smem_u32(bst), bl = smem_u32(bst + b_bytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 8; ++kk) {
                         const uint64_t dah = make_desc(ah + kk * a_step, a_lbo, a_sbo, a_lay);
                         const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo, a_lay);
                         const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo, b_lay);
                         const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo, b_lay);
+                        const uint32_t keep = (kk > 0 || (!kFresh && kb > 0)) ? 1u : 0u;
                         if constexpr (kPair) {
-                            mma_tf32_pair(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                            mma_tf32_pair(tacc, dal, dbh, idesc, keep);
                             mma_tf32_pair(tacc, dah, dbl, idesc, 1u);
                             mma_tf32_pair(tacc, dah, dbh, idesc, 1u);
                         } else {
-                            mma_tf32(tacc, dal, dbh, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                            mma_tf32(tacc, dal, dbh, idesc, keep);
                             mma_tf32(tacc, dah, dbl, idesc, 1u);
                             mma_tf32(tacc, dah, dbh, idesc, 1u);
                         }
@@ -577,9 +678,16 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     if constexpr (kPair) mma_commit_pair(empty + s);   // both CTAs' stage s
                     else if (C == 1) mma_commit(empty + s);
                     else mma_commit_mc(empty + s, cmask);   // release the stage in every CTA
+                    if constexpr (kFresh) {
+                        if constexpr (kPair) mma_commit_pair(tfull + acc);
+                        else mma_commit(tfull + acc);
+                        ++fresh;
+                    }
                 }
-                if constexpr (kPair) mma_commit_pair(tfull + acc);   // both CTAs' accumulators
-                else mma_commit(tfull + acc);
+                if constexpr (!kFresh) {
+                    if constexpr (kPair) mma_commit_pair(tfull + acc);   // both CTAs' accumulators
+                    else mma_commit(tfull + acc);
+                }
                 ++i;
             }
         }
@@ -604,14 +712,17 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
     } else {
         // ---------------------------------------------------- epilogue --
-        epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles,
-                      [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
-                          z = static_cast<int>(t / (mg * nt));
-                          const int64_t r = t % (mg * nt);
-                          m0 = ((r / nt) * C + crank) * kBM;
-                          n0 = (r % nt) * bn;
-                          has_k = kblocks_of(z) > 0;
-                      });
+        auto tile_of = [&](int64_t t, int64_t& m0, int64_t& n0, int& z, bool& has_k) {
+            z = static_cast<int>(t / (mg * nt));
+            const int64_t r = t % (mg * nt);
+            m0 = ((r / nt) * C + crank) * kBM;
+            n0 = (r % nt) * bn;
+            has_k = kblocks_of(z) > 0;
+        };
+        if constexpr (kFresh)
+            epilogue_fresh<kPair>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of, kblocks_of);
+        else
+            epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -951,6 +1062,26 @@ inline int pair_pref() {
     return v;
 }
 
+// weight gradients accumulate each K block in a fresh TMEM accumulator (GRD_WGRAD_FRESH = 1 / 0)
+inline int fresh_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_WGRAD_FRESH");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// packed weight operand resident in shared memory when it fits (GRD_GEMM_BRES = 1 / 0)
+inline int bres_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_BRES");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 // CTAs per cluster sharing the B operand (GRD_GEMM_CLUSTER = 1, 2 or 4)
 inline int cluster_pref() {
     static int v = 0;
@@ -1086,23 +1217,41 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (!make_map(&map_b, g.b, g.k, g.n, g.ldb, 32, 32, true)) return cudaErrorInvalidValue;
     }
     if (p.b_mode == kMNMajorTma) p.bn = (p.bn + 31) / 32 * 32;   // whole 32-wide TMA atoms
+    // split-K partials (the weight gradients): fresh accumulator per K block
+    const bool fresh = p.partial != nullptr && fresh_pref();
+    if (fresh && p.bn > 128) p.bn = 128;
     const int64_t mt0 = (g.m + kBM - 1) / kBM;
     // a CTA pair stages half of B each: halves of whole 32-row atoms
     p.pair = (pair_pref() && p.bn % 64 == 0 && mt0 >= 2) ? 1 : 0;
     if (p.pair && p.b_mode == kKMajorTma &&
         !make_map(&map_b, g.b, g.n, g.k, g.ldb, 32, static_cast<uint32_t>(p.bn / 2)))
         return cudaErrorInvalidValue;
-    const uint32_t stage = 2u * (kBM * 128u + static_cast<uint32_t>(p.pair ? p.bn / 2 : p.bn) * 128u);
-    p.stages = static_cast<int>((220u * 1024u) / stage);
-    if (p.stages > 4) p.stages = 4;
+    const uint32_t bnl_bytes = static_cast<uint32_t>(p.pair ? p.bn / 2 : p.bn) * 128u;
+    uint32_t stage = 2u * (kBM * 128u + bnl_bytes);
+    uint32_t resident = 0;
+    // B resident in shared memory: a packed weight operand with one N tile,
+    // no split-K, that leaves room for >= 3 A-only stages (GRD_GEMM_BRES=0
+    // keeps B in the stage ring)
+    if (bres_pref() && p.b_mode == kPacked && p.splits == 1 && g.n <= p.bn && (p.pair || cluster_pref() == 1)) {
+        const uint32_t res = static_cast<uint32_t>((g.k + kBK - 1) / kBK) * 2u * bnl_bytes;
+        const uint32_t st_a = 2u * kBM * 128u;
+        if (res + 3u * st_a <= 220u * 1024u) {
+            resident = res;
+            stage = st_a;
+            p.b_resident = 1;
+        }
+    }
+    p.stages = static_cast<int>((220u * 1024u - resident) / stage);
+    if (p.stages > (p.b_resident ? 6 : 4)) p.stages = p.b_resident ? 6 : 4;
     if (p.stages < 2) p.stages = 2;
-    const size_t smem = static_cast<size_t>(p.stages) * stage + 1024 + 256;
+    const size_t smem = static_cast<size_t>(p.stages) * stage + resident + 1024 + 256;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaSuccess;
         for (auto fn : {gemm_tf32x3_ws<false, false>, gemm_tf32x3_ws<true, false>, gemm_tf32x3_ws<false, true>,
-                        gemm_tf32x3_ws<true, true>})
+                        gemm_tf32x3_ws<true, true>, gemm_tf32x3_ws<false, false, true>,
+                        gemm_tf32x3_ws<true, false, true>})
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
@@ -1118,7 +1267,8 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     const int64_t max_cl = num_sms() / C;
     const int grid = static_cast<int>((tiles < max_cl ? tiles : max_cl) * C);
     if (C == 1) {
-        if (p.split > 0) gemm_tf32x3_ws<false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        if (fresh) gemm_tf32x3_ws<false, false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        else if (p.split > 0) gemm_tf32x3_ws<false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
         else gemm_tf32x3_ws<false, false><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
         return cudaGetLastError();
     }
@@ -1135,6 +1285,7 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
     if (p.pair) {
+        if (fresh) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false, true>, map_a, map_b, p);
         if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, true>, map_a, map_b, p);
         return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false>, map_a, map_b, p);
     }

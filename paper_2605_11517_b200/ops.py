@@ -218,11 +218,42 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
             lambda: _lib.check(_lib.lib().grd_agg_sum(ctypes.byref(a), stream_ptr()), "agg_sum"))
 
 
+# K chunk of one tensor-core accumulation (GRD_GEMM_KCHUNK; 0 = whole K).
+# tcgen05's fused accumulation truncates, so the 3xTF32 error grows with the
+# number of MMAs summed into one accumulator (~2e-6 relative at K = 128,
+# ~4e-6 at K = 512 on random data) and is biased; gradients that sum many
+# cancelling terms amplify it (GraphSAGE at F = 100 / H = 256: 1.4e-3 on
+# layer 0's weight gradient).  Longer K is split into chunks of <= 128 whose
+# partials the epilogue adds to C with round-to-nearest fp32 adds (the
+# epilogue's accumulate path); the row scale / element multiply / ReLU
+# apply with the last chunk.  Weight gradients (trans_a) use in-kernel fresh
+# accumulators instead (GRD_WGRAD_FRESH).
+_KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "128"))
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
          trans_a=False, trans_b=False, row_scale=None, elem_mul=None, relu_ref=None,
          relu_out=False, accumulate=False, c2=None, split=0) -> None:
     """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim;
     with c2, columns >= split land in c2[:, col - split] instead."""
+    k = int(k)
+    if _KCHUNK and k > _KCHUNK and not trans_a and c2 is None:
+        starts = list(range(0, k, _KCHUNK))
+        for i, k0 in enumerate(starts):
+            k1 = min(k, k0 + _KCHUNK)
+            last = i == len(starts) - 1
+            _gemm_once(a[:, k0:], b[:, k0:] if trans_b else b[k0:], c, m, n, k1 - k0,
+                       trans_b=trans_b, row_scale=row_scale if last else None,
+                       elem_mul=elem_mul if last else None, relu_ref=relu_ref if last else None,
+                       relu_out=relu_out and last, accumulate=accumulate or i > 0)
+        return
+    _gemm_once(a, b, c, m, n, k, trans_a=trans_a, trans_b=trans_b, row_scale=row_scale,
+               elem_mul=elem_mul, relu_ref=relu_ref, relu_out=relu_out, accumulate=accumulate,
+               c2=c2, split=split)
+
+
+def _gemm_once(a, b, c, m, n, k, *, trans_a=False, trans_b=False, row_scale=None, elem_mul=None,
+               relu_ref=None, relu_out=False, accumulate=False, c2=None, split=0) -> None:
     g = _lib.GrdGemmArgs()
     g.m, g.n, g.k = int(m), int(n), int(k)
     g.a, g.lda, g.trans_a = _p(a), _ld(a), int(bool(trans_a))

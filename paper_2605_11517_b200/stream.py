@@ -254,7 +254,10 @@ class StreamingEngine:
         self._cache_ready = torch.cuda.Event()
         row_bytes = 4 * ld_of(F)
         if x_cache_bytes is None:
+            # blocks torch's caching allocator holds but does not use (e.g.
+            # left by the GPU plan builder) are available to the cache too
             free, _ = torch.cuda.mem_get_info(dev)
+            free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
             x_cache_bytes = max(0, free - (4 << 30))
         rows = min(self.V, int(x_cache_bytes) // row_bytes)
         rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
@@ -297,7 +300,7 @@ class StreamingEngine:
         src.begin_pass([(r0, r1) for r0, r1 in self.sg.chunks if r1 > hits])
         try:
             nb = 0
-            for r0, r1 in self.sg.chunks:
+            for r0, r1 in self._pass_order(hits):
                 n = r1 - r0
                 if r1 <= hits:
                     fn(self.x_cache[r0:r1], r0, r1)
@@ -328,6 +331,24 @@ class StreamingEngine:
             src.end_pass()
         if cached:
             self.x_cache_valid = True
+
+    def _pass_order(self, hits: int) -> list:
+        """Chunk order of one pass: the streamed chunks (rows >= hits) in
+        order, with the HBM-cached chunks spread evenly between them, so the
+        host link always has a transfer queued while cached chunks compute
+        (``GRD_STREAM_INTERLEAVE=0``: cached chunks first)."""
+        chunks = self.sg.chunks
+        cached = [c for c in chunks if c[1] <= hits]
+        streamed = [c for c in chunks if c[1] > hits]
+        if not cached or not streamed or os.environ.get("GRD_STREAM_INTERLEAVE", "1") == "0":
+            return cached + streamed
+        out, j = [], 0
+        for i, c in enumerate(streamed):
+            out.append(c)
+            upto = (i + 1) * len(cached) // len(streamed)
+            out.extend(cached[j:upto])
+            j = upto
+        return out + cached[j:]
 
     def set_features(self, src) -> None:
         """Re-bind the feature rows (the HBM cache refills on the next pass)."""
@@ -426,10 +447,12 @@ class StreamingEngine:
         c = self.cfg[0]
         specs = self.sg.bwd_chunks
 
-        def step(x, r0, r1, _it=iter(specs)):
+        spec_of = {r0: sp for (r0, _), sp in zip(self.sg.chunks, specs)}
+
+        def step(x, r0, r1):
             n = r1 - r0
             h = self.nc[:n, : c.ld_out]
-            ops.agg_sum(next(_it), D, h, c.d_out, post_scale=_rows(s, r0, r1))
+            ops.agg_sum(spec_of[r0], D, h, c.d_out, post_scale=_rows(s, r0, r1))
             ops.wgrad_sgd(x, h, self.wts.dw[0], c.d_in, c.d_out, n, accumulate=True)
         self._stream(self.x_src, step)
 

@@ -17,6 +17,7 @@
 
 from __future__ import annotations
 
+import json
 import os
 
 import numpy as np
@@ -25,7 +26,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-from conftest import rel_l2  # noqa: E402
+from conftest import GOLDEN, rel_l2  # noqa: E402
 from test_golden_scale import digest, load, plan_digest  # noqa: E402
 import paper_2605_11517_b200 as g2  # noqa: E402
 
@@ -66,11 +67,23 @@ def test_gpu_generator_and_plan_match_reference_products():
         assert plan_digest(plan.topology(q)) == str(gold[f"plan_digest_{q}"]), f"partition {q}"
 
 
+# fp32 floor of this case (tests/golden/fp32_floor.py): a correctly rounded
+# float32 epoch is 2.3e-4 from float64 on layer 0's weight gradient (2^21
+# cancelling random-feature outer products); that tensor is bounded by 3x
+# the floor, every other tensor by the 1e-4 bar.
+FLOOR = json.loads((GOLDEN / "papers_s22_fp32_floor.json").read_text())
+
+
+def _bound(name: str) -> float:
+    return max(TOL, 3.0 * FLOOR.get(name, 0.0))
+
+
 def _check(gold, trained, trace):
     loss = float(trace[0][1])
     assert abs(loss - float(gold["loss"])) <= TOL * abs(float(gold["loss"]))
     for i, (w, dw) in enumerate(zip(trained.weights, trained.weight_grads)):
-        assert rel_l2(dw, gold[f"wgrad_{i}"]) < TOL, f"grad W{i}"
+        err = rel_l2(dw, gold[f"wgrad_{i}"])
+        assert err < _bound(f"wgrad_{i}"), f"grad W{i}: {err:.3e} (fp32 floor {FLOOR.get(f'wgrad_{i}')})"
         assert rel_l2(w, gold[f"w_final_{i}"]) < TOL, f"W{i}"
 
 
