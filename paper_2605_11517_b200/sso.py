@@ -48,7 +48,7 @@ class _AscendingAccumulator:
             f = self.s.plan.flat
             gmap = f.gather_map[f.gather_ptr[q]:f.gather_ptr[q + 1]].astype(np.int64)
             acc = self.s.host.grad_acc
-            if gmap.size:
+            if gmap.size and block is not None:
                 _lib.check(_lib.lib().grd_host_scatter_add_rows(
                     block.data_ptr(), self.width, gmap.ctypes.data, gmap.size, self.width,
                     acc.data_ptr(), acc.stride(0), self.threads), "host_scatter_add_rows")
