@@ -12,14 +12,19 @@ Per layer the engine exchanges only the rows an aggregation actually reads:
 forward, the transformed rows ``P = X W`` (transform-first) or the layer
 input (aggregate-first); backward, the pre-scaled gradient rows for the
 transposed pull.  Exchanges are one ``all_to_all_single`` each (packed by
-a gather kernel, received straight into the contiguous halo block).  GAT's
+a gather kernel, received in place into the contiguous halo block).  GAT's
 transposed pull needs per-edge attention that only the target's owner
 holds, so it runs over the transpose of the local in-CSR instead: halo rows
 collect partial sums that a reverse all-to-all returns to their owners,
 added in ascending source-rank order (``ShardDeviceGraph.reverse_add``).  The
-weight gradients of all layers are summed with one bucketed ``all_reduce``
+weight gradients of all layers live in one flat buffer
+(``engine._Weights.grad_bucket``) and are summed with one ``all_reduce``
 before the replicated SGD step, and the loss/accuracy partial sums with a
-second one.  Owner-side accumulation replaces the paper's host atomics, so
+second one.  Halo rows are received in place into the halo block when the
+exchanged buffer's rows are exactly ld(width) wide (else through a scratch
+buffer and one unpack kernel).  Choices that change which exchanges a rank
+issues (keeping the forward state instead of regathering) are agreed by an
+all-reduce MIN, so every rank runs the same collective sequence.  Owner-side accumulation replaces the paper's host atomics, so
 results are deterministic for a fixed world size.
 
 Transports: ``nccl`` (CUDA tensors over NVLink/NVSwitch) in production;

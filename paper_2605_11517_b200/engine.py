@@ -609,19 +609,6 @@ class LayerwiseEngine(_EngineBase):
             wide = max([self.maxw] + [c.ld_ext for c in self.cfg])
             self._gat_buffers(dg, model)
         self.t1 = ops.zeros_rows(self.NL, wide, dev)
-        # aggregate-first GCN layers: the forward's normalised aggregate N is
-        # kept for the backward's dW = N^T gp when it fits, instead of the
-        # reference's regather (GRD_KEEP_AGG=0 regathers)
-        self.keep_on = os.environ.get("GRD_KEEP_AGG", "1") != "0"
-        self.n_kept = {}
-        if self.keep_on:
-            hidden = [l for l, c in enumerate(self.cfg)
-                      if not (c.transform_first or c.sage or c.gat or c.rownorm or c.last)]
-            need = sum(self.NL * ld_of(self.cfg[l].d_in) * 4 for l in hidden)
-            if hidden and self._keep_fits(need):
-                self.n_kept = {l: ops.zeros_rows(self.NL, self.cfg[l].d_in, dev) for l in hidden}
-        if model.kind == "gat":
-            self._alloc_gat_kept(model)
         self.g = ops.zeros_rows(self.NL, wide, dev)
         self.h = ops.zeros_rows(self.NL, wide, dev)
         if model.kind == "sage":
@@ -633,6 +620,21 @@ class LayerwiseEngine(_EngineBase):
         # follows (once per row instead of once per edge)
         cl = self.cfg[-1]
         self.g2 = ops.zeros_rows(self.NL, cl.d_out, dev) if (cl.sage and cl.transform_first) else None
+        # aggregate-first GCN layers: the forward's normalised aggregate N is
+        # kept for the backward's dW = N^T gp when it fits, instead of the
+        # reference's regather (GRD_KEEP_AGG=0 regathers).  Decided after
+        # every engine buffer above exists, so the free-HBM margin is what
+        # the lazily allocated scratch really has left.
+        self.keep_on = os.environ.get("GRD_KEEP_AGG", "1") != "0"
+        self.n_kept = {}
+        if self.keep_on:
+            hidden = [l for l, c in enumerate(self.cfg)
+                      if not (c.transform_first or c.sage or c.gat or c.rownorm or c.last)]
+            need = sum(self.NL * ld_of(self.cfg[l].d_in) * 4 for l in hidden)
+            if hidden and self._keep_fits(need):
+                self.n_kept = {l: ops.zeros_rows(self.NL, self.cfg[l].d_in, dev) for l in hidden}
+        if model.kind == "gat":
+            self._alloc_gat_kept(model)
         # one device: SGD fused into the weight-gradient reduction; sharded:
         # local weight gradients are all-reduced first, SGD at epoch end
         self.defer_sgd = self.comm is not None

@@ -126,3 +126,10 @@ def read_checkpoint(path: str | Path) -> list[np.ndarray]:
     if off != len(raw):
         raise ValueError(f"trailing bytes in checkpoint: expected {off}, found {len(raw)}")
     return out
+
+
+def canonical_json(obj) -> str:
+    """JSON with sorted keys, 2-space indent and a trailing newline
+    (formats.py:219-221): summaries and ledgers compare as text."""
+    import json
+    return json.dumps(obj, sort_keys=True, indent=2) + "\n"

@@ -18,7 +18,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["CsrGraph", "build_csr", "generate_kronecker", "KRONECKER_INITIATOR"]
+__all__ = ["CsrGraph", "DegreeStats", "build_csr", "degree_stats", "export_edge_list",
+           "generate_kronecker", "KRONECKER_INITIATOR"]
 
 # Skewed 2x2 initiator (graph.py:30).
 KRONECKER_INITIATOR = (0.57, 0.19, 0.19, 0.05)
@@ -233,3 +234,28 @@ def generate_kronecker(scale: int, avg_degree: int, seed: int,
     dst = dst_idx[:edges] if edges < dst_idx.size else dst_idx
     return CsrGraph(num_vertices=n, num_edges=edges, src_ptr=src_ptr,
                     dst_idx=np.ascontiguousarray(dst[:edges]))
+
+
+def export_edge_list(graph: CsrGraph) -> np.ndarray:
+    """int64 [E, 2] (source, destination) pairs in CSR order (graph.py:149-152)."""
+    return np.stack([graph.edge_sources().astype(np.int64), graph.dst_idx.astype(np.int64)], axis=1)
+
+
+@dataclass
+class DegreeStats:
+    """Out-degree histogram, mean (= |E| / |V| exactly), max and population variance."""
+
+    histogram: np.ndarray
+    mean: float
+    max: int
+    variance: float
+
+
+def degree_stats(graph: CsrGraph) -> DegreeStats:
+    """Summary of the out-degree distribution (graph.py:306-327)."""
+    deg = graph.out_degrees()
+    n = graph.num_vertices
+    return DegreeStats(histogram=np.bincount(deg, minlength=1),
+                       mean=graph.num_edges / n if n else 0.0,
+                       max=int(deg.max()) if deg.size else 0,
+                       variance=float(deg.var()) if deg.size else 0.0)

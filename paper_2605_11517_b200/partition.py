@@ -26,9 +26,11 @@ __all__ = [
     "PartitionerParams",
     "expansion_ratio",
     "partition_objective",
+    "partition_score",
     "random_partition",
     "relocation_capacity",
     "switching_aware_partition",
+    "vertex_preferences",
 ]
 
 
@@ -93,6 +95,31 @@ def random_partition(num_vertices: int, num_partitions: int, seed: int = 0) -> n
     labels = np.empty(num_vertices, dtype=np.int32)
     labels[shuffled] = np.arange(num_vertices, dtype=np.int32) % num_partitions
     return labels
+
+
+def partition_score(graph: CsrGraph, labels: np.ndarray, vertex: int, part: int,
+                    alpha_balance: float, num_partitions: int) -> float:
+    """One vertex's affinity for one partition, the per-vertex term the
+    switching-aware objective sums (partition.py:114-124): 1 + (share of the
+    vertex's out-neighbours labelled ``part``) - |part| / (alpha V / P)."""
+    row = graph.dst_idx[int(graph.src_ptr[vertex]):int(graph.src_ptr[vertex + 1])]
+    labels = np.asarray(labels)
+    share = float(np.sum(labels[row] == part)) / row.size if row.size else 0.0
+    fair = alpha_balance * graph.num_vertices / num_partitions
+    return 1.0 + share - float(np.sum(labels == part)) / fair
+
+
+def vertex_preferences(graph: CsrGraph, labels: np.ndarray, vertex: int,
+                       num_partitions: int, depth: int = 2) -> list[int]:
+    """The partitions a vertex's out-neighbours fall in, most frequent first
+    and ties by ascending id, at most ``depth`` of them (partition.py:
+    127-137); empty for an isolated vertex."""
+    row = graph.dst_idx[int(graph.src_ptr[vertex]):int(graph.src_ptr[vertex + 1])]
+    if row.size == 0:
+        return []
+    counts = np.bincount(np.asarray(labels)[row], minlength=num_partitions)
+    ranked = sorted(np.flatnonzero(counts).tolist(), key=lambda q: (-int(counts[q]), q))
+    return ranked[:depth]
 
 
 def partition_objective(graph: CsrGraph, labels: np.ndarray, num_partitions: int,

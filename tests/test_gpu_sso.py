@@ -134,12 +134,28 @@ def test_offloaded_with_empty_partition(tmp_path):
     session.close()
 
 
-def test_executing_session_rejects_f64_width_and_bare_hooks():
+def test_session_modes(tmp_path):
+    """fp32 width executes; the reference's default 8-byte width stays a byte
+    model whose hooks wrap the per-partition engine (the reference's own
+    behaviour, same ledger as simulate_epoch); bare hooks are refused once a
+    session is bound to a training run's data."""
     g = g2.generate_kronecker(6, 4, seed=1)
     plan = g2.build_partition_plan(g, g2.random_partition(g.num_vertices, 2, 1), 2)
+    ds = g2.make_random_dataset(g, feature_dim=4, num_classes=2, seed=2)
+    model = g2.create_model(4, 2, num_layers=2, hidden_dim=4, seed=3)
     with pytest.raises(ValueError):
-        TierSession(plan, [4, 4, 2], "GRINNDER", HierarchyConfig(bytes_per_value=8))
-    s = TierSession(plan, [4, 4, 2], "GRINNDER", HierarchyConfig(bytes_per_value=4))
+        TierSession(plan, model.dims, "GRINNDER", HierarchyConfig(bytes_per_value=8), execute=True)
+    byte_model = TierSession(plan, model.dims, "GRINNDER", HierarchyConfig())
+    assert not byte_model.execute
+    trained, trace, ledger = g2.partitioned_train(ds, plan, model, 1, 0.05, hierarchy=byte_model)
+    assert ledger.events == simulate_epoch(plan, model.dims, "GRINNDER", HierarchyConfig()).events
+    resident, rtrace, _ = g2.partitioned_train(ds, plan, model, 1, 0.05)
+    assert abs(trace[0][1] - rtrace[0][1]) <= 1e-6 * abs(rtrace[0][1])
+    s = TierSession(plan, model.dims, "GRINNDER", HierarchyConfig(bytes_per_value=4),
+                    directory=str(tmp_path))
+    assert s.execute and not s.live
+    g2.partitioned_train(ds, plan, model, 1, 0.05, hierarchy=s)
+    assert s.live
     with pytest.raises(RuntimeError):
         s.forward_partition(0, 0)
     s.close()

@@ -105,7 +105,8 @@ def test_storage_tier_row_runs_round_trip(tmp_path):
     import torch
     from paper_2605_11517_b200.hierarchy import StorageTier
     levels = []
-    st = StorageTier(1 << 30, str(tmp_path), True, levels.append)
+    st = StorageTier(1 << 30, str(tmp_path), levels.append)
+    st.activate()
     rows = torch.arange(7 * 5, dtype=torch.float32).reshape(7, 5)
     first, count = np.array([2, 10, 11 + 1]), np.array([3, 1, 3])
     st.io(("act", 1), True, 5 * 4, first, count, rows, create=True)
