@@ -1,32 +1,46 @@
-"""Host-tier (SSO) epoch probe at a papers-shaped scale: trainer set-up time,
-epoch wall time, host-gather time, H2D/D2H bytes.
-Usage: python tools/sso_probe.py SCALE PARTITIONS"""
-import sys, time
+"""Epoch of the executing SSO manager on a papers-shaped graph (configs[3]'s
+model) for host-tier capacities that keep whole layers, force partition
+slabs, or force page-granular vertex reads: wall time per epoch, ledger
+bytes per link, the manager's storage-tier traffic.
+Usage: python tools/sso_probe.py [SCALE] [PARTITIONS] [EPOCHS]"""
+import json
+import sys
+import tempfile
+import time
+
 sys.path.insert(0, '.')
-import numpy as np, torch
-import bench
-from paper_2605_11517_b200.hierarchy import HierarchyConfig, TierSession
-from paper_2605_11517_b200.sso import OffloadedTrainer
-from paper_2605_11517_b200.model import copy_model
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2605_11517_b200 as g2  # noqa: E402
+from paper_2605_11517_b200.hierarchy import HierarchyConfig, TierSession, ledger_summary  # noqa: E402
+
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-spec = dict(bench.WORKLOADS["papers_gcn"], scale=scale, P=P)
-t0 = time.perf_counter()
+epochs = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+spec = dict(bench.WORKLOADS["papers_gcn"], scale=scale, deg=12, P=P, feature_dtype="float32")
 g, ds, plan, model, prep = bench.build_workload(spec)
-print("prep", prep, "build", round(time.perf_counter() - t0, 1), "V", g.num_vertices, "E", g.num_edges, flush=True)
-cfg = HierarchyConfig(gpu_capacity=64 << 30, host_capacity=180 << 30, bytes_per_value=4)
-sess = TierSession(plan, model.dims, "GRINNDER", cfg, aggregation_mode=model.aggregation_mode)
-t0 = time.perf_counter()
-tr = OffloadedTrainer(ds, plan, copy_model(model), sess, torch.device("cuda"))
-torch.cuda.synchronize()
-print("trainer init s", round(time.perf_counter() - t0, 2), flush=True)
-order = lambda l, ph: list(sess.partition_order(l, ph))
-for ep in range(3):
-    h0, d0 = tr.bytes_h2d, tr.bytes_d2h
-    torch.cuda.synchronize(); t0 = time.perf_counter()
-    tr.epoch(ep, 0.01, order)
-    torch.cuda.synchronize(); dt = time.perf_counter() - t0
-    L, E = model.num_layers, g.num_edges
-    print(f"epoch {ep}: {dt:.3f} s  edges/s {L*E/dt/1e9:.3f} G  "
-          f"H2D {(tr.bytes_h2d-h0)/1e9:.2f} GB  D2H {(tr.bytes_d2h-d0)/1e9:.2f} GB  loss {tr.read_stats()[0]:.5f}",
-          flush=True)
+V, E, L = g.num_vertices, g.num_edges, model.num_layers
+layer = V * 128 * 4
+out = {"graph": f"generate_kronecker({scale}, 12): {V} V / {E} E, P = {P}", "runs": {}}
+resident, rtrace, _ = g2.partitioned_train(ds, plan, model, 1, 0.01)
+for name, cap in (("layer_lru", 3 * layer), ("partition_lru", layer // 2), ("vertex", 0)):
+    with tempfile.TemporaryDirectory(dir=bench.os.environ.get("GRD_TIER_DIR")) as d:
+        cfg = HierarchyConfig(host_capacity=cap, bytes_per_value=4)
+        sess = TierSession(plan, model.dims, "GRINNDER", cfg, directory=d)
+        t0 = time.perf_counter()
+        trained, trace, ledger = g2.partitioned_train(ds, plan, model, epochs, 0.01, hierarchy=sess)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / epochs
+        summ = ledger_summary(ledger)
+        out["runs"][name] = {
+            "granularity": sess.granularity, "s_per_epoch": round(dt, 3),
+            "edges_per_s": round(L * E / dt, 1),
+            "loss_vs_resident": abs(trace[0][1] - rtrace[0][1]) / rtrace[0][1],
+            "GB_per_epoch": {k: round(v["total"] / epochs / 1e9, 3) for k, v in summ["links"].items()},
+            "cache_hit_rate": summ["cache"]["hit_rate"], "peak_residency_GB": {
+                k: round(v / 1e9, 3) for k, v in summ["peak_residency"].items()}}
+        sess.close()
+        print(name, json.dumps(out["runs"][name]), flush=True)
+print(json.dumps(out))
