@@ -164,6 +164,10 @@ int grd_direct_write(int32_t fd, int64_t offset, int64_t nbytes, const void* src
  * pread / pwrite spread over num_threads threads by bytes. */
 int grd_file_runs(int32_t fd, int32_t write, int64_t record, const int64_t* first,
                   const int64_t* count, int64_t nruns, void* buf, int32_t num_threads);
+/* The same row runs between a packed buffer and a memory-mapped tier file
+ * at `base` (memcpy into / out of the page cache, OpenMP over runs). */
+int grd_mem_runs(void* base, int32_t write, int64_t record, const int64_t* first,
+                 const int64_t* count, int64_t nruns, void* buf, int32_t num_threads);
 
 /* ------------------------------------------------------------------------
  * Device kernels (sm_100a).  All take `stream` = cudaStream_t.

@@ -161,6 +161,7 @@ SIGNATURES = {
     "grd_direct_read": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i32]),
     "grd_direct_write": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i32]),
     "grd_file_runs": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32]),
+    "grd_mem_runs": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32]),
     "grd_memcpy2d": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "grd_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_scatter_add_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),

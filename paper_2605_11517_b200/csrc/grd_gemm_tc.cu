@@ -80,6 +80,7 @@ struct Params {
     int accumulate;
     float* partial; int64_t ld_partial;   // split-K: [z][m][ld_partial]
     float* c2; int64_t ldc2; int64_t split;   // columns >= split (> 0) go to c2
+    int tma_store;                  // epilogue chunks leave through shared memory by TMA
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -329,12 +330,61 @@ __device__ __forceinline__ void epi_store_direct(const Params& p, const float (&
     }
 }
 
+// TMA-store epilogue: a warp's 32-row x 32-column chunk is written to its
+// 4 KB shared staging tile in the 128-byte-swizzled layout the tensor map
+// names (the 16-byte column group j of row r sits at group j ^ (r & 7), so a
+// warp's row-per-lane float4 stores spread over all banks) and one lane
+// issues the bulk tensor store.  The global writes are whole 128-byte row
+// segments issued by the TMA engine instead of 32 scattered 16-byte stores
+// per instruction.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void epi_stage_tma(const Params& p, const float (&v)[32], int64_t row, int64_t col0,
+                                              const EpiIn& in, uint8_t* stage, int lane) {
+    const float rs = (p.row_scale && row < p.m) ? p.row_scale[row] : 1.0f;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        const float4 oo = in.o[j / 4];
+        x.x += oo.x; x.y += oo.y; x.z += oo.z; x.w += oo.w;
+        if (p.row_scale) { x.x *= rs; x.y *= rs; x.z *= rs; x.w *= rs; }
+        if (p.elem_mul && row < p.m && col0 + j < (p.n + 3) / 4 * 4) {
+            const float4 m = *reinterpret_cast<const float4*>(p.elem_mul + row * p.ld_elem_mul + col0 + j);
+            x.x *= m.x; x.y *= m.y; x.z *= m.z; x.w *= m.w;
+        }
+        const float4 ee = in.e[j / 4];
+        if (!(ee.x > 0.f)) x.x = 0.f;
+        if (!(ee.y > 0.f)) x.y = 0.f;
+        if (!(ee.z > 0.f)) x.z = 0.f;
+        if (!(ee.w > 0.f)) x.w = 0.f;
+        if (p.relu_out) {
+            x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        }
+        const uint32_t grp = static_cast<uint32_t>(j >> 2) ^ static_cast<uint32_t>(lane & 7);
+        *reinterpret_cast<float4*>(stage + lane * 128 + grp * 16) = x;
+    }
+}
+
 // Epilogue warps' loop over the tiles of this CTA (both kernels): TMEM
 // accumulator `acc` of the i-th tile with K work, drained chunk by chunk.
 template <bool kPair, bool kSplit, class TileFn>
 __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
                                               int warp, int lane, int64_t t0, int64_t tstep,
-                                              int64_t ntiles, TileFn tile_of) {
+                                              int64_t ntiles, TileFn tile_of,
+                                              const CUtensorMap* map_c = nullptr, uint8_t* stage = nullptr) {
+    const bool tma = !kSplit && p.tma_store && stage != nullptr;
     const int q = warp & 3;                               // TMEM lane quarter
     const int half = (warp - kEpiWarp0) >> 2;             // which interleaved column chunks
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
@@ -365,6 +415,16 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
                 for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
             if (row0 >= p.m || n0 + c0 >= n_pad) continue;   // warp-uniform
+            if (tma) {
+                if (lane == 0) tma_store_wait_read();     // the staging tile's last store has read it
+                __syncwarp();
+                epi_stage_tma(p, v, row0 + lane, n0 + c0, in, stage, lane);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    tma_store_2d(map_c, stage, static_cast<int32_t>(n0 + c0), static_cast<int32_t>(row0));
+                continue;
+            }
             epi_store_direct<kSplit>(p, v, row0 + lane, n0 + c0, z, in);
         }
         if (has_k) {
@@ -378,6 +438,7 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
             ++i;
         }
     }
+    if (tma && lane == 0) tma_store_wait_all();
 }
 
 // Split-K partial tiles with fresh accumulators (kFresh): the MMA issuer
@@ -449,7 +510,7 @@ __device__ __forceinline__ void epilogue_fresh(const Params& p, uint32_t tmem, u
 template <bool kPair, bool kSplit, bool kFresh = false>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               const Params p) {
+               const __grid_constant__ CUtensorMap map_c, const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int bn = p.bn;
@@ -467,7 +528,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t stage_bytes = bres ? 2u * a_bytes : 2u * (a_bytes + b_bytes);
     uint8_t* bres_smem = smem + S * stage_bytes;
     const uint32_t bres_bytes = bres ? static_cast<uint32_t>(nkb_b) * 2u * b_bytes : 0u;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(bres_smem + bres_bytes);
+    // TMA-store staging: 4 KB per epilogue warp, 1024-byte aligned (swizzle atoms)
+    uint8_t* epi_stage = smem + ((S * stage_bytes + bres_bytes + 1023u) & ~1023u);
+    const uint32_t epi_bytes = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u : 0u;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p.tma_store ? epi_stage + epi_bytes : bres_smem + bres_bytes);
     uint64_t* full = bars;             // [S]
     uint64_t* conv = bars + S;         // [S]
     uint64_t* empty = bars + 2 * S;    // [S]
@@ -722,7 +786,8 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if constexpr (kFresh)
             epilogue_fresh<kPair>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of, kblocks_of);
         else
-            epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of);
+            epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of, &map_c,
+                                         epi_stage + (warp - kEpiWarp0) * 4096);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -1072,6 +1137,16 @@ inline int fresh_pref() {
     return v;
 }
 
+// epilogue chunks stored by TMA through shared memory (GRD_GEMM_TMA_STORE = 1 / 0)
+inline int tma_store_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_TMA_STORE");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 // packed weight operand resident in shared memory when it fits (GRD_GEMM_BRES = 1 / 0)
 inline int bres_pref() {
     static int v = -1;
@@ -1232,19 +1307,26 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     // B resident in shared memory: a packed weight operand with one N tile,
     // no split-K, that leaves room for >= 3 A-only stages (GRD_GEMM_BRES=0
     // keeps B in the stage ring)
+    // TMA-store epilogue (plain C output: no split-K partial, no split c2)
+    CUtensorMap map_c = map_a;
+    p.tma_store = 0;
+    if (tma_store_pref() && !p.partial && p.split == 0 && g.c && (g.ldc % 4) == 0 &&
+        make_map(&map_c, g.c, g.m, (g.n + 3) / 4 * 4, g.ldc, 32, 32))
+        p.tma_store = 1;
+    const uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;
     if (bres_pref() && p.b_mode == kPacked && p.splits == 1 && g.n <= p.bn && (p.pair || cluster_pref() == 1)) {
         const uint32_t res = static_cast<uint32_t>((g.k + kBK - 1) / kBK) * 2u * bnl_bytes;
         const uint32_t st_a = 2u * kBM * 128u;
-        if (res + 3u * st_a <= 220u * 1024u) {
+        if (res + 3u * st_a + epi <= 220u * 1024u) {
             resident = res;
             stage = st_a;
             p.b_resident = 1;
         }
     }
-    p.stages = static_cast<int>((220u * 1024u - resident) / stage);
+    p.stages = static_cast<int>((220u * 1024u - resident - epi) / stage);
     if (p.stages > (p.b_resident ? 6 : 4)) p.stages = p.b_resident ? 6 : 4;
     if (p.stages < 2) p.stages = 2;
-    const size_t smem = static_cast<size_t>(p.stages) * stage + resident + 1024 + 256;
+    const size_t smem = static_cast<size_t>(p.stages) * stage + resident + epi + 1024 + 256;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;
     if (!attr) {
@@ -1267,9 +1349,9 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     const int64_t max_cl = num_sms() / C;
     const int grid = static_cast<int>((tiles < max_cl ? tiles : max_cl) * C);
     if (C == 1) {
-        if (fresh) gemm_tf32x3_ws<false, false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
-        else if (p.split > 0) gemm_tf32x3_ws<false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
-        else gemm_tf32x3_ws<false, false><<<grid, kThreads, smem, st>>>(map_a, map_b, p);
+        if (fresh) gemm_tf32x3_ws<false, false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, map_c, p);
+        else if (p.split > 0) gemm_tf32x3_ws<false, true><<<grid, kThreads, smem, st>>>(map_a, map_b, map_c, p);
+        else gemm_tf32x3_ws<false, false><<<grid, kThreads, smem, st>>>(map_a, map_b, map_c, p);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -1285,12 +1367,12 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
     if (p.pair) {
-        if (fresh) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false, true>, map_a, map_b, p);
-        if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, true>, map_a, map_b, p);
-        return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false>, map_a, map_b, p);
+        if (fresh) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false, true>, map_a, map_b, map_c, p);
+        if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, true>, map_a, map_b, map_c, p);
+        return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<true, false>, map_a, map_b, map_c, p);
     }
-    if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, true>, map_a, map_b, p);
-    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, false>, map_a, map_b, p);
+    if (p.split > 0) return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, true>, map_a, map_b, map_c, p);
+    return cudaLaunchKernelEx(&cfg, gemm_tf32x3_ws<false, false>, map_a, map_b, map_c, p);
 }
 
 cudaError_t grd_tc_pack_b(const float* b, int64_t ldb, int trans_b, int64_t n, int64_t k, float* out,

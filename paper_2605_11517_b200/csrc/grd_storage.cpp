@@ -200,3 +200,32 @@ extern "C" int grd_file_runs(int32_t fd, int32_t write, int64_t record, const in
         if (e) return fail(kErrState, "file_runs: %s", std::strerror(e));
     return 0;
 }
+
+// Row-run copies between a packed buffer and a memory-mapped tier file (the
+// SSO manager's storage objects are mapped: scattered row runs become
+// memcpy's into the page cache instead of one pread / pwrite per run; the
+// kernel writes the pages back).  Same run convention as grd_file_runs.
+extern "C" int grd_mem_runs(void* base, int32_t write, int64_t record, const int64_t* first,
+                            const int64_t* count, int64_t nruns, void* buf, int32_t num_threads) {
+    clear_error();
+    if (nruns == 0) return 0;
+    if (!base || record <= 0 || !first || !count || !buf || nruns < 0)
+        return fail(kErrArg, "mem_runs: bad arguments");
+    std::vector<int64_t> at(static_cast<size_t>(nruns) + 1, 0);
+    for (int64_t i = 0; i < nruns; ++i) {
+        if (first[i] < 0 || count[i] < 0) return fail(kErrArg, "mem_runs: negative run");
+        at[i + 1] = at[i] + count[i] * record;
+    }
+    char* file = static_cast<char*>(base);
+    char* packed = static_cast<char*>(buf);
+    const int nt = num_threads > 0 ? num_threads : 1;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 64)
+    for (int64_t i = 0; i < nruns; ++i) {
+        char* f = file + first[i] * record;
+        char* b = packed + at[i];
+        const size_t len = static_cast<size_t>(at[i + 1] - at[i]);
+        if (write) std::memcpy(f, b, len);
+        else std::memcpy(b, f, len);
+    }
+    return 0;
+}

@@ -258,7 +258,10 @@ class StreamingEngine:
             # left by the GPU plan builder) are available to the cache too
             free, _ = torch.cuda.mem_get_info(dev)
             free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
-            x_cache_bytes = max(0, free - (4 << 30))
+            # margin for the lazily allocated scratch (heavy-row partials,
+            # GEMM / weight-gradient workspaces): GRD_STREAM_MARGIN_GB
+            margin = float(os.environ.get("GRD_STREAM_MARGIN_GB", "1.5"))
+            x_cache_bytes = max(0, free - int(margin * 2**30))
         rows = min(self.V, int(x_cache_bytes) // row_bytes)
         rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
         self.cache_rows = rows
@@ -641,7 +644,7 @@ def streaming_bytes(num_vertices: int, num_edges: int, model, chunk_rows: int,
     return graph + layers + chunks + 4 * E * max(lds) // 64 + 16 * V
 
 
-DEFAULT_CHUNK_ROWS = 1 << 20
+DEFAULT_CHUNK_ROWS = int(os.environ.get("GRD_CHUNK_ROWS", str(1 << 20)))
 
 
 def feature_rows(dataset, chunk_rows: int = DEFAULT_CHUNK_ROWS, host_cache_bytes: int | None = None):

@@ -403,3 +403,38 @@ def test_gat_src_grad_lane_groups(heads):
     for name in cases:
         assert np.allclose(res[name], res["warp"], rtol=1e-5, atol=1e-5), name
         assert np.allclose(res[name], ref, rtol=1e-4, atol=1e-4), name
+
+
+@pytest.mark.parametrize("tma", ["1", "0"])
+@pytest.mark.parametrize("m,n,k", [(1000, 47, 128), (300, 128, 64), (2050, 256, 96)])
+def test_gemm_output_columns_and_rows_exact(tma, m, n, k, monkeypatch):
+    """The epilogue writes exactly rows [0, m) and columns [0, round_up(n, 4))
+    of C — padding columns as zeros, nothing past them, nothing below row m —
+    whether chunks leave by per-row stores or by TMA through shared memory
+    (GRD_GEMM_TMA_STORE; read once per process, so a child process runs the
+    opposite setting)."""
+    import subprocess
+    import sys
+    code = f"""
+import sys; sys.path.insert(0, {str(Path(__file__).resolve().parents[1])!r})
+import numpy as np, torch
+from paper_2605_11517_b200 import ops
+m, n, k = {m}, {n}, {k}
+rng = np.random.default_rng(3)
+a = ops.zeros_rows(m, k, 'cuda'); a[:, :k] = torch.from_numpy(rng.normal(size=(m, k)).astype(np.float32)).cuda()
+b = ops.zeros_rows(k, n, 'cuda'); b[:, :n] = torch.from_numpy(rng.normal(size=(k, n)).astype(np.float32)).cuda()
+npad = (n + 3) // 4 * 4
+big = torch.full((m + 37, npad + 8), 7.0, device='cuda')
+c = big[:m, :]
+ops.gemm(a, b, c, m, n, k)
+want = a[:, :k].double() @ b[:, :n].double()
+err = float((c[:, :n].double() - want).norm() / want.norm())
+assert err < 5e-6, err
+assert torch.all(c[:, n:npad] == 0), 'padding columns'
+assert torch.all(big[:m, npad:] == 7.0), 'columns past the padding'
+assert torch.all(big[m:] == 7.0), 'rows past m'
+print('ok')
+"""
+    env = dict(os.environ, GRD_GEMM_TMA_STORE=tma)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -100,12 +100,14 @@ def test_manager_dry_run_equals_oracle_byte_model(seed):
 
 
 def test_storage_tier_row_runs_round_trip(tmp_path):
-    """grd_file_runs: packed row runs written at record offsets read back
-    bit for bit (and untouched regions of the file read as zeros)."""
+    """grd_mem_runs on a mapped tier file: packed row runs written at record
+    offsets read back bit for bit (untouched regions of the file read as
+    zeros); deleting the object unmaps and removes the file."""
     import torch
     from paper_2605_11517_b200.hierarchy import StorageTier
     levels = []
     st = StorageTier(1 << 30, str(tmp_path), levels.append)
+    st.sizes[("act", 1)] = 15 * 5 * 4
     st.activate()
     rows = torch.arange(7 * 5, dtype=torch.float32).reshape(7, 5)
     first, count = np.array([2, 10, 11 + 1]), np.array([3, 1, 3])
