@@ -1310,7 +1310,9 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     // TMA-store epilogue (plain C output: no split-K partial, no split c2)
     CUtensorMap map_c = map_a;
     p.tma_store = 0;
-    if (tma_store_pref() && !p.partial && p.split == 0 && g.c && (g.ldc % 4) == 0 &&
+    // measured (tools/gemm_shapes.py): -12..-33 % at N tiles of 128 / 256,
+    // +17..26 % at 48 / 192 (fewer stages fit beside the staging tiles)
+    if (tma_store_pref() && p.bn % 128 == 0 && !p.partial && p.split == 0 && g.c && (g.ldc % 4) == 0 &&
         make_map(&map_c, g.c, g.m, (g.n + 3) / 4 * 4, g.ldc, 32, 32))
         p.tma_store = 1;
     const uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;

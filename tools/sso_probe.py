@@ -34,7 +34,8 @@ for name, cap in (("layer_lru", 3 * layer), ("partition_lru", layer // 2), ("ver
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / epochs
         summ = ledger_summary(ledger)
-        out["runs"][name] = {
+        wall = {k: round(v / epochs, 3) for k, v in sorted(sess.wall.items(), key=lambda kv: -kv[1])}
+        out["runs"][name] = {"host_wall_s_per_epoch": wall,
             "granularity": sess.granularity, "s_per_epoch": round(dt, 3),
             "edges_per_s": round(L * E / dt, 1),
             "loss_vs_resident": abs(trace[0][1] - rtrace[0][1]) / rtrace[0][1],
