@@ -331,20 +331,31 @@ class DevicePartition:
         self.targets = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.int32)).to(device)
         self.gather_map = torch.from_numpy(np.ascontiguousarray(gather_map, dtype=np.int32)).to(device)
         self.fwd = AggSpec.build(tgt_ptr, src_pos, device, self_idx=self_pos)
-        # Transposed local aggregation: for gather row g, its targets in
-        # ascending order (np.add.at's edge order, training.py:141), self last.
-        csc_ptr = np.empty(self.num_gather + 1, dtype=np.int64)
-        csc_rows = np.empty(src_pos.size, dtype=np.int32)
-        src32 = np.ascontiguousarray(src_pos, dtype=np.int32)
-        _lib.check(_lib.lib().grd_csr_transpose(self.num_targets, tgt_ptr.ctypes.data, src32.ctypes.data,
-                                                self.num_gather, csc_ptr.ctypes.data, csc_rows.ctypes.data),
-                   "csr_transpose")
-        self_t = np.full(self.num_gather, -1, dtype=np.int32)
-        self_t[self_pos] = np.arange(self.num_targets, dtype=np.int32)
-        self.bwd = AggSpec.build(csc_ptr, csc_rows, device, self_idx=self_t)
+        self._csr = (tgt_ptr, src_pos, self_pos)
+        self._bwd = None
         self._deg = {"targets": np.asarray(target_indeg, dtype=np.float64),
                      "gather": np.asarray(gather_indeg, dtype=np.float64)}
         self._scales: dict = {}
+
+    @property
+    def bwd(self) -> AggSpec:
+        """Transposed local aggregation, built on first use (a forward-only
+        stage of the SSO manager never needs it): for gather row g, its
+        targets in ascending order (np.add.at's edge order, training.py:141),
+        self last."""
+        if self._bwd is None:
+            tgt_ptr, src_pos, self_pos = self._csr
+            csc_ptr = np.empty(self.num_gather + 1, dtype=np.int64)
+            csc_rows = np.empty(src_pos.size, dtype=np.int32)
+            src32 = np.ascontiguousarray(src_pos, dtype=np.int32)
+            _lib.check(_lib.lib().grd_csr_transpose(self.num_targets, tgt_ptr.ctypes.data,
+                                                    src32.ctypes.data, self.num_gather,
+                                                    csc_ptr.ctypes.data, csc_rows.ctypes.data),
+                       "csr_transpose")
+            self_t = np.full(self.num_gather, -1, dtype=np.int32)
+            self_t[self_pos] = np.arange(self.num_targets, dtype=np.int32)
+            self._bwd = AggSpec.build(csc_ptr, csc_rows, self.dev, self_idx=self_t)
+        return self._bwd
 
     @classmethod
     def from_topology(cls, topo, device) -> "DevicePartition":
