@@ -293,6 +293,13 @@ def run_ours(args, spec, rank, world, local_rank):
     gpu = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
+    if world > 1 and spec.get("host_gb"):
+        # the sharded engine keeps every local layer resident; at this size a
+        # rank's owned + halo rows (alpha ~2.7 at P = 16) exceed HBM up to
+        # N = 8 and the layer-streaming engine runs on one rank only
+        raise SystemExit(f"workload {args.workload} runs on one GPU (streaming engine); the "
+                         "sharded N > 1 path needs a per-rank streaming engine (DESIGN.md §7) — "
+                         "use --workload papers_gcn / products_sage / config1 for N > 1")
     need = spec.get("host_gb")
     if need:
         import psutil
