@@ -561,6 +561,7 @@ int64_t wgrad_splits(int64_t m, int64_t n, int64_t k) {
 
 // -------------------------------------------------------------------- K4 --
 constexpr int kLossBlocks = 1184;  // 148 SMs x 8
+constexpr int kXentRegCols = 256;  // rows up to this many classes reduce in registers
 
 __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ logits, int64_t ldl,
                                                    int64_t n_rows, int c, const int32_t* __restrict__ labels,
@@ -651,7 +652,89 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
         }
         r = n_rows;   // fall through to the block reduction
     }
-    for (int64_t r = c <= 2 * kWarp ? n_rows : int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows;
+    if (c > 2 * kWarp && c <= kXentRegCols) {
+        // 65..256 classes: the row lives in registers (up to 8 per lane, j =
+        // lane + 32 k), the next row is loaded while this one reduces; the
+        // same per-lane orders as the general loop below (max / argmax and
+        // the exp sum over ascending j, then the butterfly): the same bits
+        constexpr int NV = kXentRegCols / kWarp;
+        int64_t r = int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp;
+        float v[NV], nv[NV];
+        int y = 0, ny = 0;
+        bool on = false, non = false;
+        auto load = [&](int64_t rr, float (&x)[NV], int& yy, bool& mm) {
+            const float* row = logits + rr * ldl;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) x[k] = lane + k * kWarp < c ? row[lane + k * kWarp] : -INFINITY;
+            yy = labels[rr];
+            mm = mask[rr] != 0;
+        };
+        if (r < n_rows) load(r, v, y, on);
+        for (; r < n_rows; r += nwarps) {
+            if (r + nwarps < n_rows) load(r + nwarps, nv, ny, non);
+            float* grow = grad + r * ldg;
+            float* grow2 = grad2 ? grad2 + r * ldg2 : nullptr;
+            const float s2 = grad2 ? g2scale[r] : 0.f;
+            if (lane < c4 - c) {
+                grow[c + lane] = 0.f;
+                if (grow2) grow2[c + lane] = 0.f;
+            }
+            if (!on) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int j = lane + k * kWarp;
+                    if (j < c) {
+                        grow[j] = 0.f;
+                        if (grow2) grow2[j] = 0.f;
+                    }
+                }
+            } else {
+                float mx = -INFINITY;
+                int arg = 0x7fffffff;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int j = lane + k * kWarp;
+                    if (j < c && (v[k] > mx || (v[k] == mx && j < arg))) { mx = v[k]; arg = j; }
+                }
+                for (int off = 16; off > 0; off >>= 1) {
+                    const float om = __shfl_xor_sync(0xffffffffu, mx, off);
+                    const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+                    if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+                }
+                float e[NV];
+                float sum = 0.f;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    e[k] = lane + k * kWarp < c ? expf(v[k] - mx) : 0.f;
+                    if (lane + k * kWarp < c) sum += e[k];
+                }
+                for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+                const float scale = gscale ? gscale[r] : 1.0f;
+                float ey = 0.f;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int j = lane + k * kWarp;
+                    if (j < c) {
+                        float pr = e[k] / sum;
+                        if (j == y) { pr -= 1.0f; ey = e[k]; }
+                        const float gv = pr * inv_count * scale;
+                        grow[j] = gv;
+                        if (grow2) grow2[j] = gv * s2;
+                    }
+                }
+                ey = __shfl_sync(0xffffffffu, ey, y & (kWarp - 1));
+                if (lane == 0) {
+                    loss_acc -= static_cast<double>(logf(ey / sum));
+                    correct += (arg == y) ? 1.0 : 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) v[k] = nv[k];
+            y = ny;
+            on = non;
+        }
+    }
+    for (int64_t r = c <= kXentRegCols ? n_rows : int64_t(blockIdx.x) * (blockDim.x / kWarp) + warp; r < n_rows;
          r += nwarps) {
         const float* row = logits + r * ldl;
         float* grow = grad + r * ldg;

@@ -229,6 +229,10 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
 # apply with the last chunk.  Weight gradients (trans_a) use in-kernel fresh
 # accumulators instead (GRD_WGRAD_FRESH).
 _KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "128"))
+# ... applied only above this depth: accumulations up to 192 deep (72 MMAs)
+# stay in one accumulator (the GraphSAGE K = 200 case needs the split, the
+# papers K = 172 transposed product does not: tools/prec_matrix.py)
+_KMAX = int(os.environ.get("GRD_GEMM_KMAX", "192"))
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
@@ -237,7 +241,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: i
     """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim;
     with c2, columns >= split land in c2[:, col - split] instead."""
     k = int(k)
-    if _KCHUNK and k > _KCHUNK and not trans_a and c2 is None:
+    if _KCHUNK and k > max(_KCHUNK, _KMAX) and not trans_a and c2 is None:
         starts = list(range(0, k, _KCHUNK))
         for i, k0 in enumerate(starts):
             k1 = min(k, k0 + _KCHUNK)
