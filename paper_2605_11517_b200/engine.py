@@ -1020,6 +1020,8 @@ class LayerOps:
     def layer_forward(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
         """out = act(norm(aggregate(GA)) @ W) for one partition (training.py:86-100)."""
         c = self.cfg[l]
+        if c.sage:
+            return self._sage_forward(l, ga, part)
         W = self.wts.w[l]
         pre = self._pre(l, ga, part)
         if c.rownorm:
@@ -1052,11 +1054,71 @@ class LayerOps:
                     post_scale=part.scale("s", "targets") if c.sym else None)
         return n
 
+    def grad_w_host(self, l: int, grad_w: torch.Tensor, to_host) -> np.ndarray:
+        """A per-partition weight gradient in the model's host layout
+        (GraphSAGE: [dW_root | dW_nbr] side by side, d_out columns each)."""
+        c = self.cfg[l]
+        if c.sage:
+            return np.concatenate([to_host(grad_w[:, : c.ld_out], c.d_out, c.d_in),
+                                   to_host(grad_w[:, c.ld_out:], c.d_out, c.d_in)], axis=1)
+        return to_host(grad_w, c.d_out, c.d_in)
+
+    # ---------------------------------------------- GraphSAGE-mean, per partition --
+    # out_t = X_t W_root + mean_{u in in(t)} X_u W_nbr over the partition's
+    # gathered rows: X_t = GA[self_pos], the mean over src_pos (no self),
+    # weights [W_root | W_nbr] at columns [0, ld_out) / [ld_out, 2 ld_out).
+    def _sage_parts(self, l: int, ga: torch.Tensor, part: DevicePartition):
+        c = self.cfg[l]
+        T = part.num_targets
+        xt = ops.zeros_rows(T, c.d_in, self.device)
+        if T:
+            ops.gather_rows(ga, part.fwd.self_idx, xt, c.d_in)
+        n = ops.zeros_rows(T, c.d_in, self.device)
+        ops.agg_sum(part.fwd, ga, n, c.d_in, post_div_deg=2, no_self=True)
+        return xt, n
+
+    def _sage_forward(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
+        c = self.cfg[l]
+        W = self.wts.w[l]
+        xt, n = self._sage_parts(l, ga, part)
+        out = ops.zeros_rows(part.num_targets, c.d_out, self.device)
+        ops.gemm(xt, W[:, : c.ld_out], out, part.num_targets, c.d_out, c.d_in)
+        ops.gemm(n, W[:, c.ld_out:], out, part.num_targets, c.d_out, c.d_in, accumulate=True,
+                 relu_out=not c.last)
+        return out
+
+    def _sage_backward(self, l: int, ga: torch.Tensor, a_out: torch.Tensor, grad_out: torch.Tensor,
+                       part: DevicePartition) -> tuple[torch.Tensor, torch.Tensor]:
+        """dW_root = X_t^T gp, dW_nbr = N_t^T gp (N regathered); grad_GA: the
+        neighbour rows receive (gp W_nbr^T / deg_t) pulled over the
+        partition's CSC (no self), the target rows gp W_root^T."""
+        c = self.cfg[l]
+        W = self.wts.w[l]
+        T, G = part.num_targets, part.num_gather
+        gp = ops.zeros_rows(T, c.d_out, self.device)
+        ops.mask_scale_rows(grad_out, gp, T, c.d_out, ref=None if c.last else a_out)
+        xt, n = self._sage_parts(l, ga, part)
+        grad_w = torch.zeros_like(W)
+        ops.wgrad_sgd(xt, gp, grad_w[:, : c.ld_out], c.d_in, c.d_out, T)
+        ops.wgrad_sgd(n, gp, grad_w[:, c.ld_out:], c.d_in, c.d_out, T)
+        gn = ops.zeros_rows(T, c.d_in, self.device)
+        ops.gemm(gp, W[:, c.ld_out:], gn, T, c.d_in, c.d_out, trans_b=True,
+                 row_scale=part.scale("inv_deg", "targets"))
+        grad_ga = ops.zeros_rows(G, c.d_in, self.device)
+        ops.agg_sum(part.bwd, gn, grad_ga, c.d_in, no_self=True)
+        gx = ops.zeros_rows(T, c.d_in, self.device)
+        ops.gemm(gp, W[:, : c.ld_out], gx, T, c.d_in, c.d_out, trans_b=True)
+        if T:
+            ops.scatter_add_rows(gx, part.fwd.self_idx, grad_ga, c.d_in)
+        return grad_ga, grad_w
+
     def backward_from_ga(self, l: int, ga: torch.Tensor, a_out: torch.Tensor, grad_out: torch.Tensor,
                          part: DevicePartition) -> tuple[torch.Tensor, torch.Tensor]:
         """(grad_GA [G, d_in], grad_W [d_in, d_out]) of one partition
         (training.py:103-143), recomputing from the (re)gathered input."""
         c = self.cfg[l]
+        if c.sage:
+            return self._sage_backward(l, ga, a_out, grad_out, part)
         W = self.wts.w[l]
         dev = self.device
         T, G = part.num_targets, part.num_gather
@@ -1160,7 +1222,8 @@ class PartitionEngine(_EngineBase):
             for pid in range(P):
                 grad_ga, grad_w = results[pid]
                 if grad_probe is not None:
-                    grad_probe(epoch, l, pid, to_host(grad_ga, c.d_in), to_host(grad_w, c.d_out, c.d_in))
+                    grad_probe(epoch, l, pid, to_host(grad_ga, c.d_in),
+                               self.ops.grad_w_host(l, grad_w, to_host))
                 self._add_into(self.wts.dw[l], grad_w)
                 if l > 0:
                     ops.scatter_add_rows(grad_ga, dg.partition(pid).gather_map, self.grad_prev, c.d_in)

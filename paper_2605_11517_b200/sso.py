@@ -63,9 +63,9 @@ class OffloadedTrainer:
     """GCN partition-wise training whose data lives in the SSO tiers."""
 
     def __init__(self, dataset, plan, model, session, device):
-        if model.kind != "gcn" or model.row_normalize or model.dropout_rate:
-            raise NotImplementedError("the offloaded path trains GCN layers without "
-                                      "row normalisation / dropout")
+        if model.kind == "gat" or model.row_normalize or model.dropout_rate:
+            raise NotImplementedError("the offloaded path trains GCN and GraphSAGE layers "
+                                      "without row normalisation / dropout")
         if list(session.dims) != list(model.dims):
             raise ValueError(f"tier session dims {session.dims} != model dims {model.dims}")
         self.s, self.plan, self.device = session, plan, device
@@ -148,7 +148,7 @@ class OffloadedTrainer:
             for pid in range(self.P):                    # ascending partition id
                 if grad_probe is not None:
                     grad_probe(epoch, l, pid, to_host(probes[pid], d_in),
-                               to_host(grad_w[pid], d_out, d_in))
+                               self.lops.grad_w_host(l, grad_w[pid], to_host))
                 self._add(wts.dw[l], grad_w[pid])
             s.end_backward_layer(l)
         for w, dw in zip(wts.w, wts.dw):

@@ -87,7 +87,7 @@ def layer_forward(layer: int, input_rows: np.ndarray, topology: PartitionTopolog
     lops = LayerOps(model, dev)
     part = DevicePartition.from_topology(topology, dev)
     out = lops.layer_forward(layer, _to_dev(input_rows, dev), part)
-    return _to_host(out, weight.shape[1])
+    return _to_host(out, model.dims[layer + 1])
 
 
 def regather_backward(layer: int, partition: int, A_out: np.ndarray, grad_out: np.ndarray,
@@ -110,7 +110,7 @@ def regather_backward(layer: int, partition: int, A_out: np.ndarray, grad_out: n
     ops.gather_rows(a_in, part.gather_map, ga, d_in)
     grad_ga, grad_w = lops.backward_from_ga(layer, ga, _to_dev(A_out, dev), _to_dev(grad_out, dev),
                                             part)
-    return _to_host(grad_ga, d_in), _to_host(grad_w, d_out, d_in)
+    return _to_host(grad_ga, d_in), lops.grad_w_host(layer, grad_w, _to_host)
 
 
 def scatter_accumulate(grad_GA: np.ndarray, gather_map: np.ndarray,
@@ -311,9 +311,9 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
         raise ValueError("plan was built for a different graph")
     observed = hierarchy is not None or use_snapshots or grad_probe is not None \
         or partition_order is not None
-    if observed and model.kind != "gcn":  # GraphSAGE / GAT: layer-wise engine only
+    if observed and model.kind == "gat":  # GAT: layer-wise engine only
         raise NotImplementedError("per-partition observers (hierarchy, probes, snapshots, "
-                                  "partition_order) are implemented for GCN layers")
+                                  "partition_order) are implemented for GCN and GraphSAGE layers")
     from .hierarchy import TierSession
     if isinstance(hierarchy, TierSession) and hierarchy.execute:
         if use_snapshots:

@@ -59,10 +59,56 @@ def test_sage_power_law_graph_with_hubs():
         assert rel_l2(a, b) < TOL
 
 
-def test_sage_rejects_per_partition_observers():
-    g, ds, plan, model = _setup(7, 4, 4, 3, 2, 4, 2, "sage_mean")
+def test_gat_rejects_per_partition_observers():
+    g, ds, plan, model = _setup(7, 4, 4, 3, 2, 8, 2, "gat")
     with pytest.raises(NotImplementedError):
         g2.partitioned_train(ds, plan, model, 1, 0.01, grad_probe=lambda *a: None)
+
+
+@pytest.mark.parametrize("F,H,C,L", [(6, 12, 3, 3), (16, 8, 5, 2), (3, 37, 7, 2)])
+def test_sage_per_partition_engine(F, H, C, L):
+    """GraphSAGE through the literal per-(layer, partition) schedule (K1
+    gather of GA_p, mean over the partition's in-edges, regather backward,
+    ascending-pid scatter): equal to the layer-wise engine within 1e-5 and
+    to the float64 oracle within 1e-4; the per-partition weight-gradient
+    probes sum to the epoch's gradient."""
+    g, ds, plan, model = _setup(10, 8, F, C, L, H, 5, "sage_mean")
+    seen = {}
+    pp, trace, _ = g2.partitioned_train(
+        ds, plan, model, 1, 0.05, partition_order=lambda l, ph: range(5),
+        grad_probe=lambda e, l, p, ga, gw: seen.__setitem__((l, p), gw))
+    lw, ltrace, _ = g2.partitioned_train(ds, plan, model, 1, 0.05)
+    assert abs(trace[0][1] - ltrace[0][1]) <= 1e-6 * abs(ltrace[0][1])
+    for a, b in zip(pp.weight_grads, lw.weight_grads):
+        assert a.shape == b.shape and rel_l2(a, b) < 1e-5
+    for l in range(L):
+        total = sum(seen[(l, p)] for p in range(5))
+        assert total.shape == pp.weight_grads[l].shape
+        assert rel_l2(total, pp.weight_grads[l]) < 1e-6
+    W, grads, ref = sage_gat.train_sage(ds.features, ds.labels, ds.train_mask, g.src_ptr, g.dst_idx,
+                                        model.weights, 1, 0.05)
+    assert abs(trace[0][1] - ref[0][1]) <= TOL * abs(ref[0][1])
+    for a, b in zip(pp.weight_grads, grads):
+        assert rel_l2(a, b) < TOL
+
+
+def test_sage_offloaded_tiers(tmp_path):
+    """GraphSAGE through the executing SSO manager: the ledger equals the
+    byte model's, the weights the HBM-resident engine's."""
+    from paper_2605_11517_b200.hierarchy import HierarchyConfig, TierSession, simulate_epoch
+    g, ds, plan, model = _setup(9, 8, 6, 3, 3, 12, 4, "sage_mean")
+    cfg = HierarchyConfig(host_capacity=20_000, bytes_per_value=4)
+    sess = TierSession(plan, model.dims, "GRINNDER", cfg, aggregation_mode="sage_mean",
+                       directory=str(tmp_path))
+    trained, trace, ledger = g2.partitioned_train(ds, plan, model, 2, 0.05, hierarchy=sess)
+    sim = simulate_epoch(plan, model.dims, "GRINNDER", cfg, epochs=2, aggregation_mode="sage_mean")
+    assert ledger.events == sim.events
+    resident, rtrace, _ = g2.partitioned_train(ds, plan, model, 2, 0.05)
+    for (_, a, _), (_, b, _) in zip(trace, rtrace):
+        assert abs(a - b) <= 1e-5 * abs(b)
+    for a, b in zip(trained.weights, resident.weights):
+        assert rel_l2(a, b) < 1e-5
+    sess.close()
 
 
 def test_sage_cached_session_is_bitwise_identical():
