@@ -969,8 +969,21 @@ extern "C" int grd_agg_sum(const grd_agg_args* args, void* stream) {
     // (scaled rows of <= 32 chunks measured faster on the register kernel)
     const char* mid_env = getenv("GRD_AGG_MID");
     const bool mid_override = mid_env && atoi(mid_env) > 0;
-    if (async_on && !mid_override && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64)
-        return w4 <= 32 ? launch_async<1, 2, 2>(a, st) : launch_async<2, 2, 2>(a, st);
+    if (async_on && !mid_override && !a.edge_w && cc >= a.width && w4 > (a.src_scale ? 32 : 16) && w4 <= 64) {
+        // rows in flight per warp (GRD_AGG_ASYNC_DEPTH sweep hook: 4 default, 6, 8, 3x2)
+        static int depth = -1;
+        if (depth < 0) {
+            const char* e = getenv("GRD_AGG_ASYNC_DEPTH");
+            depth = e ? atoi(e) : 4;
+        }
+        if (w4 <= 32) {
+            if (depth == 6) return launch_async<1, 2, 3>(a, st);
+            if (depth == 8) return launch_async<1, 4, 2>(a, st);
+            if (depth == 3) return launch_async<1, 1, 3>(a, st);
+            return launch_async<1, 2, 2>(a, st);
+        }
+        return launch_async<2, 2, 2>(a, st);
+    }
     // GAT weighted rows: staged variant opt-in (GRD_AGG_ASYNC_WE=1; parity-
     // green, but 157 vs 135 ms per products_gat epoch on B200: the NV 4-byte
     // weight copies per row cost more than the staging hides)
