@@ -66,6 +66,15 @@ int grd_kronecker_generate(int32_t scale, int64_t avg_degree,
 int grd_kronecker_keys(int32_t scale, int64_t batch, const uint64_t* pcg_words,
                        const double* cum, int64_t* keys, void* stream);
 
+/* Rows of make_random_dataset's feature matrix (dataset.py:75-98) on the
+ * device, bit-exact with numpy: out[i, :F] = features[rows[i]] (rows NULL:
+ * the contiguous rows row0 .. row0 + n_rows - 1), pcg_words = {state_hi,
+ * state_lo, inc_hi, inc_lo} of PCG64(seed).  Lets each rank of a sharded
+ * run create only its own rows. */
+int grd_feature_rows(const uint64_t* pcg_words, const int64_t* rows, int64_t row0,
+                     int64_t n_rows, int32_t feature_dim, float* out, int64_t ld_out,
+                     void* stream);
+
 /* Switching-aware partitioner, bit-exact with partition.py:254-321
  * switching_aware_partition (its numba kernels _analyze_kernel :140-200 and
  * _relocate_kernel :203-251).  `labels` holds random_partition()'s labels on

@@ -144,6 +144,7 @@ SIGNATURES = {
     "grd_last_error": (ctypes.c_char_p, []),
     "grd_device_sm_count": (c_i32, [c_vp]),
     "grd_kronecker_generate": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i32]),
+    "grd_feature_rows": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "grd_kronecker_keys": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "grd_sa_partition": (c_i32, [c_i64, c_vp, c_vp, c_i32, ctypes.POINTER(GrdPartitionerParams),
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),

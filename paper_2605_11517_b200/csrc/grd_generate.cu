@@ -91,7 +91,62 @@ __global__ void __launch_bounds__(256) kron_keys_kernel(int scale, int64_t batch
     }
 }
 
+// Feature rows of make_random_dataset (dataset.py:75-98): the matrix is
+// the first draws of the dataset's PCG64 stream, numpy's random(dtype=
+// float32) = (next_uint32 >> 8) * 2^-24, next_uint32 taking the low half of
+// a 64-bit output first and its high half next, then - 0.5.  Value k of the
+// row-major [V, F] matrix is half k % 2 of output k / 2.  One thread per
+// requested row: a log-time jump to its first output, then plain steps.
+__global__ void __launch_bounds__(256) feature_rows_kernel(u128 state, u128 inc, const int64_t* rows,
+                                                           int64_t row0, int64_t n_rows, int F, float* out,
+                                                           int64_t ldo) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows) return;
+    const int64_t r = rows ? rows[i] : row0 + i;
+    const uint64_t k0 = static_cast<uint64_t>(r) * static_cast<uint64_t>(F);
+    const u128 mult = pcg_mult();
+    u128 s = advance(state, inc, k0 >> 1);          // before output k0 / 2
+    float* dst = out + i * ldo;
+    uint64_t cur = 0;
+    bool have = false;
+    if (k0 & 1) {                                    // the row starts with a high half
+        s = s * mult + inc;
+        cur = xsl_rr(s);
+        have = true;
+    }
+    for (int j = 0; j < F; ++j) {
+        uint32_t u;
+        if (have) {
+            u = static_cast<uint32_t>(cur >> 32);
+            have = false;
+        } else {
+            s = s * mult + inc;
+            cur = xsl_rr(s);
+            u = static_cast<uint32_t>(cur & 0xffffffffu);
+            have = true;
+        }
+        dst[j] = static_cast<float>(u >> 8) * (1.0f / 16777216.0f) - 0.5f;
+    }
+}
+
 }  // namespace
+
+extern "C" int grd_feature_rows(const uint64_t* pcg_words, const int64_t* rows, int64_t row0,
+                                int64_t n_rows, int32_t feature_dim, float* out, int64_t ld_out,
+                                void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!pcg_words || n_rows < 0 || feature_dim <= 0 || !out || ld_out < feature_dim || (!rows && row0 < 0))
+        return fail(kErrArg, "feature_rows: bad arguments");
+    const u128 state = (static_cast<u128>(pcg_words[0]) << 64) | pcg_words[1];
+    const u128 inc = (static_cast<u128>(pcg_words[2]) << 64) | pcg_words[3];
+    const int64_t blocks = (n_rows + 255) / 256;
+    feature_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        state, inc, rows, row0, n_rows, feature_dim, out, ld_out);
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(static_cast<int>(err), "feature_rows: %s", cudaGetErrorString(err));
+    return 0;
+}
 
 extern "C" int grd_kronecker_keys(int32_t scale, int64_t batch, const uint64_t* pcg_words, const double* cum,
                                   int64_t* keys, void* stream) {

@@ -26,3 +26,19 @@ def test_gpu_generator_matches_host(scale, deg, seed):
     assert dev.num_vertices == host.num_vertices and dev.num_edges == host.num_edges
     np.testing.assert_array_equal(dev.src_ptr, host.src_ptr)
     np.testing.assert_array_equal(dev.dst_idx, host.dst_idx)
+
+
+@pytest.mark.parametrize("n,F,seed", [(1000, 128, 1), (777, 7, 3), (50, 100, 15)])
+def test_gpu_feature_rows_match_dataset(n, F, seed):
+    """grd_feature_rows: any rows of make_random_dataset's feature matrix,
+    bit-exact, without the others (a sharded run's per-rank rows)."""
+    from paper_2605_11517_b200.dataset import random_feature_rows
+    ds = g2.make_random_dataset(g2.build_csr([], n), feature_dim=F, num_classes=3, seed=seed,
+                                feature_dtype=np.float32)
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(n, size=n // 3, replace=False))
+    got = random_feature_rows(F, seed, rows=rows).cpu().numpy()
+    np.testing.assert_array_equal(got[:, :F], ds.features[rows])
+    assert not got[:, F:].any()
+    got = random_feature_rows(F, seed, row0=5, n_rows=n - 5).cpu().numpy()
+    np.testing.assert_array_equal(got[:, :F], ds.features[5:])

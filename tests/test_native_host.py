@@ -241,3 +241,15 @@ def test_file_backing_of_mmapped_features(tmp_path):
     row5 = raw[off + 5 * 48: off + 6 * 48].view(np.float32)
     np.testing.assert_array_equal(row5, mm.features[5])
     assert file_backing(np.zeros((3, 4), np.float32)) is None
+
+
+@pytest.mark.parametrize("n,F,C,seed", [(1000, 128, 10, 1), (999, 7, 5, 3), (57, 3, 47, 11)])
+def test_labels_mask_without_features_match_dataset(n, F, C, seed):
+    """random_labels_mask jumps the PCG64 stream past the feature draws (odd
+    draw counts leave numpy's buffered half) and equals make_random_dataset."""
+    from paper_2605_11517_b200 import make_random_dataset
+    from paper_2605_11517_b200.dataset import random_labels_mask
+    ds = make_random_dataset(build_csr([], n), feature_dim=F, num_classes=C, seed=seed)
+    labels, mask = random_labels_mask(n, F, C, seed)
+    np.testing.assert_array_equal(labels, ds.labels)
+    np.testing.assert_array_equal(mask, ds.train_mask)
