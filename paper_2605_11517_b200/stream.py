@@ -173,6 +173,11 @@ class StreamGraph:
             [_chunk_spec(self.bwd, bwd_ptr, r0, r1, self.self_ids) for r0, r1 in self.chunks]
         self._deg = np.diff(t_ptr).astype(np.float64)
         self._scales: dict[str, torch.Tensor] = {}
+        self.n_rows = self.n_local = n      # rows computed / buffer rows
+        self.comm = None
+
+    def exchange(self, buf: torch.Tensor, width: int) -> None:
+        """One device holds every row: nothing to exchange."""
 
     def scale(self, name: str | None) -> torch.Tensor | None:
         if name is None:
@@ -184,6 +189,41 @@ class StreamGraph:
         return t
 
 
+class ShardStreamGraph:
+    """One rank's shard for the streaming engine (distributed.py): rows the
+    rank computes are its owned vertices, the layer buffers hold
+    [owned | halo] rows (engine.ShardDeviceGraph's layout), and every
+    aggregation is preceded by one halo exchange of its input (NCCL
+    all-to-all, received in place into the halo block).  Chunks run over
+    the owned rows; features are needed for owned rows only — the first
+    layer's halo rows travel as P0 = X W0."""
+
+    def __init__(self, graph, plan, shard, comm, device, chunk_rows: int, max_width: int):
+        from .engine import ShardDeviceGraph
+        dg = ShardDeviceGraph(graph, plan, shard, comm, device)
+        self.dg, self.comm, self.device, self.shard = dg, comm, device, shard
+        self.num_vertices = plan.num_vertices
+        self.num_edges = int(shard.in_ptr[-1])
+        self.n_rows, self.n_local = shard.n_own, shard.n_local
+        self.symmetric = False
+        self.fwd, self.bwd = dg.fwd, dg.bwd
+        self.fwd.partial(max_width)
+        self.bwd.partial(max_width)
+        self.self_ids = torch.arange(max(self.n_local, 1), dtype=torch.int32, device=device)
+        self.chunks = _chunk_ranges(self.n_rows, int(chunk_rows))
+        in_ptr = np.ascontiguousarray(shard.in_ptr, dtype=np.int64)
+        out_ptr = np.ascontiguousarray(shard.out_ptr, dtype=np.int64)
+        self.fwd_chunks = [_chunk_spec(self.fwd, in_ptr, r0, r1, self.self_ids) for r0, r1 in self.chunks]
+        self.bwd_chunks = [_chunk_spec(self.bwd, out_ptr, r0, r1, self.self_ids)
+                           for r0, r1 in self.chunks]
+
+    def exchange(self, buf: torch.Tensor, width: int) -> None:
+        self.dg.exchange(buf, width)
+
+    def scale(self, name: str | None) -> torch.Tensor | None:
+        return self.dg.scale(name)
+
+
 def _rows(t: torch.Tensor | None, r0: int, r1: int) -> torch.Tensor | None:
     return None if t is None else t[r0:r1]
 
@@ -192,7 +232,8 @@ class StreamingEngine:
     """One GCN epoch with host-resident features (module docstring)."""
 
     def __init__(self, sg: StreamGraph, model, features, labels: np.ndarray,
-                 train_mask: np.ndarray, x_cache_bytes: int | None = None):
+                 train_mask: np.ndarray, x_cache_bytes: int | None = None,
+                 mask_count: int | None = None):
         why = streaming_supported(model)
         if why is not None:
             raise NotImplementedError(why)
@@ -200,14 +241,20 @@ class StreamingEngine:
         self.sg, self.device, self.model = sg, dev, model
         self.dims = model.dims
         self.L = model.num_layers
-        self.V = sg.num_vertices
+        self.V = sg.n_rows          # rows this engine computes (owned rows when sharded)
+        self.NL = sg.n_local        # rows of the layer buffers (owned + halo when sharded)
+        self.comm = sg.comm
+        if self.comm is not None and (model.kind != "gcn" or self.L > 3):
+            raise NotImplementedError("the sharded streaming engine trains GCN models of <= 3 "
+                                      "layers")
         self.mode = model.aggregation_mode
         self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1) for l in range(self.L)]
         self.wts = _Weights(model, dev)
         F = self.dims[0]
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
         self.mask = torch.from_numpy(np.asarray(train_mask, dtype=np.uint8)).to(dev)
-        self.mask_count = int(np.count_nonzero(train_mask))
+        # sharded: the global count (each rank holds its owned rows' mask)
+        self.mask_count = int(np.count_nonzero(train_mask)) if mask_count is None else int(mask_count)
         if self.mask_count == 0:
             raise ValueError("loss mask selects no vertices")
         last = self.cfg[-1]
@@ -219,12 +266,12 @@ class StreamingEngine:
             # [gp | mean^T gp] in backward: twice a layer's output width
             width = max([hid] + [2 * c.ld_out for c in self.cfg])
         # two whole-height layer buffers (zeroed once: pad columns stay 0)
-        self.buf = [ops.zeros_rows(self.V, width, dev), ops.zeros_rows(self.V, width, dev)]
+        self.buf = [ops.zeros_rows(self.NL, width, dev), ops.zeros_rows(self.NL, width, dev)]
         # transform-first last layer: its scaled logit gradient G' is pulled
         # whole, so it needs a third (narrow) buffer; GraphSAGE keeps
         # [G | mean^T G] there
         gw = 2 * last.ld_out if self.sage else last.d_out
-        self.gbuf = ops.zeros_rows(self.V, gw, dev) if last.transform_first else None
+        self.gbuf = ops.zeros_rows(self.NL, gw, dev) if last.transform_first else None
         # deeper hidden layers (l >= 2) kept in pinned host memory
         hw = hid if self.sage else width
         self.host_acts = {l: torch.zeros((self.V, hw), dtype=torch.float32, pin_memory=True)
@@ -391,6 +438,7 @@ class StreamingEngine:
                     x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)))
             else:
                 ops.gemm(B[1][:, : c.ld_in], W[l], P, V, c.d_out, c.d_in, row_scale=s)
+            sg.exchange(P, c.d_out)                               # halo rows of P
             ops.agg_sum(sg.fwd, P, B[1][:, : c.ld_out], c.d_out, post_div_deg=not c.sym,
                         post_scale=s, relu=True)
             if l + 1 in self.host_acts:
@@ -406,6 +454,7 @@ class StreamingEngine:
                 self._backward_first(D, s)
                 break
             H = B[0][:, : c.ld_out]
+            sg.exchange(D, c.d_out)
             ops.agg_sum(sg.bwd, D, H, c.d_out, post_scale=s)            # H = A_hat^T D
             ref_scale = self._pre_scale(l - 1)
             if l == 1:
@@ -415,6 +464,7 @@ class StreamingEngine:
                 P0 = B[1][:, : c0.ld_out]
                 self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
                     x, W[0], P0[r0:r1], r1 - r0, c0.d_out, c0.d_in, row_scale=_rows(s0, r0, r1)))
+                sg.exchange(P0, c0.d_out)
                 for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
                     n = r1 - r0
                     a = self.ac[:n, : c.ld_in]
@@ -426,6 +476,10 @@ class StreamingEngine:
                     self._hidden_grad(l, a, H, B[0], r0, r1, ref_scale)
                 self._stream(HostRows(self.host_acts[l]), step)
             B[0], B[1] = B[1], B[0]
+        if self.comm is not None:      # every layer's weight gradient in one all-reduce
+            self.comm.all_reduce_sum(self.wts.grad_bucket)
+            self.stats.copy_(self.stats_all.sum(dim=0))
+            self.comm.all_reduce_sum(self.stats)
         # ---- SGD (training.py:352-354) ----
         for w, dw in zip(W, dW):
             ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
@@ -451,6 +505,7 @@ class StreamingEngine:
         specs = self.sg.bwd_chunks
 
         spec_of = {r0: sp for (r0, _), sp in zip(self.sg.chunks, specs)}
+        self.sg.exchange(D, c.d_out)
 
         def step(x, r0, r1):
             n = r1 - r0
@@ -473,6 +528,7 @@ class StreamingEngine:
         if not c.transform_first:
             # N = A_hat A (regathered per chunk), logits = N W; gn = (G W^T) * pre_scale
             Q = B[0][:, : c.ld_in]
+            sg.exchange(A, c.d_in)
             for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
                 n = r1 - r0
                 N = self.nc[:n, : c.ld_in]
@@ -488,11 +544,13 @@ class StreamingEngine:
                          row_scale=_rows(self.sg.scale(c.pre_scale), r0, r1))
             post = self._combine(c.sym, prev_ref_scale)
             # dA_{L-1} = relu'(A) (A_hat^T Q) * post, in place over A
+            sg.exchange(Q, c.d_in)
             ops.agg_sum(sg.bwd, Q, A, c.d_in, post_scale=post, mask_ref=A)
             return
         # transform-first: P = A W (whole), logits rows = act-free A_hat P
         P = B[0][:, : c.ld_out]
         ops.gemm(A, W, P, self.V, C, c.d_in, row_scale=s)
+        sg.exchange(P, C)
         G = self.gbuf
         pre = self.sg.scale(c.pre_scale)
         for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
@@ -502,6 +560,7 @@ class StreamingEngine:
             ops.softmax_xent(lg, n, C, self.labels[r0:r1], self.mask[r0:r1], self.mask_count,
                              G[r0:r1], self.stats_all[i], self.partials, grad_scale=pre[r0:r1])
         H = B[0][:, : c.ld_out]
+        sg.exchange(G, C)
         ops.agg_sum(sg.bwd, G, H, C, post_scale=s)                  # H = A_hat^T G'
         for r0, r1 in sg.chunks:
             self._hidden_grad(l, A[r0:r1], H, B[0], r0, r1, prev_ref_scale)
@@ -601,7 +660,11 @@ class StreamingEngine:
 
     def read_stats(self) -> tuple[float, float]:
         """(loss, accuracy) of the last epoch: per-chunk sums added in chunk
-        order on the host (float64)."""
+        order on the host (float64); sharded: the ranks' sums all-reduced at
+        the end of the epoch."""
+        if self.comm is not None:
+            st = self.stats.cpu().numpy()
+            return float(st[2]) / self.mask_count, float(st[3]) / self.mask_count
         s = self.stats_all.cpu().numpy()
         loss = float(np.sum(s[:, 2])) / self.mask_count
         acc = float(np.sum(s[:, 3])) / self.mask_count
@@ -695,27 +758,59 @@ class StreamSession:
     layerwise = True
 
     def __init__(self, dataset, plan, model, chunk_rows: int = DEFAULT_CHUNK_ROWS,
-                 x_cache_bytes: int | None = None, host_cache_bytes: int | None = None):
+                 x_cache_bytes: int | None = None, host_cache_bytes: int | None = None,
+                 comm=None, shard=None, owned_features: torch.Tensor | None = None):
+        """``comm``: this process is one rank of a sharded run (distributed.
+        Communicator): the rank streams its owned rows only; ``shard`` (a
+        ShardPlan, default build_shard_plan) and ``owned_features`` (page-
+        locked [n_own, round_up(F, 4)] rows in the shard's owned order,
+        default gathered from ``dataset.features``) let a caller that never
+        materialises the whole feature matrix supply them."""
         from .model import copy_model
         self.dev = torch.device("cuda", torch.cuda.current_device())
-        key = ("stream_graph", str(self.dev), int(chunk_rows))
-        sg = plan.device_cache.get(key)
-        if sg is None:
-            maxw = max(ld_of(d) for d in model.dims)
-            sg = StreamGraph(dataset.graph, self.dev, chunk_rows, maxw)
-            plan.device_cache[key] = sg
+        self.comm = comm
+        maxw = max(ld_of(d) for d in model.dims)
+        if comm is None:
+            key = ("stream_graph", str(self.dev), int(chunk_rows))
+            sg = plan.device_cache.get(key)
+            if sg is None:
+                sg = StreamGraph(dataset.graph, self.dev, chunk_rows, maxw)
+                plan.device_cache[key] = sg
+            src = feature_rows(dataset, chunk_rows, host_cache_bytes)
+            labels, mask, count = dataset.labels, dataset.train_mask, None
+        else:
+            key = ("stream_shard", comm.rank, comm.world, str(self.dev), int(chunk_rows))
+            sg = plan.device_cache.get(key)
+            if sg is None:
+                if shard is None:
+                    from .distributed import build_shard_plan
+                    shard = build_shard_plan(dataset.graph, plan, comm.rank, comm.world, comm)
+                sg = ShardStreamGraph(dataset.graph, plan, shard, comm, self.dev, chunk_rows, maxw)
+                plan.device_cache[key] = sg
+            owned = sg.shard.owned
+            if owned_features is None:
+                f = dataset.features.shape[1]
+                owned_features = torch.zeros((owned.size, ld_of(f)), dtype=torch.float32,
+                                             pin_memory=True)
+                np.copyto(owned_features.numpy()[:, :f], dataset.features[owned], casting="same_kind")
+            src = HostRows(owned_features)
+            labels = np.asarray(dataset.labels)[owned]
+            mask = np.asarray(dataset.train_mask)[owned]
+            count = int(np.count_nonzero(dataset.train_mask))
         self.sg = sg
         self.dg = sg
         self.model = copy_model(model)
         self.dataset = dataset
         if x_cache_bytes is None and os.environ.get("GRD_X_CACHE_GB"):
             x_cache_bytes = int(float(os.environ["GRD_X_CACHE_GB"]) * 2**30)
-        self.engine = StreamingEngine(sg, self.model, feature_rows(dataset, chunk_rows, host_cache_bytes),
-                                      dataset.labels, dataset.train_mask, x_cache_bytes=x_cache_bytes)
+        self.engine = StreamingEngine(sg, self.model, src, labels, mask, x_cache_bytes=x_cache_bytes,
+                                      mask_count=count)
 
     def reset(self, dataset, model) -> int:
         from .model import copy_model
         eng = self.engine
+        if self.comm is not None:
+            raise NotImplementedError("a sharded streaming session is bound to its dataset")
         eng.set_features(feature_rows(dataset, self.sg.chunks[0][1] if self.sg.chunks else 1))
         from .training import pinned_rows
         eng.labels.copy_(pinned_rows(dataset, "labels", np.asarray(dataset.labels), torch.int32),

@@ -389,10 +389,10 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
             gc.collect()
             torch.cuda.empty_cache()
     if sess is None:
-        stream = layerwise and comm is None and _use_streaming(dataset, model)
+        stream = layerwise and _use_streaming(dataset, model, comm)
         if stream:
             from .stream import StreamSession
-            sess = StreamSession(dataset, plan, model)
+            sess = StreamSession(dataset, plan, model, comm=comm)
         else:
             sess = TrainSession(dataset, plan, model, layerwise=layerwise, comm=comm)
         plan.device_cache[key] = sess
@@ -403,9 +403,11 @@ def session_for(dataset: LabeledDataset, plan: PartitionPlan, model: ModelState,
     return sess
 
 
-def _use_streaming(dataset: LabeledDataset, model: ModelState) -> bool:
+def _use_streaming(dataset: LabeledDataset, model: ModelState, comm=None) -> bool:
     """Stream the layers through HBM (stream.py) when the resident engine's
-    working set does not fit the device; GRD_ENGINE=stream|resident forces."""
+    working set does not fit the device; GRD_ENGINE=stream|resident forces.
+    Sharded: a rank's rows are its owned vertices plus their halo (about
+    three times V / world on the papers-shaped graphs)."""
     import os
     from .stream import resident_bytes, streaming_supported
     forced = os.environ.get("GRD_ENGINE", "")
@@ -413,12 +415,14 @@ def _use_streaming(dataset: LabeledDataset, model: ModelState) -> bool:
         if forced == "stream" and streaming_supported(model) is not None:
             raise NotImplementedError(streaming_supported(model))
         return forced == "stream"
-    if streaming_supported(model) is not None:
+    if streaming_supported(model) is not None or (comm is not None and model.kind != "gcn"):
         return False
     free, _ = torch.cuda.mem_get_info()
     avail = free + torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     g = dataset.graph
-    return resident_bytes(g.num_vertices, g.num_edges, model) > 0.9 * avail
+    rows = g.num_vertices if comm is None else min(g.num_vertices, 3 * g.num_vertices // comm.world)
+    edges = g.num_edges if comm is None else g.num_edges // comm.world
+    return resident_bytes(rows, edges, model) > 0.9 * avail
 
 
 def _offloaded_train(dataset, plan, model, epochs, lr, hierarchy, grad_probe, partition_order):
