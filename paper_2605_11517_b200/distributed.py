@@ -38,7 +38,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["ShardPlan", "Communicator", "assign_partitions", "build_shard_plan"]
+__all__ = ["LabelPlan", "ShardPlan", "Communicator", "assign_partitions", "build_shard_plan",
+           "lean_shard_plan"]
 
 
 def assign_partitions(plan, world: int) -> np.ndarray:
@@ -167,6 +168,64 @@ def build_shard_plan(graph, plan, rank: int, world: int, comm=None) -> ShardPlan
 class _Requests:
     ids: np.ndarray
     counts: np.ndarray
+
+
+class LabelPlan:
+    """What a shard needs of a partition plan, from the labels alone (no
+    whole-graph gather maps): per-partition sizes for the rank assignment,
+    global in-degrees for the degree scales.  Lets every rank of a
+    configs[3]-size run skip the ~16 GB host plan (lean_shard_plan)."""
+
+    def __init__(self, graph, labels: np.ndarray, num_partitions: int):
+        from types import SimpleNamespace
+        self.labels = np.asarray(labels, dtype=np.int32)
+        self.num_partitions = int(num_partitions)
+        self.num_vertices = int(graph.num_vertices)
+        indeg = np.bincount(np.asarray(graph.dst_idx), minlength=self.num_vertices)
+        self.flat = SimpleNamespace(in_degree=indeg.astype(np.int32))
+        self._t = np.bincount(self.labels, minlength=self.num_partitions).astype(np.int64)
+        self._e = np.bincount(self.labels, weights=indeg.astype(np.float64),
+                              minlength=self.num_partitions).astype(np.int64)
+        self.device_cache: dict = {}
+
+    def partition_sizes(self):
+        return self._t, np.zeros_like(self._t), self._e
+
+
+def lean_shard_plan(graph, lplan: LabelPlan, rank: int, world: int, comm=None) -> ShardPlan:
+    """build_shard_plan for a symmetric graph (the generators' graphs are)
+    without the whole plan: owned rows = the targets of the rank's
+    partitions (partition by partition, ascending ids — the plan's perm
+    order), in-neighbours = out-neighbours (neighbours ascending by id
+    instead of by gather position: only the float summation order
+    differs), halo in (owner rank, id) order, send lists exchanged."""
+    n = lplan.num_vertices
+    labels = lplan.labels.astype(np.int64)
+    part_rank = assign_partitions(lplan, world)
+    mine = np.flatnonzero(part_rank == rank)
+    owned = np.flatnonzero(np.isin(labels, mine))
+    owned = owned[np.argsort(labels[owned], kind="stable")]
+    owner = part_rank[labels]
+    ptr, nbr = _csr_rows(graph.src_ptr, graph.dst_idx.astype(np.int64), owned)
+    cand = np.unique(nbr)
+    halo = cand[owner[cand] != rank]
+    halo = halo[np.lexsort((halo, owner[halo]))]
+    halo_owner = owner[halo]
+    lid = np.full(n, -1, dtype=np.int64)
+    lid[owned] = np.arange(owned.size)
+    lid[halo] = owned.size + np.arange(halo.size)
+    local = lid[nbr].astype(np.int32)
+    sp = ShardPlan(
+        rank=rank, world=world, part_rank=part_rank, owned=owned, halo=halo,
+        halo_owner=halo_owner, recv_counts=np.bincount(halo_owner, minlength=world).astype(np.int64),
+        in_ptr=ptr, in_idx=local, out_ptr=ptr, out_idx=local)
+    if comm is not None:
+        requests = comm.exchange_ids(halo, sp.recv_counts)
+        sp.send_counts = requests.counts
+        sp.send_idx = lid[requests.ids].astype(np.int32)
+        if (sp.send_idx < 0).any() or (sp.send_idx >= owned.size).any():
+            raise RuntimeError("halo request for a row this rank does not own")
+    return sp
 
 
 class Communicator:

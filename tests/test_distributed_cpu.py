@@ -109,3 +109,27 @@ def test_shard_plans_cover_the_graph(tmp_path, world):
         for t, st in enumerate(shards):
             if t != r:
                 assert s["send_counts"][t] == st["recv_counts"][r]
+
+
+def test_lean_shard_plan_equals_plan_based_shard_on_symmetric_graphs():
+    """The plan-free shard builder (symmetric graphs) gives the same owned
+    rows, halo, halo owners and per-row neighbour sets as build_shard_plan."""
+    import paper_2605_11517_b200 as g2
+    from paper_2605_11517_b200.distributed import LabelPlan, build_shard_plan, lean_shard_plan
+    g = g2.generate_kronecker(10, 8, seed=3)
+    labels = g2.switching_aware_partition(g, 6, g2.PartitionerParams(seed=1)).labels
+    plan = g2.build_partition_plan(g, labels, 6)
+    lp = LabelPlan(g, labels, 6)
+    for world in (1, 2, 3):
+        for rank in range(world):
+            a = build_shard_plan(g, plan, rank, world)
+            b = lean_shard_plan(g, lp, rank, world)
+            np.testing.assert_array_equal(a.part_rank, b.part_rank)
+            np.testing.assert_array_equal(a.owned, b.owned)
+            np.testing.assert_array_equal(a.halo, b.halo)
+            np.testing.assert_array_equal(a.halo_owner, b.halo_owner)
+            np.testing.assert_array_equal(a.in_ptr, b.in_ptr)
+            for r in range(a.n_own):
+                sa = np.sort(a.in_idx[a.in_ptr[r]:a.in_ptr[r + 1]])
+                sb = np.sort(b.in_idx[b.in_ptr[r]:b.in_ptr[r + 1]])
+                np.testing.assert_array_equal(sa, sb)
