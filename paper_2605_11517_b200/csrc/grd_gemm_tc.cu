@@ -81,6 +81,7 @@ struct Params {
     float* partial; int64_t ld_partial;   // split-K: [z][m][ld_partial]
     float* c2; int64_t ldc2; int64_t split;   // columns >= split (> 0) go to c2
     int tma_store;                  // epilogue chunks leave through shared memory by TMA
+    int kch;                        // K blocks per TMEM accumulation (0: the whole K)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -274,7 +275,8 @@ struct EpiIn {
     float4 o[8], e[8];
 };
 
-__device__ __forceinline__ void epi_prefetch(const Params& p, int64_t row, int64_t col0, EpiIn& in) {
+__device__ __forceinline__ void epi_prefetch(const Params& p, int64_t row, int64_t col0, EpiIn& in,
+                                             bool accumulate) {
     const int64_t n_pad = (p.n + 3) / 4 * 4;
     const bool live = row < p.m && col0 < n_pad && !p.partial;
     const float* crow = p.c + row * p.ldc + col0;
@@ -282,8 +284,8 @@ __device__ __forceinline__ void epi_prefetch(const Params& p, int64_t row, int64
     for (int j4 = 0; j4 < 8; ++j4) {
         const int64_t n = col0 + 4 * j4;
         const bool ok = live && n < n_pad;
-        in.o[j4] = (ok && p.accumulate) ? *reinterpret_cast<const float4*>(crow + 4 * j4)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        in.o[j4] = (ok && accumulate) ? *reinterpret_cast<const float4*>(crow + 4 * j4)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
         in.e[j4] = (ok && p.relu_ref) ? __ldg(reinterpret_cast<const float4*>(p.relu_ref + row * p.ld_relu_ref + n))
                                       : make_float4(1.f, 1.f, 1.f, 1.f);
     }
@@ -377,6 +379,23 @@ __device__ __forceinline__ void epi_stage_tma(const Params& p, const float (&v)[
     }
 }
 
+// A K chunk's partial sum (not the tile's last chunk): C = C_so_far + acc,
+// no epilogue operators yet; the next chunk reads it back (same thread,
+// same addresses, the tile hot in L2).
+__device__ __forceinline__ void epi_store_raw(const Params& p, const float (&v)[32], int64_t row, int64_t col0,
+                                              const EpiIn& in) {
+    if (row >= p.m) return;
+    const int64_t n_pad = (p.n + 3) / 4 * 4;
+    float* crow = p.c + row * p.ldc + col0;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        if (col0 + j >= n_pad) continue;
+        const float4 oo = in.o[j / 4];
+        *reinterpret_cast<float4*>(crow + j) =
+            make_float4(v[j] + oo.x, v[j + 1] + oo.y, v[j + 2] + oo.z, v[j + 3] + oo.w);
+    }
+}
+
 // Epilogue warps' loop over the tiles of this CTA (both kernels): TMEM
 // accumulator `acc` of the i-th tile with K work, drained chunk by chunk.
 template <bool kPair, bool kSplit, class TileFn>
@@ -389,53 +408,66 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
     const int half = (warp - kEpiWarp0) >> 2;             // which interleaved column chunks
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const int bn = p.bn;
+    const int64_t nkb = (p.k + kBK - 1) / kBK;
+    // K chunks accumulated separately (p.kch): each chunk's TMEM partial is
+    // added to C with round-to-nearest fp32 adds, the epilogue operators
+    // apply with the last chunk (kSplit / split-K tiles: one chunk)
+    const int nch = (!kSplit && p.kch > 0 && !p.partial) ? static_cast<int>((nkb + p.kch - 1) / p.kch) : 1;
     int64_t i = 0;
     for (int64_t t = t0; t < ntiles; t += tstep) {
         int64_t m0, n0;
         int z;
         bool has_k;
         tile_of(t, m0, n0, z, has_k);
-        const int acc = static_cast<int>(i & 1);
         const int64_t row0 = m0 + q * 32;
         const int64_t n_pad = (p.n + 3) / 4 * 4;
-        bool waited = false;
-        for (int c0 = 32 * half; c0 < bn; c0 += 64) {
-            EpiIn in;
-            epi_prefetch(p, row0 + lane, n0 + c0, in);
-            if (has_k && !waited) {
-                mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                waited = true;
-            }
-            float v[32];
-            if (has_k) {
-                tmem_ld32(tmem + lane_base + static_cast<uint32_t>(acc * bn + c0), v);
-            } else {
+        const int chunks = has_k ? nch : 1;
+        for (int ch = 0; ch < chunks; ++ch) {
+            const bool last = ch == chunks - 1;
+            const int acc = static_cast<int>(i & 1);
+            bool waited = false;
+            for (int c0 = 32 * half; c0 < bn; c0 += 64) {
+                EpiIn in;
+                epi_prefetch(p, row0 + lane, n0 + c0, in, ch > 0 || p.accumulate);
+                if (has_k && !waited) {
+                    mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    waited = true;
+                }
+                float v[32];
+                if (has_k) {
+                    tmem_ld32(tmem + lane_base + static_cast<uint32_t>(acc * bn + c0), v);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                }
+                if (row0 >= p.m || n0 + c0 >= n_pad) continue;   // warp-uniform
+                if (!last) {
+                    epi_store_raw(p, v, row0 + lane, n0 + c0, in);
+                    continue;
+                }
+                if (tma && chunks == 1) {
+                    if (lane == 0) tma_store_wait_read();     // the staging tile's last store has read it
+                    __syncwarp();
+                    epi_stage_tma(p, v, row0 + lane, n0 + c0, in, stage, lane);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        tma_store_2d(map_c, stage, static_cast<int32_t>(n0 + c0), static_cast<int32_t>(row0));
+                    continue;
+                }
+                epi_store_direct<kSplit>(p, v, row0 + lane, n0 + c0, z, in);
             }
-            if (row0 >= p.m || n0 + c0 >= n_pad) continue;   // warp-uniform
-            if (tma) {
-                if (lane == 0) tma_store_wait_read();     // the staging tile's last store has read it
-                __syncwarp();
-                epi_stage_tma(p, v, row0 + lane, n0 + c0, in, stage, lane);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0)
-                    tma_store_2d(map_c, stage, static_cast<int32_t>(n0 + c0), static_cast<int32_t>(row0));
-                continue;
+            if (has_k) {
+                // a warp without columns in this tile (bn <= 32) still waits for
+                // the accumulator before releasing it: no arrival may run ahead
+                // into the buffer's next phase
+                if (!waited) mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                if (kPair) mbar_arrive_cluster(tempty + acc, 0);
+                else mbar_arrive(tempty + acc);
+                ++i;
             }
-            epi_store_direct<kSplit>(p, v, row0 + lane, n0 + c0, z, in);
-        }
-        if (has_k) {
-            // a warp without columns in this tile (bn <= 32) still waits for
-            // the accumulator before releasing it: no arrival may run ahead
-            // into the buffer's next phase
-            if (!waited) mbar_wait(tfull + acc, static_cast<uint32_t>((i / 2) & 1));
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            if (kPair) mbar_arrive_cluster(tempty + acc, 0);
-            else mbar_arrive(tempty + acc);
-            ++i;
         }
     }
     if (tma && lane == 0) tma_store_wait_all();
@@ -707,7 +739,18 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     asm volatile("tcgen05.fence::after_thread_sync;");
                 }
                 uint32_t tacc = tmem + static_cast<uint32_t>(acc * bn);
+                const int64_t kch = (!kFresh && p.kch > 0 && !p.partial) ? p.kch : 0;
                 for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+                    if (kch && kb > 0 && kb % kch == 0) {
+                        // next K chunk: publish this one, move to the other accumulator
+                        if constexpr (kPair) mma_commit_pair(tfull + acc);
+                        else mma_commit(tfull + acc);
+                        ++i;
+                        acc = static_cast<int>(i & 1);
+                        if (i >= 2) mbar_wait(tempty + acc, static_cast<uint32_t>((i / 2 - 1) & 1));
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        tacc = tmem + static_cast<uint32_t>(acc * bn);
+                    }
                     if constexpr (kFresh) {
                         // a fresh accumulator per K block (epilogue_fresh sums them)
                         acc = static_cast<int>(fresh & 1);
@@ -728,7 +771,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         const uint64_t dal = make_desc(al + kk * a_step, a_lbo, a_sbo, a_lay);
                         const uint64_t dbh = make_desc(bh + kk * b_step, b_lbo, b_sbo, b_lay);
                         const uint64_t dbl = make_desc(bl + kk * b_step, b_lbo, b_sbo, b_lay);
-                        const uint32_t keep = (kk > 0 || (!kFresh && kb > 0)) ? 1u : 0u;
+                        const uint32_t keep = (kk > 0 || (!kFresh && (kch ? kb % kch : kb) > 0)) ? 1u : 0u;
                         if constexpr (kPair) {
                             mma_tf32_pair(tacc, dal, dbh, idesc, keep);
                             mma_tf32_pair(tacc, dah, dbl, idesc, 1u);
@@ -1137,6 +1180,23 @@ inline int fresh_pref() {
     return v;
 }
 
+inline int kch_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_KCH");
+        v = e ? atoi(e) : 4;
+    }
+    return v;
+}
+inline int64_t kmax_pref() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_KMAX");
+        v = e ? atoll(e) : 192;
+    }
+    return v;
+}
+
 // epilogue chunks stored by TMA through shared memory (GRD_GEMM_TMA_STORE = 1 / 0)
 inline int tma_store_pref() {
     static int v = -1;
@@ -1307,12 +1367,20 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     // B resident in shared memory: a packed weight operand with one N tile,
     // no split-K, that leaves room for >= 3 A-only stages (GRD_GEMM_BRES=0
     // keeps B in the stage ring)
+    // K chunks accumulated separately when K is deeper than the chunk limit
+    // (GRD_GEMM_KCH K blocks per accumulation, default 4 = 128; GRD_GEMM_KMAX
+    // the deepest single accumulation, default 192): tcgen05's fused
+    // accumulation truncates, so the error grows with the chain length
+    // (profiles/r02_gemm_precision.md)
+    p.kch = 0;
+    if (!p.partial && p.split == 0 && kch_pref() > 0 && g.k > kmax_pref()) p.kch = kch_pref();
     // TMA-store epilogue (plain C output: no split-K partial, no split c2)
     CUtensorMap map_c = map_a;
     p.tma_store = 0;
     // measured (tools/gemm_shapes.py): -12..-33 % at N tiles of 128 / 256,
     // +17..26 % at 48 / 192 (fewer stages fit beside the staging tiles)
-    if (tma_store_pref() && p.bn % 128 == 0 && !p.partial && p.split == 0 && g.c && (g.ldc % 4) == 0 &&
+    if (tma_store_pref() && p.kch == 0 && p.bn % 128 == 0 && !p.partial && p.split == 0 && g.c &&
+        (g.ldc % 4) == 0 &&
         make_map(&map_c, g.c, g.m, (g.n + 3) / 4 * 4, g.ldc, 32, 32))
         p.tma_store = 1;
     const uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;

@@ -1,5 +1,6 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; exec > gpurun_out/dbg.log 2>&1
-GRD_BENCH_BACKEND=gloo timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --workload papers_s22 --steps 3 --warmup 3 > gpurun_out/bench_s22_n2.json 2> gpurun_out/bench_s22_n2.err; echo "n2 rc=$?"
-tail -c 1500 gpurun_out/bench_s22_n2.json; tail -20 gpurun_out/bench_s22_n2.err
-timeout 600 python bench.py --workload papers_s22 --steps 3 --warmup 3 --no-engines --no-cpu-baseline > gpurun_out/bench_s22_n1.json 2>&1; echo "n1 rc=$?"
-python -c "import json; d=json.load(open('gpurun_out/bench_s22_n1.json')); print(d['ms_per_step'], d['config']['loss_last_step'])"
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_papers_full.json 2> gpurun_out/bench_papers_full.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/ref_papers_full.json 2>&1; echo "ref rc=$?"
+for w in products_sage products_gat config1 papers_gcn; do timeout 900 python bench.py --workload $w --steps 10 --warmup 3 --no-engines > gpurun_out/bench_$w.json 2>&1; echo "$w rc=$?"; done
