@@ -1183,8 +1183,11 @@ inline int fresh_pref() {
 inline int kch_pref() {
     static int v = -1;
     if (v < 0) {
+        // in-kernel chunks (C partials re-read from L2 per chunk) measured
+        // slower than the host-side split at the products shapes (44.7 vs
+        // 43.5 ms per epoch: the epilogue drains every chunk): opt-in
         const char* e = getenv("GRD_GEMM_KCH");
-        v = e ? atoi(e) : 4;
+        v = e ? atoi(e) : 0;
     }
     return v;
 }
@@ -1367,10 +1370,10 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     // B resident in shared memory: a packed weight operand with one N tile,
     // no split-K, that leaves room for >= 3 A-only stages (GRD_GEMM_BRES=0
     // keeps B in the stage ring)
-    // K chunks accumulated separately when K is deeper than the chunk limit
-    // (GRD_GEMM_KCH K blocks per accumulation, default 4 = 128; GRD_GEMM_KMAX
-    // the deepest single accumulation, default 192): tcgen05's fused
-    // accumulation truncates, so the error grows with the chain length
+    // K chunks accumulated separately inside the kernel when K is deeper
+    // than GRD_GEMM_KMAX (GRD_GEMM_KCH K blocks per accumulation; opt-in, the
+    // default split is ops.gemm's, one launch per 128-deep chunk): tcgen05's
+    // fused accumulation truncates, so the error grows with the chain length
     // (profiles/r02_gemm_precision.md)
     p.kch = 0;
     if (!p.partial && p.split == 0 && kch_pref() > 0 && g.k > kmax_pref()) p.kch = kch_pref();

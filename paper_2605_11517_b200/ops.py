@@ -218,15 +218,19 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
             lambda: _lib.check(_lib.lib().grd_agg_sum(ctypes.byref(a), stream_ptr()), "agg_sum"))
 
 
-# Deep K is accumulated in chunks inside the GEMM kernel (GRD_GEMM_KCH /
-# GRD_GEMM_KMAX, grd_gemm_tc.cu): tcgen05's fused accumulation truncates, so
-# the 3xTF32 error grows with the number of MMAs summed into one accumulator
-# and is biased; gradients that sum many cancelling terms amplify it
-# (GraphSAGE at F = 100 / H = 256: 1.4e-3 on layer 0's weight gradient with
-# one K = 200 accumulation).  The host-side split below (each chunk a
-# separate launch accumulating into C) is kept as a measurement aid:
-# GRD_GEMM_KCHUNK=128 enables it (default 0).
-_KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "0"))
+# K chunk of one tensor-core accumulation (GRD_GEMM_KCHUNK; 0 = whole K).
+# tcgen05's fused accumulation truncates, so the 3xTF32 error grows with the
+# number of MMAs summed into one accumulator (~2e-6 relative at K = 128,
+# ~4e-6 at K = 512 on random data) and is biased; gradients that sum many
+# cancelling terms amplify it (GraphSAGE at F = 100 / H = 256: 1.4e-3 on
+# layer 0's weight gradient).  K deeper than _KMAX (192: the GraphSAGE
+# K = 200 case needs the split, the papers K = 172 product does not,
+# tools/prec_matrix.py) is split into 128-deep chunks whose partials the
+# epilogue adds to C with round-to-nearest fp32 adds (its accumulate path);
+# the row scale / element multiply / ReLU apply with the last chunk.  (An
+# in-kernel variant, GRD_GEMM_KCH, measured slower.)  Weight gradients
+# (trans_a) use in-kernel fresh accumulators instead (GRD_WGRAD_FRESH).
+_KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "128"))
 _KMAX = int(os.environ.get("GRD_GEMM_KMAX", "192"))
 
 

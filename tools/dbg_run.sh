@@ -1,6 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; exec > gpurun_out/dbg.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_papers_full.json 2> gpurun_out/bench_papers_full.err; echo "bench rc=$?"
-timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/ref_papers_full.json 2>&1; echo "ref rc=$?"
-for w in products_sage products_gat config1 papers_gcn; do timeout 900 python bench.py --workload $w --steps 10 --warmup 3 --no-engines > gpurun_out/bench_$w.json 2>&1; echo "$w rc=$?"; done
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x 2>&1 | tail -3
+timeout 300 python tools/gemm_prec_shapes.py 2>&1 | grep -E "16384"
+timeout 300 python tools/prec_matrix.py sage 2>&1 | tail -1
+timeout 300 python tools/prec_matrix.py papers 2>&1 | tail -1
+timeout 300 python tools/gemm_shapes.py products | python -c "import json,sys; d=json.load(sys.stdin); [print(k, v['ms'], v.get('frac')) for k,v in d.items()]"
+timeout 900 python bench.py --workload products_sage --steps 10 --warmup 3 --no-engines --no-cpu-baseline > gpurun_out/bench_ps.json 2>&1; python -c "import json; d=json.load(open('gpurun_out/bench_ps.json')); print('products', d['ms_per_step'], {k: v['ms_per_epoch'] for k, v in d['kernels'].items()})"
