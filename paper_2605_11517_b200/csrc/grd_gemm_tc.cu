@@ -1248,7 +1248,13 @@ using namespace grd_tc;
 
 int64_t grd_tc_pack_elems(int64_t n, int64_t k) {
     const int bn = pick_bn(n);
-    return ((n + bn - 1) / bn) * ((k + kBK - 1) / kBK) * 2 * int64_t(bn) * kBK;
+    // fp32 elements of the packed weight operand: the 3xTF32 layout (32-deep
+    // K blocks of fp32 hi|lo) or the bf16x3 one (64-deep blocks of bf16
+    // hi|lo = half as many fp32 slots per element, but K padded to 64),
+    // whichever is larger
+    const int64_t tf32 = ((n + bn - 1) / bn) * ((k + kBK - 1) / kBK) * 2 * int64_t(bn) * kBK;
+    const int64_t bf16 = ((n + bn - 1) / bn) * ((k + kBK16 - 1) / kBK16) * int64_t(bn) * kBK16;
+    return tf32 > bf16 ? tf32 : bf16;
 }
 
 int grd_tc_bn(int64_t n) { return pick_bn(n); }
@@ -1312,7 +1318,9 @@ static cudaError_t gemm_bf16x3(const GrdTcGemm& g, cudaStream_t st) {
 }
 
 cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
-    if (g.bf16) return gemm_bf16x3(g, st);
+    // the opt-in bf16x3 kernel serves plain products only (split outputs and
+    // accumulating launches — the K-chunked ones — stay 3xTF32)
+    if (g.bf16 && !g.c2 && !g.accumulate) return gemm_bf16x3(g, st);
     Params p{};
     p.m = g.m;
     p.n = g.n;
