@@ -1067,7 +1067,10 @@ extern "C" int grd_gemm(const grd_gemm_args* args, void* stream) {
     if (!g.workspace || g.workspace_elems < need)
         return fail(kErrArg, "gemm: workspace needs %lld floats", (long long)need);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    t.bf16 = !g.trans_a && grd_tc_bf16x3();
+    // opt-in bf16x3 serves plain products only (split outputs and
+    // accumulating launches — the K-chunked ones — stay 3xTF32); the packed
+    // operand's layout follows the same decision
+    t.bf16 = !g.trans_a && !g.c2 && !g.accumulate && grd_tc_bf16x3();
     cudaError_t e = grd_tc_pack_b(g.b, g.ldb, g.trans_b, g.n, g.k, g.workspace, st, t.bf16);
     if (e == cudaSuccess) {
         t.b_packed = g.workspace;

@@ -1318,9 +1318,7 @@ static cudaError_t gemm_bf16x3(const GrdTcGemm& g, cudaStream_t st) {
 }
 
 cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
-    // the opt-in bf16x3 kernel serves plain products only (split outputs and
-    // accumulating launches — the K-chunked ones — stay 3xTF32)
-    if (g.bf16 && !g.c2 && !g.accumulate) return gemm_bf16x3(g, st);
+    if (g.bf16) return gemm_bf16x3(g, st);   // grd_gemm decides (and packs B) for it
     Params p{};
     p.m = g.m;
     p.n = g.n;
