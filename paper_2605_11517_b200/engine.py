@@ -357,6 +357,27 @@ class DevicePartition:
             self._bwd = AggSpec.build(csc_ptr, csc_rows, self.dev, self_idx=self_t)
         return self._bwd
 
+    def gat_specs(self):
+        """(fwd, pull, edge_perm) of a GAT layer over this partition, in
+        gather-position space: the forward rows are the targets with output /
+        self row self_pos[t] (so t_v, the self loop, O and gO all live at the
+        target's gather row), the pull's rows are the gather rows with their
+        targets' gather rows as neighbours (ascending target), and edge_perm
+        maps each pull edge to its forward edge (per-edge attention).  A
+        gather row that is not a target gets no self term in the backward:
+        its gO row and delta_self entry are zero."""
+        if getattr(self, "_gat", None) is None:
+            tgt_ptr, src_pos, self_pos = self._csr
+            fwd = AggSpec.build(tgt_ptr, src_pos, self.dev, out_idx=self_pos)
+            tgt = np.repeat(np.arange(self.num_targets, dtype=np.int64), np.diff(tgt_ptr))
+            order = np.argsort(src_pos, kind="stable")
+            ptr = np.zeros(self.num_gather + 1, dtype=np.int64)
+            np.cumsum(np.bincount(src_pos, minlength=self.num_gather), out=ptr[1:])
+            pull = AggSpec.build(ptr, self_pos[tgt[order]], self.dev)
+            perm = torch.from_numpy(np.concatenate([order.astype(np.int32), np.zeros(1, np.int32)]))
+            self._gat = (fwd, pull, perm.to(self.dev))
+        return self._gat
+
     @classmethod
     def from_topology(cls, topo, device) -> "DevicePartition":
         return cls(topo.partition_id, topo.targets, topo.gather_map, topo.tgt_ptr, topo.src_pos,
@@ -1014,14 +1035,37 @@ class LayerOps:
         self.dims = model.dims
         self.L = model.num_layers
         self.cfg = [_LayerCfg(l, self.dims, model.aggregation_mode, model.row_normalize,
-                              l == self.L - 1) for l in range(self.L)]
+                              l == self.L - 1, model.heads) for l in range(self.L)]
+        if model.kind == "gat" and model.row_normalize:
+            raise NotImplementedError("GAT layers have no row normalisation")
         self.wts = weights if weights is not None else _Weights(model, device)
+
+    # ------------------------------------------ weight-gradient plumbing --
+    def grad_sink(self, l: int) -> torch.Tensor:
+        """Where a layer's per-partition weight gradients are summed: dW, or
+        GAT's fused dW_ext (linear in the partition sums, converted once)."""
+        return self.wts.dwext[l] if self.wts.gat else self.wts.dw[l]
+
+    def sgd(self, lr: float) -> None:
+        """W -= lr dW for every layer (GAT: dW, datt from dW_ext first)."""
+        wt = self.wts
+        for l in range(self.L):
+            if wt.gat:
+                c = self.cfg[l]
+                d_in, dh, dhp = wt.shape[l]
+                ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp,
+                                    wt.dw[l], wt.datt[l], lr)
+            else:
+                w, dw = wt.w[l], wt.dw[l]
+                ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
 
     def layer_forward(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
         """out = act(norm(aggregate(GA)) @ W) for one partition (training.py:86-100)."""
         c = self.cfg[l]
         if c.sage:
             return self._sage_forward(l, ga, part)
+        if c.gat:
+            return self._gat_forward(l, ga, part)
         W = self.wts.w[l]
         pre = self._pre(l, ga, part)
         if c.rownorm:
@@ -1061,7 +1105,89 @@ class LayerOps:
         if c.sage:
             return np.concatenate([to_host(grad_w[:, : c.ld_out], c.d_out, c.d_in),
                                    to_host(grad_w[:, c.ld_out:], c.d_out, c.d_in)], axis=1)
+        if c.gat:      # dW_ext -> (dW, datt) stacked as the model's [W ; a_src ; a_dst]
+            d_in, dh, dhp = self.wts.shape[l]
+            dw = torch.zeros_like(self.wts.w[l])
+            datt = torch.zeros_like(self.wts.att[l])
+            ops.gat_param_grads(grad_w, self.wts.w[l], self.wts.att[l], d_in, c.heads, dh, dhp,
+                                dw, datt, 0.0)
+            w = to_host(dw, c.heads * dhp, d_in).reshape(d_in, c.heads, dhp)[:, :, :dh]
+            a = datt.double().cpu().numpy()[:, :, :dh]
+            return np.concatenate([w.reshape(d_in, c.heads * dh), a.reshape(2, c.heads * dh)])
         return to_host(grad_w, c.d_out, c.d_in)
+
+    # ------------------------------------------------- GAT, per partition --
+    # The layer over one partition's gathered rows GA (G rows): P_ext = GA
+    # W_ext, the edge softmax over each target's in-edges + self loop, the
+    # attention-weighted sum; every per-vertex quantity lives at the
+    # target's gather row (DevicePartition.gat_specs), the T output rows are
+    # gathered from there.
+    def _gat_regather(self, l: int, ga: torch.Tensor, part: DevicePartition):
+        """(P_ext, alpha, alpha_self, O) of one partition; O per head, in
+        gather-row space, ReLU applied for hidden layers."""
+        c = self.cfg[l]
+        wt = self.wts
+        d_in, dh, dhp = wt.shape[l]
+        G, dev = part.num_gather, self.device
+        fwd, _, _ = part.gat_specs()
+        ops.gat_build_wext(wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.wext[l])
+        pext = ops.zeros_rows(G, c.ld_ext, dev)
+        ops.gemm(ga, wt.wext[l], pext, G, c.n_ext, c.d_in)
+        alpha = torch.zeros(max(fwd.nnz * c.heads, 1), dtype=torch.float32, device=dev)
+        alpha_self = torch.zeros(max(G * c.heads, 1), dtype=torch.float32, device=dev)
+        ops.gat_softmax(fwd, pext, c.heads, c.dhp, alpha, alpha_self)
+        o = ops.zeros_rows(G, c.hdp, dev)
+        ops.agg_sum(fwd, pext[:, : c.hdp], o, c.hdp, edge_w=alpha, self_w=alpha_self,
+                    heads=c.heads, head_ld=c.dhp, relu=not c.last)
+        return pext, alpha, alpha_self, o
+
+    def _gat_forward(self, l: int, ga: torch.Tensor, part: DevicePartition) -> torch.Tensor:
+        c = self.cfg[l]
+        T = part.num_targets
+        out = ops.zeros_rows(T, c.d_out, self.device)
+        if T == 0:
+            return out
+        _, _, _, o = self._gat_regather(l, ga, part)
+        if c.last:
+            ot = ops.zeros_rows(T, c.hdp, self.device)
+            ops.gather_rows(o, part.fwd.self_idx, ot, c.hdp)
+            ops.head_mean(ot, T, c.heads, c.dh, c.dhp, out)
+        else:
+            ops.gather_rows(o, part.fwd.self_idx, out, c.hdp)
+        return out
+
+    def _gat_backward(self, l: int, ga: torch.Tensor, a_out: torch.Tensor, grad_out: torch.Tensor,
+                      part: DevicePartition) -> tuple[torch.Tensor, torch.Tensor]:
+        """Regather P_ext / attention / O from GA, then: delta and dt (edge
+        softmax backward), dP = sum alpha gO and ds over the pull, dW_ext =
+        GA^T dP_ext, grad_GA = dP_ext W_ext^T."""
+        c = self.cfg[l]
+        wt = self.wts
+        T, G, dev = part.num_targets, part.num_gather, self.device
+        grad_w = torch.zeros_like(wt.wext[l])
+        grad_ga = ops.zeros_rows(G, c.d_in, dev)
+        if T == 0:
+            return grad_ga, grad_w
+        fwd, pull, perm = part.gat_specs()
+        pext, alpha, alpha_self, o = self._gat_regather(l, ga, part)
+        gt = ops.zeros_rows(T, c.hdp, dev)
+        if c.last:
+            ops.head_mean(grad_out, T, c.heads, c.dh, c.dhp, gt, backward=True)
+        else:      # ReLU mask from the layer's output, so gO.relu(O) = gO.O
+            ops.mask_scale_rows(grad_out, gt, T, c.d_out, ref=a_out)
+        go = ops.zeros_rows(G, c.hdp, dev)
+        ops.scatter_add_rows(gt, part.fwd.self_idx, go, c.hdp)
+        delta = torch.zeros_like(alpha)
+        delta_self = torch.zeros_like(alpha_self)
+        gext = ops.zeros_rows(G, c.ld_ext, dev)
+        ops.gat_softmax_bwd(fwd, pext, c.heads, c.dhp, alpha, alpha_self, go, o, delta,
+                            delta_self, gext)
+        ops.agg_sum(pull, go, gext[:, : c.hdp], c.hdp, edge_w=alpha, edge_w_perm=perm,
+                    self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
+        ops.gat_src_grad(pull, c.heads, c.dhp, perm, delta, delta_self, gext)
+        ops.wgrad_sgd(ga, gext, grad_w, c.d_in, c.n_ext, G)
+        ops.gemm(gext, wt.wext[l], grad_ga, G, c.d_in, c.n_ext, trans_b=True)
+        return grad_ga, grad_w
 
     # ---------------------------------------------- GraphSAGE-mean, per partition --
     # out_t = X_t W_root + mean_{u in in(t)} X_u W_nbr over the partition's
@@ -1119,6 +1245,8 @@ class LayerOps:
         c = self.cfg[l]
         if c.sage:
             return self._sage_backward(l, ga, a_out, grad_out, part)
+        if c.gat:
+            return self._gat_backward(l, ga, a_out, grad_out, part)
         W = self.wts.w[l]
         dev = self.device
         T, G = part.num_targets, part.num_gather
@@ -1197,8 +1325,8 @@ class PartitionEngine(_EngineBase):
         self.check_loss(epoch)
         if hierarchy is not None:
             hierarchy.loss_stage()
-        for dw in self.wts.dw:
-            dw.zero_()
+        for l in range(self.L):
+            self.ops.grad_sink(l).zero_()
         for l in reversed(range(self.L)):
             c = self.cfg[l]
             x = self.layer_input(l)
@@ -1224,7 +1352,7 @@ class PartitionEngine(_EngineBase):
                 if grad_probe is not None:
                     grad_probe(epoch, l, pid, to_host(grad_ga, c.d_in),
                                self.ops.grad_w_host(l, grad_w, to_host))
-                self._add_into(self.wts.dw[l], grad_w)
+                self._add_into(self.ops.grad_sink(l), grad_w)
                 if l > 0:
                     ops.scatter_add_rows(grad_ga, dg.partition(pid).gather_map, self.grad_prev, c.d_in)
             if l > 0 and self.dmask[l] is not None:
@@ -1232,9 +1360,7 @@ class PartitionEngine(_EngineBase):
             if hierarchy is not None:
                 hierarchy.end_backward_layer(l)
             self.grad_cur, self.grad_prev = self.grad_prev, self.grad_cur
-        for l in range(self.L):
-            w, dw = self.wts.w[l], self.wts.dw[l]
-            ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
+        self.ops.sgd(lr)
         if hierarchy is not None:
             hierarchy.end_epoch()
 

@@ -60,11 +60,12 @@ class _AscendingAccumulator:
 
 
 class OffloadedTrainer:
-    """GCN partition-wise training whose data lives in the SSO tiers."""
+    """Partition-wise training (GCN, GraphSAGE, GAT layers) whose data lives
+    in the SSO tiers."""
 
     def __init__(self, dataset, plan, model, session, device):
-        if model.kind == "gat" or model.row_normalize or model.dropout_rate:
-            raise NotImplementedError("the offloaded path trains GCN and GraphSAGE layers "
+        if model.row_normalize or model.dropout_rate:
+            raise NotImplementedError("the offloaded path trains GCN, GraphSAGE and GAT layers "
                                       "without row normalisation / dropout")
         if list(session.dims) != list(model.dims):
             raise ValueError(f"tier session dims {session.dims} != model dims {model.dims}")
@@ -121,9 +122,9 @@ class OffloadedTrainer:
         if not np.isfinite(loss):
             raise ValueError(f"non-finite loss {loss} at epoch {epoch}; "
                              f"reduce the learning rate or check the inputs")
-        wts = self.lops.wts
-        for dw in wts.dw:
-            dw.zero_()
+        lops = self.lops
+        for l in range(self.L):
+            lops.grad_sink(l).zero_()
         for l in reversed(range(self.L)):
             d_in, d_out = self.dims[l], self.dims[l + 1]
             acc = _AscendingAccumulator(s, self.P, d_in) if l > 0 else None
@@ -149,10 +150,9 @@ class OffloadedTrainer:
                 if grad_probe is not None:
                     grad_probe(epoch, l, pid, to_host(probes[pid], d_in),
                                self.lops.grad_w_host(l, grad_w[pid], to_host))
-                self._add(wts.dw[l], grad_w[pid])
+                self._add(lops.grad_sink(l), grad_w[pid])
             s.end_backward_layer(l)
-        for w, dw in zip(wts.w, wts.dw):
-            ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
+        lops.sgd(lr)
         s.end_epoch()
 
     _eye: dict = {}

@@ -311,9 +311,6 @@ def partitioned_train(dataset: LabeledDataset, plan: PartitionPlan, model: Model
         raise ValueError("plan was built for a different graph")
     observed = hierarchy is not None or use_snapshots or grad_probe is not None \
         or partition_order is not None
-    if observed and model.kind == "gat":  # GAT: layer-wise engine only
-        raise NotImplementedError("per-partition observers (hierarchy, probes, snapshots, "
-                                  "partition_order) are implemented for GCN and GraphSAGE layers")
     from .hierarchy import TierSession
     if isinstance(hierarchy, TierSession) and hierarchy.execute:
         if use_snapshots:
