@@ -232,6 +232,8 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
 # (trans_a) use in-kernel fresh accumulators instead (GRD_WGRAD_FRESH).
 _KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "128"))
 _KMAX = int(os.environ.get("GRD_GEMM_KMAX", "192"))
+# whether input-gradient GEMMs (A @ W^T) are split too (GRD_GEMM_KSPLIT_TB)
+_KSPLIT_TB = os.environ.get("GRD_GEMM_KSPLIT_TB", "1") != "0"
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
@@ -240,7 +242,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: i
     """c[:m,:n] (=|+=) epi(opA(a) @ opB(b)) over the first k of the inner dim;
     with c2, columns >= split land in c2[:, col - split] instead."""
     k = int(k)
-    if _KCHUNK and k > max(_KCHUNK, _KMAX) and not trans_a and c2 is None:
+    if _KCHUNK and k > max(_KCHUNK, _KMAX) and not trans_a and c2 is None and (_KSPLIT_TB or not trans_b):
         starts = list(range(0, k, _KCHUNK))
         for i, k0 in enumerate(starts):
             k1 = min(k, k0 + _KCHUNK)

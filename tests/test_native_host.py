@@ -253,3 +253,33 @@ def test_labels_mask_without_features_match_dataset(n, F, C, seed):
     labels, mask = random_labels_mask(n, F, C, seed)
     np.testing.assert_array_equal(labels, ds.labels)
     np.testing.assert_array_equal(mask, ds.train_mask)
+
+
+@pytest.mark.parametrize("scale,deg,P", [(8, 6, 3), (10, 8, 5)])
+def test_gat_partition_specs_are_consistent(scale, deg, P):
+    """The per-partition GAT specs (engine.DevicePartition.gat_specs, host
+    side on CPU tensors): the forward rows are the targets with output row
+    self_pos; every pull edge of gather row g maps (edge_perm) to a forward
+    edge whose source is g and whose target's gather row is the pull
+    edge's neighbour, each forward edge exactly once, targets ascending."""
+    from paper_2605_11517_b200.engine import DevicePartition
+    g = generate_kronecker(scale, deg, seed=scale)
+    plan = build_partition_plan(g, random_partition(g.num_vertices, P, 1), P)
+    for q in range(P):
+        part = DevicePartition.from_plan(plan, q, "cpu")
+        fwd, pull, perm = part.gat_specs()
+        tgt_ptr, src_pos, self_pos = part._csr
+        assert np.array_equal(fwd.out_idx.numpy(), self_pos)
+        E = src_pos.size
+        perm = perm.numpy()[:E]
+        assert np.array_equal(np.sort(perm), np.arange(E))
+        tgt_of_edge = np.repeat(np.arange(part.num_targets), np.diff(tgt_ptr))
+        ptr = pull.row_ptr.numpy()
+        idx = pull.idx.numpy()
+        assert ptr[-1] == E and ptr.size == part.num_gather + 1
+        rows = np.repeat(np.arange(part.num_gather), np.diff(ptr))
+        assert np.array_equal(src_pos[perm], rows)
+        assert np.array_equal(self_pos[tgt_of_edge[perm]], idx)
+        for r in range(part.num_gather):   # targets ascending within a pull row
+            t = tgt_of_edge[perm[ptr[r]:ptr[r + 1]]]
+            assert np.all(np.diff(t) >= 0)

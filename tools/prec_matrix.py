@@ -16,7 +16,7 @@ def rel(a, b):
 
 
 case = sys.argv[1]
-tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in ("GRD_GEMM_KCHUNK", "GRD_WGRAD_FRESH"))
+tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in ("GRD_GEMM_KCHUNK", "GRD_WGRAD_FRESH", "GRD_GEMM_KSPLIT_TB"))
 if case == "papers":
     z = dict(np.load("tests/golden/papers_s22.npz"))
     scale, deg, F, C, L, H, P = [int(x) for x in z["spec"]]
