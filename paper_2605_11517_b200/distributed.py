@@ -206,8 +206,10 @@ def lean_shard_plan(graph, lplan: LabelPlan, rank: int, world: int, comm=None) -
     owned = np.flatnonzero(np.isin(labels, mine))
     owned = owned[np.argsort(labels[owned], kind="stable")]
     owner = part_rank[labels]
-    ptr, nbr = _csr_rows(graph.src_ptr, graph.dst_idx.astype(np.int64), owned)
-    cand = np.unique(nbr)
+    # int32 neighbour ids (no int64 copy of the whole edge array: 13 GB
+    # per rank at configs[3])
+    ptr, nbr = _csr_rows(graph.src_ptr, np.asarray(graph.dst_idx, dtype=np.int32), owned)
+    cand = np.unique(nbr).astype(np.int64)
     halo = cand[owner[cand] != rank]
     halo = halo[np.lexsort((halo, owner[halo]))]
     halo_owner = owner[halo]
