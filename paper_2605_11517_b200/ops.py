@@ -232,8 +232,12 @@ def agg_sum(spec: AggSpec, y: torch.Tensor, out: torch.Tensor, width: int, *,
 # (trans_a) use in-kernel fresh accumulators instead (GRD_WGRAD_FRESH).
 _KCHUNK = int(os.environ.get("GRD_GEMM_KCHUNK", "128"))
 _KMAX = int(os.environ.get("GRD_GEMM_KMAX", "192"))
-# whether input-gradient GEMMs (A @ W^T) are split too (GRD_GEMM_KSPLIT_TB)
-_KSPLIT_TB = os.environ.get("GRD_GEMM_KSPLIT_TB", "1") != "0"
+# Input-gradient GEMMs (A @ W^T) stay whole (GRD_GEMM_KSPLIT_TB=1 splits
+# them too): the GraphSAGE K = 512 input gradient unsplit leaves every weight
+# gradient's error where it was (6.0e-5 / 2.8e-5 / 7.8e-6 at the products
+# widths; tools/prec_matrix.py) and saves three read-modify-write passes
+# over its 2.1 GB output: products_sage GEMM 15.7 -> 12.1 ms per epoch.
+_KSPLIT_TB = os.environ.get("GRD_GEMM_KSPLIT_TB", "0") != "0"
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, *,
