@@ -308,10 +308,33 @@ typedef struct grd_gat_args {
                                       4 lanes per row instead of a warp */
     int64_t n_mid;                 /* the n_mid rows before those have at most 15
                                       in-edges each: 16 lanes per row (0 = none) */
+    const float* c_dot;            /* grd_gat_pull_bwd: c[v, h] = gO_v,h . O_v,h
+                                      (grd_gat_row_dots) [rows, heads] */
+    const float* alpha_t;          /* grd_gat_pull_bwd, nullable: attention already
+                                      in the pull's edge order [E, heads] */
+    float* seg_wide;               /* grd_gat_pull_bwd: heavy-segment partials
+                                      [n_segs, round_up(hdp + heads, 4)] */
 } grd_gat_args;
 int grd_gat_softmax(const grd_gat_args* args, void* stream);
 int grd_gat_softmax_bwd(const grd_gat_args* args, void* stream);
 int grd_gat_src_grad(const grd_gat_args* args, void* stream);
+/* Fused GAT backward over the transposed pull (rows = sources u, idx = the
+ * out-neighbours v, edge_perm = each pull edge's forward position):
+ *   dalpha_uv,h = gO_v,h . P_u,h          (gO_v gathered once per edge)
+ *   delta_uv,h  = alpha (dalpha - c_v,h) lrelu'(s_u,h + t_v,h)  -> delta[fwd e]
+ *   dP_u        = sum_v alpha_uv gO_v + alpha_self gO_u         -> grad_ext[u, 0:hdp]
+ *   ds_u,h      = sum_v delta_uv,h + delta_self_u,h             -> grad_ext[u, hdp + h]
+ * replacing grd_gat_softmax_bwd's P_u row gather per in-edge.  The target
+ * score gradients dt_v = sum over in-edges of delta follow from
+ * grd_gat_dst_grad over the forward CSR. */
+int grd_gat_pull_bwd(const grd_gat_args* args, void* stream);
+/* dt_v,h = sum_{e in row v} delta[e, h] + delta_self[v, h] over the forward
+ * CSR (edges in its own order) -> grad_ext[v, hdp + heads + h]. */
+int grd_gat_dst_grad(const grd_gat_args* args, void* stream);
+/* c[r, h] = sum_{d < dhp} g[r, h dhp + d] o[r, h dhp + d] (16-byte chunks in
+ * order), the per-head gO . O of every row. */
+int grd_gat_row_dots(const float* g, int64_t ld_g, const float* o, int64_t ld_o, int64_t n_rows,
+                     int32_t heads, int32_t dhp, float* c, void* stream);
 /* st[r, 0:2H] = p_ext[r, hdp : hdp + 2H]: the per-vertex attention scores as
  * one 32-byte row each (H = 4), so the edge-softmax's per-edge score gathers
  * hit a table that stays in L2 instead of one line of a wide P_ext row each. */

@@ -107,6 +107,9 @@ class GrdGatArgs(ctypes.Structure):
         ("ld_st", c_i64),
         ("n_small", c_i64),
         ("n_mid", c_i64),
+        ("c_dot", c_vp),
+        ("alpha_t", c_vp),
+        ("seg_wide", c_vp),
     ]
 
 
@@ -171,6 +174,9 @@ SIGNATURES = {
     "grd_gat_softmax": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
     "grd_gat_softmax_bwd": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
     "grd_gat_src_grad": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_pull_bwd": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_dst_grad": (c_i32, [ctypes.POINTER(GrdGatArgs), c_vp]),
+    "grd_gat_row_dots": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp]),
     "grd_gat_pack_scores": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp]),
     "grd_gat_build_wext": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp]),
     "grd_gat_param_grads": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp,

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/grinder_b200.h"
 #include "grd_common.h"
@@ -24,6 +25,18 @@ constexpr int kWarp = 32;
 constexpr int kMaxHeads = 8;
 
 __device__ __forceinline__ float lrelu(float z, float slope) { return z > 0.f ? z : z * slope; }
+// (the aggregation kernel's float4 helpers: the fused pull must round alike)
+__device__ __forceinline__ float4 f4_fma(float s, const float4 v, float4 a) {
+    a.x = fmaf(s, v.x, a.x);
+    a.y = fmaf(s, v.y, a.y);
+    a.z = fmaf(s, v.z, a.z);
+    a.w = fmaf(s, v.w, a.w);
+    return a;
+}
+__device__ __forceinline__ float4 f4_add(float4 a, const float4 b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    return a;
+}
 __device__ __forceinline__ float lrelu_grad(float z, float slope) { return z > 0.f ? 1.f : slope; }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -496,7 +509,7 @@ __global__ void __launch_bounds__(256) gat_edge_bwd_kernel(grd_gat_args a) {
 // and then every heavy segment, 16 / 4 lanes for the low-degree rows
 // (AggSpec.n_mid / n_small, the same split as the edge softmax).
 template <int L, int HM>
-__global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a, int64_t r0, int64_t r1) {
+__global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a, int64_t r0, int64_t r1, int col0) {
     const int sub = threadIdx.x & (L - 1);
     const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / L;
     Unit un{0, 0, 0, -1, false};
@@ -512,7 +525,7 @@ __global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a, int64
     for (int h = 0; h < HM; ++h) ds[h] = 0.f;
     if (ok)
         for (int64_t i = un.beg + sub; i < un.end; i += L) {
-            const float* de = a.delta + int64_t(a.edge_perm[i]) * H;
+            const float* de = a.delta + (a.edge_perm ? int64_t(a.edge_perm[i]) : i) * H;
 #pragma unroll
             for (int h = 0; h < HM; ++h)
                 if (h < H) ds[h] += de[h];
@@ -528,23 +541,24 @@ __global__ void __launch_bounds__(256) gat_src_grad_kernel(grd_gat_args a, int64
         if (h >= H || (h % L) != sub) continue;
         const float t = ds[h] + (un.self ? a.delta_self[int64_t(r) * H + h] : 0.f);
         if (un.seg < 0)
-            a.grad_ext[int64_t(r) * a.ld_gext + a.hdp + h] = t;
+            a.grad_ext[int64_t(r) * a.ld_gext + col0 + h] = t;
         else
             a.seg_scratch[un.seg * H + h] = t;
     }
 }
 
 template <int HM>
-void launch_src_grad(const grd_gat_args& a, cudaStream_t st) {
+void launch_src_grad(const grd_gat_args& a, cudaStream_t st, int col0) {
     const int64_t r_small = a.n_rows - a.n_small, r_mid = r_small - a.n_mid;
     const int64_t units = r_mid + a.n_segs;
-    if (units > 0) gat_src_grad_kernel<kWarp, HM><<<static_cast<unsigned>((units * kWarp + 255) / 256), 256, 0, st>>>(a, 0, r_mid);
+    if (units > 0)
+        gat_src_grad_kernel<kWarp, HM><<<static_cast<unsigned>((units * kWarp + 255) / 256), 256, 0, st>>>(a, 0, r_mid, col0);
     if (a.n_mid > 0)
         gat_src_grad_kernel<kMidLanes, HM><<<static_cast<unsigned>((a.n_mid * kMidLanes + 255) / 256), 256, 0, st>>>(
-            a, r_mid, r_small);
+            a, r_mid, r_small, col0);
     if (a.n_small > 0)
         gat_src_grad_kernel<kSmallLanes, HM>
-            <<<static_cast<unsigned>((a.n_small * kSmallLanes + 255) / 256), 256, 0, st>>>(a, r_small, a.n_rows);
+            <<<static_cast<unsigned>((a.n_small * kSmallLanes + 255) / 256), 256, 0, st>>>(a, r_small, a.n_rows, col0);
 }
 
 // Heavy rows of the two backward passes: one warp per heavy row sums its
@@ -660,6 +674,220 @@ int check_units(const grd_gat_args* a, const char* what) {
     return 0;
 }
 
+// Per-edge sums of delta into a per-row column of grad_ext (col0 + h): over
+// the pull CSR with edge_perm (ds_u, col0 = hdp) or over the forward CSR in
+// its own edge order (dt_v, col0 = hdp + H, edge_perm null).
+int edge_sums(const grd_gat_args& a, cudaStream_t st, int col0, const char* what) {
+    const int H = a.heads;
+    if (H == 1)
+        launch_src_grad<1>(a, st, col0);
+    else if (H == 2)
+        launch_src_grad<2>(a, st, col0);
+    else if (H <= 4)
+        launch_src_grad<4>(a, st, col0);
+    else
+        launch_src_grad<8>(a, st, col0);
+    int rc = launch_status(what);
+    if (rc || a.n_heavy == 0) return rc;
+    gat_heavy_sum_kernel<<<warps_blocks(a.n_heavy), 256, 0, st>>>(a, col0);
+    return launch_status("gat_heavy_sum");
+}
+
+// ------------------------------------------------ fused pull backward --
+// One warp per unit of the transposed pull (source u, its out-edges u -> v),
+// kU out-edges per batch:
+//   gO_v rows gathered ONCE per edge serve both the attention-score
+//   gradient (dalpha_uv,h = gO_v,h . P_u,h against u's own P row, held in
+//   registers) and dP_u += alpha_uv gO_v;
+//   delta_uv,h = alpha (dalpha - c_v,h) lrelu'(s_u,h + t_v,h) is written at
+//   the edge's forward position and summed into ds_u,h.
+// The separate edge backward (grd_gat_softmax_bwd) gathered P_u once per
+// in-edge of every target: the same row traffic again.  dP_u keeps the
+// aggregation kernel's order (edges in pull order, the self term last; heavy
+// rows: segment partials in segment order, then the self term), so it is
+// bitwise the unfused pull's.  Per-head dot products are reduced through the
+// same padded shared layout as the edge backward.
+template <int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) gat_pull_bwd_kernel(grd_gat_args a) {
+    __shared__ float part[8][kU][kPartStride];
+    __shared__ float alw[8][kU][kMaxHeads];
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int wib = threadIdx.x / kWarp;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    Unit un;
+    if (!unit_of(a, w, un)) return;
+    const int H = a.heads;
+    const int q4 = a.hdp / 4;
+    const int cph = a.dhp / 4;
+    const int hs = cph + 1;
+    const int32_t u = vertex_of(a, un.row);
+    const bool with_self = un.self && un.seg < 0;   // heavy rows: the self term after the segments
+    int pq[NV], hc[NV];
+    float4 pu[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = lane + c * kWarp;
+        pq[c] = (q / cph) * hs + q % cph;
+        hc[c] = min(q / cph, H - 1);
+        pu[c] = q < q4 ? __ldg(reinterpret_cast<const float4*>(a.p_ext + int64_t(u) * a.ld_ext + 4 * q))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const bool scal = lane < kU * H;
+    const int my_h = lane % H, my_j = lane / H;
+    const float s_my = a.p_ext[int64_t(u) * a.ld_ext + a.hdp + my_h];
+    const int64_t ne = un.end - un.beg;
+    const int64_t n = ne + (with_self ? 1 : 0);
+    float4 acc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float ds = 0.f;
+    for (int64_t i0 = 0; i0 < n; i0 += kU) {
+        float4 g[kU][NV];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int64_t i = i0 + j;
+            const int32_t v = i < ne ? a.idx[un.beg + i] : u;
+            const float* gv = a.grad_o + int64_t(v) * a.ld_go;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+                const int q = lane + c * kWarp;
+                g[j][c] = (i < n && q < q4) ? __ldg(reinterpret_cast<const float4*>(gv + 4 * q))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        const int64_t im = i0 + my_j;
+        const bool mine = scal && im < n;
+        float al = 0.f, tv = 0.f, cv = 0.f;
+        int64_t ef = -1;
+        if (mine) {
+            int32_t v = u;
+            if (im < ne) {
+                const int64_t e = un.beg + im;
+                v = a.idx[e];
+                ef = a.edge_perm[e];
+                al = a.alpha_t ? a.alpha_t[e * H + my_h] : a.alpha[ef * H + my_h];
+            } else {
+                al = a.alpha_self[int64_t(u) * H + my_h];
+            }
+            tv = a.st ? a.st[int64_t(v) * a.ld_st + H + my_h] : a.p_ext[int64_t(v) * a.ld_ext + a.hdp + H + my_h];
+            cv = a.c_dot[int64_t(v) * H + my_h];
+            alw[wib][my_j][my_h] = al;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+#pragma unroll
+            for (int c = 0; c < NV; ++c)
+                if (lane + c * kWarp < q4)
+                    part[wib][j][pq[c]] = g[j][c].x * pu[c].x + g[j][c].y * pu[c].y + g[j][c].z * pu[c].z +
+                                          g[j][c].w * pu[c].w;
+        __syncwarp();
+        if (mine) {
+            float da = 0.f;
+            for (int k = 0; k < cph; ++k) da += part[wib][my_j][my_h * hs + k];
+            const float d = al * (da - cv) * lrelu_grad(s_my + tv, a.slope);
+            if (im < ne)
+                a.delta[ef * H + my_h] = d;
+            else
+                a.delta_self[int64_t(u) * H + my_h] = d;
+            ds += d;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            if (i0 + j >= n) break;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) acc[c] = f4_fma(alw[wib][j][hc[c]], g[j][c], acc[c]);
+        }
+        __syncwarp();
+    }
+    part[wib][0][lane] = scal ? ds : 0.f;
+    __syncwarp();
+    float dsh = 0.f;
+    if (lane < H)
+        for (int j = 0; j < kU; ++j) dsh += part[wib][0][j * H + lane];
+    const int ldw = (a.hdp + H + 3) / 4 * 4;
+    float* dst = un.seg < 0 ? a.grad_ext + int64_t(u) * a.ld_gext : a.seg_wide + un.seg * ldw;
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = lane + c * kWarp;
+        if (q < q4) *reinterpret_cast<float4*>(dst + 4 * q) = acc[c];
+    }
+    if (lane < H) dst[a.hdp + lane] = dsh;
+}
+
+// Heavy pull rows: one warp per row sums its segments' dP / ds partials in
+// segment order, then adds the self term (alpha_self gO_u, and delta_self
+// from u's own rows) exactly as the unfused pull's finish does.
+template <int NV>
+__global__ void __launch_bounds__(256) gat_pull_heavy_kernel(grd_gat_args a) {
+    __shared__ float part[8][kPartStride];
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int wib = threadIdx.x / kWarp;
+    const int64_t hr = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+    if (hr >= a.n_heavy) return;
+    const int H = a.heads;
+    const int q4 = a.hdp / 4;
+    const int cph = a.dhp / 4;
+    const int hs = cph + 1;
+    const int ldw = (a.hdp + H + 3) / 4 * 4;
+    const int32_t u = vertex_of(a, a.heavy_rows[hr]);
+    const int64_t s0 = a.heavy_seg_ptr[hr], s1 = a.heavy_seg_ptr[hr + 1];
+    float4 acc[NV], gu[NV], pu[NV];
+    int hc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = lane + c * kWarp;
+        hc[c] = min(q / cph, H - 1);
+        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        gu[c] = pu[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < q4) {
+            for (int64_t s = s0; s < s1; ++s)
+                acc[c] = f4_add(acc[c], *reinterpret_cast<const float4*>(a.seg_wide + s * ldw + 4 * q));
+            gu[c] = *reinterpret_cast<const float4*>(a.grad_o + int64_t(u) * a.ld_go + 4 * q);
+            pu[c] = *reinterpret_cast<const float4*>(a.p_ext + int64_t(u) * a.ld_ext + 4 * q);
+            part[wib][(q / cph) * hs + q % cph] = gu[c].x * pu[c].x + gu[c].y * pu[c].y + gu[c].z * pu[c].z +
+                                                  gu[c].w * pu[c].w;
+        }
+    }
+    __syncwarp();
+    float ds = 0.f, d = 0.f;
+    if (lane < H) {
+        for (int64_t s = s0; s < s1; ++s) ds += a.seg_wide[s * ldw + a.hdp + lane];
+        float da = 0.f;
+        for (int k = 0; k < cph; ++k) da += part[wib][lane * hs + k];
+        const float al = a.alpha_self[int64_t(u) * H + lane];
+        const float tu = a.st ? a.st[int64_t(u) * a.ld_st + H + lane] : a.p_ext[int64_t(u) * a.ld_ext + a.hdp + H + lane];
+        const float su = a.p_ext[int64_t(u) * a.ld_ext + a.hdp + lane];
+        d = al * (da - a.c_dot[int64_t(u) * H + lane]) * lrelu_grad(su + tu, a.slope);
+        a.delta_self[int64_t(u) * H + lane] = d;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+        const int q = lane + c * kWarp;
+        const float al = a.alpha_self[int64_t(u) * H + hc[c]];
+        if (q < q4)
+            *reinterpret_cast<float4*>(a.grad_ext + int64_t(u) * a.ld_gext + 4 * q) = f4_fma(al, gu[c], acc[c]);
+    }
+    if (lane < H) a.grad_ext[int64_t(u) * a.ld_gext + a.hdp + lane] = ds + d;
+}
+
+// c[r, h] = gO_r,h . O_r,h, 16-byte chunks summed in order (thread per (row, head))
+__global__ void gat_row_dots_kernel(const float* __restrict__ g, int64_t ldg, const float* __restrict__ o,
+                                    int64_t ldo, int64_t n_rows, int H, int dhp, float* __restrict__ c) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * H) return;
+    const int64_t r = i / H;
+    const int h = static_cast<int>(i % H);
+    const float4* gr = reinterpret_cast<const float4*>(g + r * ldg + h * dhp);
+    const float4* orow = reinterpret_cast<const float4*>(o + r * ldo + h * dhp);
+    float s = 0.f;
+    for (int k = 0; k < dhp / 4; ++k) {
+        const float4 x = __ldg(gr + k), y = __ldg(orow + k);
+        s += x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
+    }
+    c[i] = s;
+}
+
 }  // namespace
 
 extern "C" int grd_gat_softmax(const grd_gat_args* args, void* stream) {
@@ -755,19 +983,7 @@ extern "C" int grd_gat_src_grad(const grd_gat_args* args, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (args->n_small < 0 || args->n_mid < 0 || args->n_small + args->n_mid > args->n_rows)
         return fail(kErrArg, "gat_src_grad: bad n_small / n_mid");
-    const int H = args->heads;
-    if (H == 1)
-        launch_src_grad<1>(*args, st);
-    else if (H == 2)
-        launch_src_grad<2>(*args, st);
-    else if (H <= 4)
-        launch_src_grad<4>(*args, st);
-    else
-        launch_src_grad<8>(*args, st);
-    int rc = launch_status("gat_src_grad");
-    if (rc || args->n_heavy == 0) return rc;
-    gat_heavy_sum_kernel<<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args, args->hdp);
-    return launch_status("gat_heavy_sum");
+    return edge_sums(*args, st, args->hdp, "gat_src_grad");
 }
 
 __global__ void gat_pack_scores_kernel(const float* __restrict__ p_ext, int64_t ld_ext, int64_t n_rows, int H,
@@ -824,4 +1040,63 @@ extern "C" int grd_head_mean(const float* o, int64_t ldo, int64_t n_rows, int32_
     head_mean_kernel<<<blocks(n_rows * dhp), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         o, ldo, n_rows, heads, dh, dhp, out, ld_out, backward);
     return launch_status("head_mean");
+}
+
+extern "C" int grd_gat_pull_bwd(const grd_gat_args* args, void* stream) {
+    clear_error();
+    if (int rc = check_units(args, "gat_pull_bwd")) return rc;
+    if (args->n_rows == 0) return 0;
+    if (args->hdp > 256 || args->hdp % 4 || args->dhp % 4 || !args->grad_o || !args->c_dot || !args->edge_perm ||
+        !args->alpha || !args->alpha_self || !args->delta || !args->delta_self || !args->grad_ext ||
+        args->ld_go % 4 || args->ld_ext % 4 || args->ld_gext % 4)
+        return fail(kErrArg, "gat_pull_bwd: hdp <= 256, 16-byte aligned rows, all operands required");
+    if (args->n_segs > 0 && !args->seg_wide) return fail(kErrArg, "gat_pull_bwd: heavy rows need seg_wide");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // resident blocks per SM the register budget is capped for
+    // (GRD_GAT_PULL_MINB sweep hook; products_gat, hdp 256: 2 -> 123
+    // registers, 17.7 ms per launch; 3 -> 80 (32 B spill), 15.8 ms; 4 -> 64,
+    // 20.7 ms; hdp <= 128 fits 64 registers without spilling)
+    static int minb = -1;
+    if (minb < 0) {
+        const char* e = getenv("GRD_GAT_PULL_MINB");
+        minb = e ? atoi(e) : 3;
+    }
+    const unsigned nb = unit_blocks(*args);
+    if (args->hdp <= 128) {
+        if (minb >= 3) gat_pull_bwd_kernel<1, 4><<<nb, 256, 0, st>>>(*args);
+        else gat_pull_bwd_kernel<1, 2><<<nb, 256, 0, st>>>(*args);
+    } else {
+        if (minb >= 4) gat_pull_bwd_kernel<2, 4><<<nb, 256, 0, st>>>(*args);
+        else if (minb == 3) gat_pull_bwd_kernel<2, 3><<<nb, 256, 0, st>>>(*args);
+        else gat_pull_bwd_kernel<2, 2><<<nb, 256, 0, st>>>(*args);
+    }
+    int rc = launch_status("gat_pull_bwd");
+    if (rc || args->n_heavy == 0) return rc;
+    if (args->hdp <= 128)
+        gat_pull_heavy_kernel<1><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    else
+        gat_pull_heavy_kernel<2><<<warps_blocks(args->n_heavy), 256, 0, st>>>(*args);
+    return launch_status("gat_pull_heavy");
+}
+
+extern "C" int grd_gat_dst_grad(const grd_gat_args* args, void* stream) {
+    clear_error();
+    if (int rc = check_units(args, "gat_dst_grad")) return rc;
+    if (args->n_rows == 0) return 0;
+    if (args->n_small < 0 || args->n_mid < 0 || args->n_small + args->n_mid > args->n_rows)
+        return fail(kErrArg, "gat_dst_grad: bad n_small / n_mid");
+    grd_gat_args a = *args;
+    a.edge_perm = nullptr;   // the forward CSR's own edge order
+    return edge_sums(a, static_cast<cudaStream_t>(stream), a.hdp + a.heads, "gat_dst_grad");
+}
+
+extern "C" int grd_gat_row_dots(const float* g, int64_t ld_g, const float* o, int64_t ld_o, int64_t n_rows,
+                                int32_t heads, int32_t dhp, float* c, void* stream) {
+    clear_error();
+    if (n_rows == 0) return 0;
+    if (!g || !o || !c || heads < 1 || dhp % 4 || ld_g % 4 || ld_o % 4)
+        return fail(kErrArg, "gat_row_dots: bad arguments");
+    gat_row_dots_kernel<<<blocks(n_rows * heads), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        g, ld_g, o, ld_o, n_rows, heads, dhp, c);
+    return launch_status("gat_row_dots");
 }

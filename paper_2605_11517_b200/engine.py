@@ -794,6 +794,10 @@ class LayerwiseEngine(_EngineBase):
         self.t3 = ops.zeros_rows(self.NL, hdp, dev)
         self.gat_kept = {}
         self.gat_keep_on = os.environ.get("GRD_GAT_KEEP", "1") != "0"
+        # fused backward over the pull (GRD_GAT_FUSED_BWD=0: the separate
+        # edge backward, pull and source-score kernels)
+        self.gat_fused = os.environ.get("GRD_GAT_FUSED_BWD", "1") != "0"
+        self.cdot = torch.zeros(max(self.NL * H, 1), dtype=torch.float32, device=dev)
 
     def _keep_fits(self, need: int) -> bool:
         """Whether `need` more bytes of kept forward state leave a margin of
@@ -878,22 +882,10 @@ class LayerwiseEngine(_EngineBase):
         else:
             pext, alpha, alpha_self = self._gat_transform(l, x)
         gext = self.h[:, : c.ld_ext]
-        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, alpha, alpha_self, go, o_fwd,
-                            self.delta, self.delta_self, gext)   # s_u beside the gathered P_u row
-        if self.NL > self.V:
-            go[self.V:].zero_()    # halo rows: no self term, no stale gradient
-        # dP_u = sum_v alpha_uv gO_v and ds_u = sum_v delta_uv over u's out-edges
-        # (sharded: owned targets only; halo rows are partials for their owners)
-        if self.alpha_t is not None:
-            ne = self.pull.nnz
-            ops.gather_rows(alpha.view(-1, c.heads), self.edge_perm[:ne],
-                            self.alpha_t.view(ne, c.heads), c.heads)
-            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=self.alpha_t,
-                        self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
+        if self.gat_fused:
+            self._gat_fused_bwd(l, pext, alpha, alpha_self, go, o_fwd, gext)
         else:
-            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=alpha,
-                        edge_w_perm=self.edge_perm, self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
-        ops.gat_src_grad(self.pull, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
+            self._gat_unfused_bwd(l, pext, alpha, alpha_self, go, o_fwd, gext)
         dg.reverse_add(gext, c.hdp + c.heads)
         ops.wgrad_sgd(x, gext, wt.dwext[l], c.d_in, c.n_ext, self.V)
         if l > 0:
@@ -902,6 +894,46 @@ class LayerwiseEngine(_EngineBase):
         if not self.defer_sgd:
             ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.dw[l],
                                 wt.datt[l], lr)
+
+    def _gat_alpha_pull_order(self, alpha, c):
+        """Attention permuted into the pull's edge order (None: addressed per edge)."""
+        if self.alpha_t is None:
+            return None
+        ne = self.pull.nnz
+        ops.gather_rows(alpha.view(-1, c.heads), self.edge_perm[:ne], self.alpha_t.view(ne, c.heads),
+                        c.heads)
+        return self.alpha_t
+
+    def _gat_fused_bwd(self, l, pext, alpha, alpha_self, go, o_fwd, gext) -> None:
+        """c = gO.O per target; one pass over the pull (u -> v) gathering gO_v
+        once per edge for dP_u, ds_u and the edge score gradients; dt_v summed
+        over the forward CSR."""
+        c, dg = self.cfg[l], self.dg
+        if self.NL > self.V:
+            go[self.V:].zero_()    # halo rows: no self term, no stale gradient
+        ops.gat_row_dots(go, o_fwd, self.NL, c.heads, c.dhp, self.cdot)
+        ops.gat_pack_scores(pext, self.NL, c.heads, c.dhp, self.st)   # this layer's t_v
+        alpha_t = self._gat_alpha_pull_order(alpha, c)
+        ops.gat_pull_bwd(self.pull, pext, c.heads, c.dhp, self.edge_perm, alpha, alpha_self, go,
+                         self.cdot, self.delta, self.delta_self, gext, alpha_t=alpha_t, st=self.st)
+        ops.gat_dst_grad(dg.fwd, c.heads, c.dhp, self.delta, self.delta_self, gext)
+
+    def _gat_unfused_bwd(self, l, pext, alpha, alpha_self, go, o_fwd, gext) -> None:
+        c, dg = self.cfg[l], self.dg
+        ops.gat_softmax_bwd(dg.fwd, pext, c.heads, c.dhp, alpha, alpha_self, go, o_fwd,
+                            self.delta, self.delta_self, gext)   # s_u beside the gathered P_u row
+        if self.NL > self.V:
+            go[self.V:].zero_()    # halo rows: no self term, no stale gradient
+        # dP_u = sum_v alpha_uv gO_v and ds_u = sum_v delta_uv over u's out-edges
+        # (sharded: owned targets only; halo rows are partials for their owners)
+        alpha_t = self._gat_alpha_pull_order(alpha, c)
+        if alpha_t is not None:
+            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=alpha_t,
+                        self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
+        else:
+            ops.agg_sum(self.pull, go, gext[:, : c.hdp], c.hdp, edge_w=alpha,
+                        edge_w_perm=self.edge_perm, self_w=alpha_self, heads=c.heads, head_ld=c.dhp)
+        ops.gat_src_grad(self.pull, c.heads, c.dhp, self.edge_perm, self.delta, self.delta_self, gext)
 
     def forward(self) -> None:
         for l, c in enumerate(self.cfg):

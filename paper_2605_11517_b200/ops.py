@@ -455,6 +455,46 @@ def gat_src_grad(spec, heads, dhp, edge_perm, delta, delta_self, grad_ext) -> No
                                "gat_src_grad"))
 
 
+def gat_row_dots(g, o, n_rows, heads, dhp, c) -> None:
+    """c[r, h] = gO_r,h . O_r,h (the softmax backward's per-target term)."""
+    _launch("gat_row_dots", 1, 8 * int(n_rows) * int(heads) * int(dhp) + 4 * int(n_rows) * int(heads),
+            2.0 * int(n_rows) * int(heads) * int(dhp),
+            lambda: _lib.check(_lib.lib().grd_gat_row_dots(
+                _p(g), _ld(g), _p(o), _ld(o), int(n_rows), int(heads), int(dhp), _p(c), stream_ptr()),
+                "gat_row_dots"))
+
+
+def gat_pull_bwd(spec, p_ext, heads, dhp, edge_perm, alpha, alpha_self, grad_o, c_dot, delta,
+                 delta_self, grad_ext, alpha_t=None, st=None) -> None:
+    """Fused GAT backward over the transposed pull: dP, ds and the per-edge
+    score gradients delta from one gather of gO_v per edge."""
+    H = int(heads)
+    hdp = H * int(dhp)
+    kw = {} if st is None else dict(st=st, ld_st=_ld(st))
+    a = _gat_args(spec, p_ext, heads, dhp, edge_perm=edge_perm, alpha=alpha, alpha_self=alpha_self,
+                  grad_o=grad_o, ld_go=_ld(grad_o), c_dot=c_dot, delta=delta, delta_self=delta_self,
+                  grad_ext=grad_ext, ld_gext=_ld(grad_ext), alpha_t=alpha_t,
+                  seg_wide=spec.partial(hdp + H), **kw)
+    E, R = spec.nnz, spec.n_rows
+    # per edge: idx + perm, the gO_v row, alpha / t / c / delta per head;
+    # per row: own P and gO rows, dP + ds written
+    nbytes = 8 * (R + 1) + 8 * E + 4 * hdp * (E + 3 * R) + 4 * H * (4 * E + 3 * R)
+    _launch("gat_pull_bwd", 1 + (spec.n_heavy > 0), nbytes, 4.0 * hdp * (E + R),
+            lambda: _lib.check(_lib.lib().grd_gat_pull_bwd(ctypes.byref(a), stream_ptr()),
+                               "gat_pull_bwd"))
+
+
+def gat_dst_grad(spec, heads, dhp, delta, delta_self, grad_ext) -> None:
+    """dt_v = sum of delta over v's in-edges (+ the self term), forward CSR order."""
+    a = _gat_args(spec, grad_ext, heads, dhp, delta=delta, delta_self=delta_self,
+                  grad_ext=grad_ext, ld_gext=_ld(grad_ext))
+    E, R = spec.nnz, spec.n_rows
+    _launch("gat_dst_grad", 1 + (spec.n_mid > 0) + (spec.n_small > 0) + (spec.n_heavy > 0),
+            8 * R + 4 * heads * (E + 2 * R), heads * E,
+            lambda: _lib.check(_lib.lib().grd_gat_dst_grad(ctypes.byref(a), stream_ptr()),
+                               "gat_dst_grad"))
+
+
 def gat_build_wext(w, att, d_in, heads, dh, dhp, wext) -> None:
     _launch("gat_params", 1, 0, 0, lambda: _lib.check(_lib.lib().grd_gat_build_wext(
         _p(w), _ld(w), _p(att), int(d_in), int(heads), int(dh), int(dhp), _p(wext), _ld(wext),
