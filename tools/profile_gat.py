@@ -32,3 +32,10 @@ ops.agg_sum(dg.bwd, go, gext[:, :hdp], hdp, edge_w=alpha, edge_w_perm=perm, self
 ops.gat_src_grad(dg.bwd, H, dhp, perm, delta, dself, gext)
 torch.cuda.synchronize()
 print("ok", n, E, dg.fwd.n_heavy, dg.fwd.n_segs)
+# the fused pull backward (default path): row dots, the pull, the target sums
+cdot = torch.zeros(n * H, device=dev)
+ops.gat_row_dots(go, O, n, H, dhp, cdot)
+ops.gat_pull_bwd(dg.bwd, pext, H, dhp, perm, alpha, aself, go, cdot, delta, dself, gext, st=st)
+ops.gat_dst_grad(dg.fwd, H, dhp, delta, dself, gext)
+torch.cuda.synchronize()
+print("fused ok")
