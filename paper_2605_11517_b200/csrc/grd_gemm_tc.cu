@@ -82,6 +82,8 @@ struct Params {
     float* c2; int64_t ldc2; int64_t split;   // columns >= split (> 0) go to c2
     int tma_store;                  // epilogue chunks leave through shared memory by TMA
     int kch;                        // K blocks per TMEM accumulation (0: the whole K)
+    int hi_raw;                     // 1: the raw fp32 tile is the hi operand (the MMA reads
+                                    // only its tf32 bits), the converter writes lo alone
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -239,7 +241,8 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
-__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t bytes, int ctid, int nthr) {
+__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t bytes, int ctid, int nthr,
+                                           bool write_hi = true) {
     const uint32_t r0 = smem_u32(raw), l0 = smem_u32(lo);
     const uint32_t n16 = bytes / 16;
     uint32_t i = ctid;
@@ -250,14 +253,14 @@ __device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, uint32_t b
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float4 h = hi4(v[u]);
-            sts128(r0 + (i + u * nthr) * 16u, h);
+            if (write_hi) sts128(r0 + (i + u * nthr) * 16u, h);
             sts128(l0 + (i + u * nthr) * 16u, make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w));
         }
     }
     for (; i < n16; i += nthr) {
         const float4 v = lds128(r0 + i * 16u);
         const float4 h = hi4(v);
-        sts128(r0 + i * 16u, h);
+        if (write_hi) sts128(r0 + i * 16u, h);
         sts128(l0 + i * 16u, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
     }
 }
@@ -809,9 +812,9 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int s = static_cast<int>(g % S);
                 mbar_wait(full + s, static_cast<uint32_t>((g / S) & 1));
                 uint8_t* st = smem + s * stage_bytes;
-                split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads);
+                split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads, !p.hi_raw);
                 uint8_t* bh = st + 2 * a_bytes;
-                if (p.b_mode != kPacked) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads);
+                if (p.b_mode != kPacked) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads, !p.hi_raw);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (pair) mbar_arrive_cluster(conv + s, 0);     // the issuing CTA's barrier
                 else mbar_arrive(conv + s);
@@ -1210,6 +1213,20 @@ inline int tma_store_pref() {
     return v;
 }
 
+// Raw fp32 tiles as the hi operand (GRD_GEMM_HI_RAW = 1 / 0): kind::tf32
+// reads only the top 19 bits of each fp32 element, i.e. exactly the hi
+// split (A & 0xffffe000) the converter used to write back, so the converter
+// writes the lo tile alone.  Same errors to 3 digits on every shape of
+// tools/gemm_prec_shapes.py; 1-5 % per launch (tools/gemm_shapes.py).
+inline int hi_raw_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_HI_RAW");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 // packed weight operand resident in shared memory when it fits (GRD_GEMM_BRES = 1 / 0)
 inline int bres_pref() {
     static int v = -1;
@@ -1382,6 +1399,7 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     // fused accumulation truncates, so the error grows with the chain length
     // (profiles/r02_gemm_precision.md)
     p.kch = 0;
+    p.hi_raw = hi_raw_pref();
     if (!p.partial && p.split == 0 && kch_pref() > 0 && g.k > kmax_pref()) p.kch = kch_pref();
     // TMA-store epilogue (plain C output: no split-K partial, no split c2)
     CUtensorMap map_c = map_a;
