@@ -38,10 +38,21 @@ aggregation epilogue), and in backward the gradient buffer holds
 [gp | mean_in^T gp] so the weight gradient and the input gradient are one
 GEMM each per chunk (engine.LayerwiseEngine._forward_sage/_backward_sage).
 
+GAT layers (configs[2]'s model) stream with four layer-height buffers —
+[P | s | t] of the layer at hand, the layer input / upstream gradient, the
+last layer's per-head aggregate then every layer's d[P | s | t], and a
+regathered hidden input — plus the attention and its gradient per edge:
+the forward transform streams the features, the loss runs per chunk, each
+layer's backward is the fused pull backward (engine.LayerwiseEngine), and
+hidden layers regather their input (layer 1 from the streamed features
+through layer 0, deeper layers from pinned host memory) and recompute
+their attention.
+
 Supported: GCN layers (mean_self_loop / symmetric_norm) without row
 normalisation or dropout, L >= 2, hidden layers transform-first
 (d_{l+1} <= d_l for l < L-1); the last layer either way.  GraphSAGE-mean:
-every layer transform-first (the last one included).
+every layer transform-first (the last one included).  GAT: any L >= 2 (one
+device).
 """
 
 from __future__ import annotations
@@ -62,14 +73,16 @@ __all__ = ["StreamGraph", "StreamingEngine", "streaming_supported", "register_ho
 
 def streaming_supported(model) -> str | None:
     """None if the streaming engine can train ``model``, else the reason."""
-    if model.kind not in ("gcn", "sage"):
-        return "the streaming engine trains GCN and GraphSAGE-mean layers"
+    if model.kind not in ("gcn", "sage", "gat"):
+        return "the streaming engine trains GCN, GraphSAGE-mean and GAT layers"
     if model.row_normalize or model.dropout_rate:
         return "the streaming engine trains without row normalisation / dropout"
     dims = model.dims
     L = len(dims) - 1
     if L < 2:
         return "the streaming engine needs at least two layers"
+    if model.kind == "gat":
+        return None                 # every layer transforms first ([P | s | t] = A W_ext)
     last = L if model.kind == "sage" else L - 1
     if any(dims[l + 1] > dims[l] for l in range(last)):
         return ("GraphSAGE layers must all be transform-first (d_out <= d_in)"
@@ -134,6 +147,31 @@ def _chunk_spec(parent: AggSpec, host_ptr: np.ndarray, r0: int, r1: int,
         n_heavy=int(heavy.size), n_segs=int(seg_heavy.size), nnz=int(sub[-1] - sub[0]))
     spec._partial = parent._partial      # same stream, sequential: one scratch
     return spec
+
+
+def _pull_perm(sg) -> torch.Tensor:
+    """For every edge of the out-CSR (the GAT pull: row u, neighbour v) its
+    position in the forward in-CSR (row v, neighbour u), plus one padding
+    element — device sorts of the (source, target) keys (setup only)."""
+    dev = sg.device
+    V = sg.num_vertices
+
+    def keys(spec, row_is_source: bool):
+        ptr = spec.row_ptr
+        rows = torch.repeat_interleave(torch.arange(spec.n_rows, device=dev, dtype=torch.int64),
+                                       ptr[1:] - ptr[:-1])
+        cols = spec.idx[: spec.nnz].to(torch.int64)
+        return rows * V + cols if row_is_source else cols * V + rows
+
+    k_in = keys(sg.fwd, False)            # (source, target) of every forward edge
+    order = torch.argsort(k_in)
+    k_sorted = k_in[order]
+    del k_in
+    k_out = keys(sg.bwd, True)
+    pos = order[torch.searchsorted(k_sorted, k_out)]
+    if not torch.equal(k_sorted[torch.searchsorted(k_sorted, k_out)], k_out):
+        raise RuntimeError("the out-CSR and the in-CSR hold different edges")
+    return torch.cat([pos.to(torch.int32), torch.zeros(1, dtype=torch.int32, device=dev)])
 
 
 class StreamGraph:
@@ -248,7 +286,8 @@ class StreamingEngine:
             raise NotImplementedError("the sharded streaming engine trains GCN models of <= 3 "
                                       "layers")
         self.mode = model.aggregation_mode
-        self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1) for l in range(self.L)]
+        self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1, model.heads)
+                    for l in range(self.L)]
         self.wts = _Weights(model, dev)
         F = self.dims[0]
         self.labels = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(dev)
@@ -265,15 +304,20 @@ class StreamingEngine:
             # layer buffers hold the pair Y = [Y_root | Y_nbr] in forward and
             # [gp | mean^T gp] in backward: twice a layer's output width
             width = max([hid] + [2 * c.ld_out for c in self.cfg])
+        self.gat = model.kind == "gat"
+        if self.gat:
+            self._gat_buffers(sg, model, hid)
+            width = self.ext_w
         # two whole-height layer buffers (zeroed once: pad columns stay 0)
-        self.buf = [ops.zeros_rows(self.NL, width, dev), ops.zeros_rows(self.NL, width, dev)]
+        self.buf = [ops.zeros_rows(self.NL, width, dev),
+                    ops.zeros_rows(self.NL, hid if self.gat else width, dev)]
         # transform-first last layer: its scaled logit gradient G' is pulled
         # whole, so it needs a third (narrow) buffer; GraphSAGE keeps
         # [G | mean^T G] there
         gw = 2 * last.ld_out if self.sage else last.d_out
-        self.gbuf = ops.zeros_rows(self.NL, gw, dev) if last.transform_first else None
+        self.gbuf = ops.zeros_rows(self.NL, gw, dev) if (last.transform_first and not self.gat) else None
         # deeper hidden layers (l >= 2) kept in pinned host memory
-        hw = hid if self.sage else width
+        hw = hid if (self.sage or self.gat) else width
         self.host_acts = {l: torch.zeros((self.V, hw), dtype=torch.float32, pin_memory=True)
                           for l in range(2, self.L - 1)}
         cr = max(r1 - r0 for r0, r1 in sg.chunks)
@@ -422,6 +466,9 @@ class StreamingEngine:
     def epoch(self, lr: float) -> None:
         if self.sage:
             self._epoch_sage(lr)
+            return
+        if self.gat:
+            self._epoch_gat(lr)
             return
         sg, cfg, L, V = self.sg, self.cfg, self.L, self.V
         W, dW = self.wts.w, self.wts.dw
@@ -658,6 +705,148 @@ class StreamingEngine:
         for w, dw in zip(W, dW):
             ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)
 
+    # ------------------------------------------------------------------ GAT --
+    # Buffers: B0 [P | s | t] of the layer at hand; B1 the layer input A_l in
+    # forward and the upstream gradient gO in backward; B2 the last layer's
+    # per-head aggregate O, then every layer's dL/d[P | s | t]; B3 the last
+    # layer's gO, then the regathered input A_l of a hidden layer.  Per edge:
+    # attention and score gradients (E x heads each).  The backward of a
+    # hidden layer regathers A_l (layer 1: from the streamed features, layer
+    # 0's transform, softmax and aggregation; deeper: from pinned host
+    # memory) and recomputes its [P | s | t] and attention — the
+    # reference's regather, applied to the layer that does not fit.
+    def _gat_buffers(self, sg, model, hid: int) -> None:
+        dev = self.device
+        H = model.heads
+        cl = self.cfg[-1]
+        self.ext_w = max(c.ld_ext for c in self.cfg)
+        E = sg.fwd.nnz
+        self.gbuf2 = ops.zeros_rows(self.NL, max(self.ext_w, cl.hdp), dev)
+        self.gbuf3 = ops.zeros_rows(self.NL, max(hid, cl.hdp), dev)
+        self.alpha = torch.zeros(max(E * H, 1), dtype=torch.float32, device=dev)
+        self.delta = torch.zeros_like(self.alpha)
+        self.alpha_self = torch.zeros(max(self.NL * H, 1), dtype=torch.float32, device=dev)
+        self.delta_self = torch.zeros_like(self.alpha_self)
+        self.cdot = torch.zeros_like(self.alpha_self)
+        self.st = ops.zeros_rows(self.NL, 2 * H, dev)
+        self.edge_perm = _pull_perm(sg)
+
+    def _gat_transform(self, l: int, src, P: torch.Tensor) -> None:
+        """[P | s | t] = A_l W_ext -> P (src: a device matrix, or the streamed
+        feature rows for layer 0), then the edge softmax of layer l."""
+        c, wt = self.cfg[l], self.wts
+        d_in, dh, dhp = wt.shape[l]
+        ops.gat_build_wext(wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.wext[l])
+        if isinstance(src, torch.Tensor):
+            ops.gemm(src[:, : c.ld_in], wt.wext[l], P, self.V, c.n_ext, c.d_in)
+        else:
+            self._stream(src, lambda x, r0, r1: ops.gemm(x, wt.wext[l], P[r0:r1], r1 - r0, c.n_ext,
+                                                         c.d_in))
+        ops.gat_pack_scores(P, self.NL, c.heads, c.dhp, self.st)
+        ops.gat_softmax(self.sg.fwd, P, c.heads, c.dhp, self.alpha, self.alpha_self, st=self.st)
+
+    def _gat_aggregate(self, l: int, P: torch.Tensor, out: torch.Tensor) -> None:
+        c = self.cfg[l]
+        ops.agg_sum(self.sg.fwd, P[:, : c.hdp], out, c.hdp, edge_w=self.alpha, self_w=self.alpha_self,
+                    heads=c.heads, head_ld=c.dhp, relu=not c.last)
+
+    def _gat_backward(self, l: int, P: torch.Tensor, gO: torch.Tensor, G: torch.Tensor) -> None:
+        """dL/d[P | s | t] of layer l into G (engine.LayerwiseEngine's fused
+        pull backward; c = gO . O is in self.cdot)."""
+        c = self.cfg[l]
+        ops.gat_pull_bwd(self.sg.bwd, P, c.heads, c.dhp, self.edge_perm, self.alpha,
+                         self.alpha_self, gO, self.cdot, self.delta, self.delta_self, G, st=self.st)
+        ops.gat_dst_grad(self.sg.fwd, c.heads, c.dhp, self.delta, self.delta_self, G)
+
+    def _gat_input_grad(self, l: int, G: torch.Tensor, A: torch.Tensor, out: torch.Tensor) -> None:
+        """Per chunk: gO_{l-1} = relu'(A_l) (G W_ext^T) and c_{l-1} = gO . A_l
+        (A_l = relu(O_{l-1}), the lower layer's output), written to ``out``
+        (which may be A's own buffer: each chunk is read before it is
+        overwritten)."""
+        c = self.cfg[l]
+        cp = self.cfg[l - 1]
+        for r0, r1 in self.sg.chunks:
+            n = r1 - r0
+            d = self.dc[:n, : c.ld_in]
+            ops.gemm(G[r0:r1, : c.ld_ext], self.wts.wext[l], d, n, c.d_in, c.n_ext, trans_b=True,
+                     relu_ref=A[r0:r1])
+            ops.gat_row_dots(d, A[r0:r1], n, cp.heads, cp.dhp, self.cdot[r0 * cp.heads:])
+            ops.gather_rows(d, self.sg.self_ids[:n], out[r0:r1], c.ld_in)
+
+    def _epoch_gat(self, lr: float) -> None:
+        cfg, L, V = self.cfg, self.L, self.V
+        wt = self.wts
+        for dw in wt.dwext:
+            dw.zero_()
+        B0, B1 = self.buf
+        B2, B3 = self.gbuf2, self.gbuf3
+        # ---- forward ----
+        for l in range(L - 1):
+            c = cfg[l]
+            P = B0[:, : c.ld_ext]
+            self._gat_transform(l, self.x_src if l == 0 else B1, P)
+            self._gat_aggregate(l, P, B1[:, : c.hdp])            # A_{l+1} over A_l
+            if l + 1 in self.host_acts:
+                self._to_host(B1, self.host_acts[l + 1])
+        l = L - 1
+        c = cfg[l]
+        P = B0[:, : c.ld_ext]
+        self._gat_transform(l, self.x_src if l == 0 else B1, P)
+        O = B2[:, : c.hdp]
+        self._gat_aggregate(l, P, O)
+        # loss per chunk: logits = mean over heads, gO = dL/dlogits / heads
+        C = c.d_out
+        for i, (r0, r1) in enumerate(self.sg.chunks):
+            n = r1 - r0
+            lg = self.lc[:n]
+            ops.head_mean(O[r0:r1], n, c.heads, c.dh, c.dhp, lg)
+            g = self.gc[:n]
+            ops.softmax_xent(lg, n, C, self.labels[r0:r1], self.mask[r0:r1], self.mask_count, g,
+                             self.stats_all[i], self.partials)
+            ops.head_mean(g, n, c.heads, c.dh, c.dhp, B3[r0:r1, : c.hdp], backward=True)
+        ops.gat_row_dots(B3[:, : c.hdp], O, V, c.heads, c.dhp, self.cdot)
+        # ---- backward of the last layer: its [P | s | t], attention, input in place ----
+        G = B2[:, : c.ld_ext]
+        self._gat_backward(l, P, B3[:, : c.hdp], G)
+        if l == 0:
+            self._stream(self.x_src, lambda x, r0, r1: ops.wgrad_sgd(
+                x, G[r0:r1], wt.dwext[0], c.d_in, c.n_ext, r1 - r0, accumulate=True))
+        else:
+            A = B1[:, : c.ld_in]
+            ops.wgrad_sgd(A, G, wt.dwext[l], c.d_in, c.n_ext, V)
+            self._gat_input_grad(l, G, A, B1)                       # gO_{L-2} over A_{L-1}
+        # ---- hidden layers: gO_l in B1 ----
+        for l in reversed(range(L - 1)):
+            c = cfg[l]
+            P = B0[:, : c.ld_ext]
+            if l == 0:
+                self._gat_transform(0, self.x_src, P)
+            else:
+                A = B3[:, : c.ld_in]
+                if l == 1:            # regather A_1 from the streamed features
+                    P0 = B0[:, : cfg[0].ld_ext]
+                    self._gat_transform(0, self.x_src, P0)
+                    self._gat_aggregate(0, P0, A)
+                else:
+                    self._stream(HostRows(self.host_acts[l]),
+                                 lambda a, r0, r1, _A=A: ops.gather_rows(
+                                     a, self.sg.self_ids[: r1 - r0], _A[r0:r1], _A.shape[1]))
+                self._gat_transform(l, A, P)
+            G = B2[:, : c.ld_ext]
+            self._gat_backward(l, P, B1[:, : c.hdp], G)
+            if l == 0:
+                self._stream(self.x_src, lambda x, r0, r1: ops.wgrad_sgd(
+                    x, G[r0:r1], wt.dwext[0], c.d_in, c.n_ext, r1 - r0, accumulate=True))
+            else:
+                ops.wgrad_sgd(A, G, wt.dwext[l], c.d_in, c.n_ext, V)
+                self._gat_input_grad(l, G, A, B1)
+        # ---- SGD: dW, datt from dW_ext ----
+        for l in range(L):
+            c = cfg[l]
+            d_in, dh, dhp = wt.shape[l]
+            ops.gat_param_grads(wt.dwext[l], wt.w[l], wt.att[l], d_in, c.heads, dh, dhp, wt.dw[l],
+                                wt.datt[l], lr)
+
     def read_stats(self) -> tuple[float, float]:
         """(loss, accuracy) of the last epoch: per-chunk sums added in chunk
         order on the host (float64); sharded: the ranks' sums all-reduced at
@@ -703,6 +892,14 @@ def streaming_bytes(num_vertices: int, num_edges: int, model, chunk_rows: int,
         gw = 2 * lds[-1]
     graph = (1 if symmetric else 2) * (8 * (V + 1) + 4 * E) + 4 * V
     layers = 2 * 4 * V * width + (4 * V * gw if lds[-1] <= lds[-2] else 0)
+    if model.kind == "gat":
+        # B0 / B2 [P | s | t], B1 / B3 a layer (heads x padded head width),
+        # attention + score gradients per edge and the pull's permutation
+        H = model.heads
+        hdp = max(H * ld_of(d // H) for d in model.dims[1:-1]) if len(model.dims) > 2 else 0
+        hdp = max(hdp, H * lds[-1])
+        ext = ld_of(hdp + 2 * H)
+        layers = 4 * V * (2 * ext + 2 * hdp) + 8 * E * H + 4 * E + 16 * V * H
     chunks = 4 * int(chunk_rows) * (2 * max(lds) + 3 * max(lds) + 2 * lds[-1])
     return graph + layers + chunks + 4 * E * max(lds) // 64 + 16 * V
 

@@ -210,3 +210,62 @@ def test_streaming_sage_from_nvme_tier(tmp_path):
         assert abs(l1 - l2) <= 1e-5 * abs(l2)
     for i in range(3):
         assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+
+
+GAT_CASES = [
+    # (scale, deg, F, C, L, H, heads, directed, chunk rows)
+    (11, 12, 48, 7, 3, 32, 4, False, 300),    # configs[2]-like, 3 layers
+    (11, 12, 40, 5, 2, 16, 2, True, 256),     # directed graph: separate out-CSR for the pull
+    (10, 16, 64, 9, 4, 32, 4, False, 200),    # L = 4: A_2 kept on the host and streamed back
+]
+
+
+@pytest.mark.parametrize("case", GAT_CASES)
+def test_streaming_gat_matches_resident_and_oracle(case):
+    """GAT through the streaming engine (four layer-height buffers, the
+    features streamed, hidden layers regathered in the backward): same
+    epoch as the resident layer-wise engine (1e-5) and the builder oracle
+    (1e-4), with a partial HBM feature cache and split heavy rows."""
+    from oracle import sage_gat
+    scale, deg, F, C, L, H, heads, directed, rows = case
+    g, ds, plan, _ = _setup(scale, deg, F, C, L, H, "gat", directed)
+    model = g2.create_model(F, C, num_layers=L, hidden_dim=H, seed=scale + 3, aggregation_mode="gat",
+                            heads=heads)
+    epochs, lr = 2, 0.05
+    ref = TrainSession(ds, plan, model)
+    m_ref, tr_ref = ref.train(epochs, lr, use_graph=False)
+    ss = StreamSession(ds, plan, model, chunk_rows=rows, x_cache_bytes=3 * rows * 4 * F)
+    assert ss.engine.gat and ss.engine.cache_rows == 3 * rows
+    assert any(s.n_segs for s in ss.sg.fwd_chunks)
+    if L > 3:
+        assert 2 in ss.engine.host_acts
+    m_st, tr_st = ss.train(epochs, lr)
+    for (_, l1, a1), (_, l2, a2) in zip(tr_st, tr_ref):
+        assert abs(l1 - l2) <= 1e-5 * abs(l2)
+        assert abs(a1 - a2) <= 2.0 / ds.train_mask.sum()
+    W, grads, tr_or = sage_gat.train_gat(np.asarray(ds.features, np.float64), ds.labels,
+                                         ds.train_mask, g.src_ptr, g.dst_idx, model.weights, heads,
+                                         epochs, lr)
+    for i in range(L):
+        assert rel_l2(m_st.weights[i], m_ref.weights[i]) < 1e-5
+        assert rel_l2(m_st.weight_grads[i], m_ref.weight_grads[i]) < 1e-5
+        assert rel_l2(m_st.weights[i], W[i]) < 1e-4
+    for (_, l1, _), (_, l2, _) in zip(tr_st, tr_or):
+        assert abs(l1 - l2) <= 1e-4 * abs(l2)
+
+
+def test_partitioned_train_streams_gat(monkeypatch):
+    """GRD_ENGINE=stream routes a GAT model to the streaming engine."""
+    g, ds, plan, _ = _setup(10, 8, 16, 4, 2, 8, "gat")
+    model = g2.create_model(16, 4, num_layers=2, hidden_dim=8, seed=3, aggregation_mode="gat", heads=2)
+    monkeypatch.setenv("GRD_ENGINE", "stream")
+    plan.device_cache.clear()
+    st, tst, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    assert isinstance(g2.training.session_for(ds, plan, model), StreamSession)
+    monkeypatch.setenv("GRD_ENGINE", "resident")
+    plan.device_cache.clear()
+    rs, trs, _ = g2.partitioned_train(ds, plan, model, epochs=1, lr=0.05)
+    assert abs(tst[0][1] - trs[0][1]) <= 1e-5 * abs(trs[0][1])
+    for a, b in zip(st.weights, rs.weights):
+        assert rel_l2(a, b) < 1e-5
+    plan.device_cache.clear()
