@@ -457,10 +457,12 @@ def run_ours(args, spec, rank, world, local_rank):
             dram = float(tr[name])
             gbs = dram / per_launch_s / 1e9
             r.update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4), traffic=int(dram),
+                     frac_nominal_8TBs=round(gbs / 8000.0, 4),
                      basis="ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
                            f"({tr.get('_source', 'profiles/traffic.json')}) / live launch time")
         else:
             r.update(achieved=round(model_gbs, 1), frac=round(model_gbs / hbm_peak, 4),
+                     frac_nominal_8TBs=round(model_gbs / 8000.0, 4),
                      traffic=None, basis="streaming model (no ncu DRAM capture of this workload)")
         return r
 
@@ -669,16 +671,47 @@ def run_sharded_stream(args, spec, rank, world, dev, backend):
                 "d2h_bytes_per_step": int(sum(w.size * 8 * 2 for w in model.weights)),
                 "api": "sharded StreamSession epoch (the engine partitioned_train dispatches to) "
                        "with page-locked host feature rows, weights downloaded every step"},
-        "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(model_gbs, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(model_gbs / hbm_peak, 4),
-                     "traffic": None, "peak_source": peak_kind,
-                     "basis": "streaming model (rank 0; no ncu capture of the sharded run)"},
+        "roofline": sharded_roof(args.workload, dom, model_gbs, hbm_peak, peak_kind),
         "kernels": {k: {"ms_per_epoch": round(v["ms"], 3), "launches": v["launches"]}
                     for k, v in per_kernel.items()},
         "clocks": clock, "gpu_launches": launches * args.steps,
     }
     dist.destroy_process_group()
     return out
+
+
+def sharded_roof(workload, dom, model_gbs, hbm_peak, peak_kind):
+    """Roofline of the sharded run's dominant kernel (rank 0).  ncu cannot
+    capture a multi-rank command, so the DRAM side is estimated: the
+    streaming-model rate times the kernel's DRAM / streaming-model byte
+    ratio measured at N = 1 on the same workload (profiles/traffic.json
+    over the N = 1 bench line's algorithmic bytes per launch)."""
+    r = {"kernel": dom, "bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_source": peak_kind,
+         "streaming_model_GBs": round(model_gbs, 1),
+         "streaming_model_frac": round(model_gbs / hbm_peak, 4)}
+    ratio = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(workload, {})
+        line = json.loads((ROOT / "profiles" / f"r02_bench_{workload}.json").read_text())
+        for key in ("roofline", "agg_roofline"):
+            rf = line.get(key) or {}
+            if rf.get("kernel") == dom and dom in tr and rf.get("algorithmic_bytes_per_launch"):
+                ratio = float(tr[dom]) / float(rf["algorithmic_bytes_per_launch"])
+                break
+    except (OSError, ValueError):
+        ratio = None
+    if ratio is None:
+        r.update(achieved=round(model_gbs, 1), frac=round(model_gbs / hbm_peak, 4),
+                 frac_nominal_8TBs=round(model_gbs / 8000.0, 4), traffic=None,
+                 basis="streaming model (rank 0; no ncu capture of the sharded run)")
+    else:
+        gbs = model_gbs * ratio
+        r.update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4),
+                 frac_nominal_8TBs=round(gbs / 8000.0, 4), traffic=None, dram_per_model_byte=round(ratio, 4),
+                 basis="rank 0's streaming-model rate x the DRAM / model byte ratio ncu measured "
+                       "for this kernel at N = 1 (profiles/traffic.json, profiles/r02_bench_"
+                       f"{workload}.json)")
+    return r
 
 
 def oracle_sample(spec, key):
