@@ -1383,7 +1383,16 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
     if (fresh && p.bn > 128) p.bn = 128;
     const int64_t mt0 = (g.m + kBM - 1) / kBM;
     // a CTA pair stages half of B each: halves of whole 32-row atoms
-    p.pair = (pair_pref() && p.bn % 64 == 0 && mt0 >= 2) ? 1 : 0;
+    // GRD_GEMM_PAIR = 1 (auto): pairs for forward / input-gradient N tiles
+    // of 256, where half of B per CTA buys the stages (products N = 256 /
+    // 512: 2.59 vs 3.68 ms unpaired); single CTAs for narrower tiles (papers
+    // shapes, bn 128 / 192: 1 M x 128 x 128 0.361 -> 0.287 ms, 16 M x 128 x
+    // 128 5.47 -> 4.49, the K = 172 input gradient 0.560 -> 0.393) and for
+    // the weight gradients (256 x 256 over 2 M rows: 2.42 -> 2.05 ms;
+    // tools/gemm_shapes.py, tools/wgrad_one.py); 2: pair whenever possible
+    const int pp = pair_pref();
+    const bool pair_ok = pp == 2 || (pp == 1 && p.partial == nullptr && p.bn >= 256);
+    p.pair = (pair_ok && p.bn % 64 == 0 && mt0 >= 2) ? 1 : 0;
     if (p.pair && p.b_mode == kKMajorTma &&
         !make_map(&map_b, g.b, g.n, g.k, g.ldb, 32, static_cast<uint32_t>(p.bn / 2)))
         return cudaErrorInvalidValue;
