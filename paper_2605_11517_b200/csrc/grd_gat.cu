@@ -702,11 +702,11 @@ int edge_sums(const grd_gat_args& a, cudaStream_t st, int col0, const char* what
 //   delta_uv,h = alpha (dalpha - c_v,h) lrelu'(s_u,h + t_v,h) is written at
 //   the edge's forward position and summed into ds_u,h.
 // The separate edge backward (grd_gat_softmax_bwd) gathered P_u once per
-// in-edge of every target: the same row traffic again.  dP_u keeps the
-// aggregation kernel's order (edges in pull order, the self term last; heavy
-// rows: segment partials in segment order, then the self term), so it is
-// bitwise the unfused pull's.  Per-head dot products are reduced through the
-// same padded shared layout as the edge backward.
+// in-edge of every target: the same row traffic again.  dP_u sums its
+// edges in pull order with the self term last (heavy rows: each segment's
+// edges in order, segment partials in segment order, then the self term) —
+// a fixed order, deterministic run to run.  Per-head dot products are
+// reduced through the same padded shared layout as the edge backward.
 template <int NV, int MINB>
 __global__ void __launch_bounds__(256, MINB) gat_pull_bwd_kernel(grd_gat_args a) {
     __shared__ float part[8][kU][kPartStride];

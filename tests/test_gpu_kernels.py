@@ -266,6 +266,25 @@ def test_gat_kernels_match_autograd(heads, dh, scale, deg, use_st):
     assert rel_l2(dP, Pt.grad.numpy()) < 1e-6
     assert rel_l2(ge[:, hdp:hdp + heads], st.grad.numpy()) < 1e-5
     assert rel_l2(ge[:, hdp + heads:], tt.grad.numpy()) < 1e-5
+    # the fused pull backward (one gO_v gather per edge): dP, the score
+    # gradients against autograd, delta against the edge backward's (light
+    # rows sum in the unfused pull's order; its heavy segments stride their
+    # edges over lane groups, so those rows round differently)
+    cdot = torch.zeros(n * heads, device=DEV)
+    ops.gat_row_dots(god, O, n, heads, dhp, cdot)
+    dlt2, dlt2_s = torch.zeros_like(alpha), torch.zeros_like(alpha_self)
+    gext2 = ops.zeros_rows(n, hdp + 2 * heads, DEV)
+    ops.gat_pull_bwd(dg.bwd, pe, heads, dhp, perm, alpha, alpha_self, god, cdot, dlt2, dlt2_s, gext2,
+                     st=st_tab)
+    ops.gat_dst_grad(dg.fwd, heads, dhp, dlt2, dlt2_s, gext2)
+    ge2 = _host(gext2, hdp + 2 * heads)
+    dP2 = ge2[:, :hdp].reshape(n, heads, dhp)[:, :, :dh]
+    assert rel_l2(dP2, Pt.grad.numpy()) < 1e-6
+    assert rel_l2(ge2[:, :hdp], ge[:, :hdp]) < 1e-6
+    assert rel_l2(ge2[:, hdp:hdp + heads], st.grad.numpy()) < 1e-5
+    assert rel_l2(ge2[:, hdp + heads:], tt.grad.numpy()) < 1e-5
+    assert rel_l2(dlt2.cpu().numpy(), dlt.cpu().numpy()) < 1e-6
+    assert rel_l2(dlt2_s.cpu().numpy(), dlt_s.cpu().numpy()) < 1e-6
 
 
 def test_gemm_bf16x3_opt_in_path():
