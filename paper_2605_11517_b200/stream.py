@@ -282,9 +282,9 @@ class StreamingEngine:
         self.V = sg.n_rows          # rows this engine computes (owned rows when sharded)
         self.NL = sg.n_local        # rows of the layer buffers (owned + halo when sharded)
         self.comm = sg.comm
-        if self.comm is not None and (model.kind != "gcn" or self.L > 3):
-            raise NotImplementedError("the sharded streaming engine trains GCN models of <= 3 "
-                                      "layers")
+        if self.comm is not None and (model.kind not in ("gcn", "sage") or self.L > 3):
+            raise NotImplementedError("the sharded streaming engine trains GCN and GraphSAGE "
+                                      "models of <= 3 layers")
         self.mode = model.aggregation_mode
         self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1, model.heads)
                     for l in range(self.L)]
@@ -620,15 +620,23 @@ class StreamingEngine:
     def _sage_layer_out(self, spec, Y: torch.Tensor, out: torch.Tensor, c, r0: int | None = None,
                         r1: int | None = None, relu: bool = True) -> None:
         """out = act(Y_root + mean_in(Y_nbr)) over the rows of ``spec``
-        (all rows, or the chunk [r0, r1) with chunk-local output rows)."""
+        (all rows, or the chunk [r0, r1) with chunk-local output rows).  The
+        caller has filled Y_nbr's halo rows (sharded: _sage_halo)."""
         lo = c.ld_out
         root = Y[:, :lo] if r0 is None else Y[r0:r1, :lo]
         ops.agg_sum(spec, Y[:, lo: 2 * lo], out, c.d_out, post_div_deg=2, no_self=True,
                     add_y=root, relu=relu)
 
-    def _sage_pull(self, G: torch.Tensor, c) -> None:
-        """G[:, lo:2lo] = mean_in^T G[:, :lo] (pull over out-edges, 1/deg_v)."""
+    def _sage_halo(self, Y: torch.Tensor, c) -> None:
+        """Halo rows of the neighbour half Y_nbr (sharded; one device: no-op)."""
         lo = c.ld_out
+        self.sg.exchange(Y[:, lo: 2 * lo], c.d_out)
+
+    def _sage_pull(self, G: torch.Tensor, c) -> None:
+        """G[:, lo:2lo] = mean_in^T G[:, :lo] (pull over out-edges, 1/deg_v;
+        sharded: gp's halo rows first, the graph is symmetric)."""
+        lo = c.ld_out
+        self.sg.exchange(G[:, :lo], c.d_out)
         ops.agg_sum(self.sg.bwd, G[:, :lo], G[:, lo: 2 * lo], c.d_out,
                     src_scale=self.sg.scale("inv_deg"), no_self=True)
 
@@ -660,6 +668,7 @@ class StreamingEngine:
                     x, W[0], Y[r0:r1], r1 - r0, 2 * c.ld_out, c.d_in))
             else:
                 ops.gemm(B1[:, : c.ld_in], W[l], Y, V, 2 * c.ld_out, c.d_in)
+            self._sage_halo(Y, c)
             self._sage_layer_out(sg.fwd, Y, B1[:, : c.ld_out], c)
             if l + 1 in self.host_acts:
                 self._to_host(B1, self.host_acts[l + 1])
@@ -669,6 +678,7 @@ class StreamingEngine:
         A = B1[:, : c.ld_in]
         Y = B0[:, : 2 * c.ld_out]
         ops.gemm(A, W[l], Y, V, 2 * c.ld_out, c.d_in)
+        self._sage_halo(Y, c)
         G = self.gbuf
         C = c.d_out
         for i, ((r0, r1), spec) in enumerate(zip(sg.chunks, sg.fwd_chunks)):
@@ -694,6 +704,7 @@ class StreamingEngine:
                 Y0 = B1[:, : 2 * c0.ld_out]
                 self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
                     x, W[0], Y0[r0:r1], r1 - r0, 2 * c0.ld_out, c0.d_in))
+                self._sage_halo(Y0, c0)
                 for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
                     a = self.ac[: r1 - r0, : c.ld_in]
                     self._sage_layer_out(spec, Y0, a, c0, r0, r1)
@@ -701,6 +712,10 @@ class StreamingEngine:
             else:
                 self._stream(HostRows(self.host_acts[l]),
                              lambda a, r0, r1, _l=l: self._sage_grad(_l, a, B0, r0, r1))
+        if self.comm is not None:      # every layer's weight gradient in one all-reduce
+            self.comm.all_reduce_sum(self.wts.grad_bucket)
+            self.stats.copy_(self.stats_all.sum(dim=0))
+            self.comm.all_reduce_sum(self.stats)
         # ---- SGD (training.py:352-354) ----
         for w, dw in zip(W, dW):
             ops.wgrad_sgd(w, w, dw, dw.shape[0], dw.shape[1], 0, accumulate=True, w=w, lr=lr)

@@ -155,7 +155,7 @@ def test_two_ranks_over_nccl_match_one_device(tmp_path, case):
     assert np.allclose(r0["trace"][:, 1], np.array(trace)[:, 1], rtol=1e-4)
 
 
-def _worker_stream(rank, world, port, out):
+def _worker_stream(rank, world, port, out, mode="mean_self_loop"):
     """Two ranks of the sharded layer-streaming engine sharing one GPU."""
     import torch.distributed as dist
     from paper_2605_11517_b200.distributed import Communicator
@@ -163,7 +163,7 @@ def _worker_stream(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ds, plan, model = _setup_stream()
+    ds, plan, model = _setup_stream(mode)
     sess = StreamSession(ds, plan, model, chunk_rows=300, x_cache_bytes=200 * 64,
                          comm=Communicator())
     assert sess.engine.V == sess.sg.shard.n_own and sess.engine.NL == sess.sg.shard.n_local
@@ -174,17 +174,19 @@ def _worker_stream(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def _setup_stream():
+def _setup_stream(mode="mean_self_loop"):
     g = g2.generate_kronecker(11, 10, seed=4)
     ds = g2.make_random_dataset(g, feature_dim=16, num_classes=7, seed=5)
     part = g2.switching_aware_partition(g, 6, g2.PartitionerParams(seed=6))
     plan = g2.build_partition_plan(g, part.labels, 6)
-    # configs[3]'s structure: transform-first hidden layers, aggregate-first last layer
-    model = g2.create_model(16, 7, num_layers=3, hidden_dim=8, seed=7)
+    # configs[3]'s structure: transform-first hidden layers, aggregate-first
+    # last layer (GraphSAGE, configs[4]'s model: every layer transform-first)
+    model = g2.create_model(16, 7, num_layers=3, hidden_dim=8, seed=7, aggregation_mode=mode)
     return ds, plan, model
 
 
-def test_sharded_streaming_engine_matches_one_device(tmp_path):
+@pytest.mark.parametrize("mode", ["mean_self_loop", "sage_mean"])
+def test_sharded_streaming_engine_matches_one_device(tmp_path, mode):
     """The layer-streaming engine over a rank's shard (owned rows streamed,
     halo rows of every aggregation's input exchanged, one bucketed weight-
     gradient all-reduce, loss sums all-reduced): two ranks on one GPU equal
@@ -195,8 +197,8 @@ def test_sharded_streaming_engine_matches_one_device(tmp_path):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mp.spawn(_worker_stream, args=(2, port, str(tmp_path)), nprocs=2, join=True)
-    ds, plan, model = _setup_stream()
+    mp.spawn(_worker_stream, args=(2, port, str(tmp_path), mode), nprocs=2, join=True)
+    ds, plan, model = _setup_stream(mode)
     single = StreamSession(ds, plan, model, chunk_rows=300, x_cache_bytes=200 * 64)
     trained, trace = single.train(3, 0.05)
     r0, r1 = (dict(np.load(tmp_path / f"r{r}.npz")) for r in range(2))
