@@ -497,8 +497,10 @@ def run_ours(args, spec, rank, world, local_rank):
             "storage_read_bytes_per_epoch": storage_bytes if streaming else None,
             "engine": f"streaming: {sess.engine.cache_rows} of {g.num_vertices} feature rows "
                       f"cached in HBM; {sess.engine.x_src.describe()}; {stream_bytes / 1e9:.1f} GB "
-                      "over the host link per epoch (inside value and e2e; e2e refills the HBM "
-                      "cache every call)" if streaming else
+                      "over the host link per epoch (inside value; the layer-0 backward leaves the "
+                      "streamed rows in the free layer buffer for the next epoch's layer-0 "
+                      "transform; e2e re-binds the features every call, so it refills the HBM "
+                      "cache and streams every pass)" if streaming else
                       "HBM-resident layer-wise (inputs resident before the timed region)",
         },
         "e2e": {"value": round(edges_per_epoch / e2e_s, 1), "unit": "edges/s",
@@ -630,6 +632,9 @@ def run_sharded_stream(args, spec, rank, world, dev, backend):
     h0 = eng.h2d_bytes
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        # features re-bound every step (as partitioned_train does): the HBM
+        # cache and the stashed rows are refilled from the host inside it
+        eng.set_features(eng.x_src)
         sess.run_epoch(0, LR)
         eng.wts.export(sess.model)
     torch.cuda.synchronize()

@@ -356,6 +356,9 @@ class StreamingEngine:
         rows = min(self.V, int(x_cache_bytes) // row_bytes)
         rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
         self.cache_rows = rows
+        # stash needs the layers to leave no pad columns that must stay zero
+        self.stash_on = (os.environ.get("GRD_STREAM_STASH", "1") != "0"
+                         and all(ld_of(d) == d for d in self.dims[1:]))
         self.x_cache = torch.empty((rows, ld_of(F)), dtype=torch.float32, device=dev) if rows else None
         self.set_features(features)
 
@@ -376,20 +379,32 @@ class StreamingEngine:
             return consumer_scale
         return self.sg.scale("inv_deg1")
 
-    def _stream(self, src, fn) -> None:
+    def _stream(self, src, fn, stash_to: torch.Tensor | None = None,
+                stash_from: torch.Tensor | None = None) -> None:
         """For every row chunk: fn(rows, r0, r1) on the compute stream, the
         rows coming from the HBM feature cache when cached, else by H2D from
         the row source (tiers.py: host memory or the NVMe tier file) on the
         copy stream into one of two device buffers.  A buffer's copy waits
         only for that buffer's last use, so the first transfers of a pass
-        overlap whatever compute precedes it."""
+        overlap whatever compute precedes it.
+
+        ``stash_to``: a free whole-height layer buffer that receives every
+        row (streamed chunks land in their own rows instead of the chunk
+        buffers; cached chunks are copied from the HBM cache) and keeps
+        them.  ``stash_from``: such a buffer filled earlier — every row is
+        read in place, no transfer.  ``fn`` may be None (fill only)."""
+        if stash_from is not None:
+            for r0, r1 in self.sg.chunks:
+                if fn is not None:
+                    fn(stash_from[r0:r1, :src.width], r0, r1)
+            return
         cur = torch.cuda.current_stream(self.device)
         cs = self.copy_stream
         width = src.width
         cached = src is self.x_src and self.x_cache is not None
         fill = cached and not self.x_cache_valid
-        if fill:
-            cs.wait_stream(cur)            # earlier readers of the cache are done
+        if fill or stash_to is not None:
+            cs.wait_stream(cur)            # earlier readers of the cache / stash buffer are done
         hits = self.cache_rows if cached and not fill else 0
         src.begin_pass([(r0, r1) for r0, r1 in self.sg.chunks if r1 > hits])
         try:
@@ -397,11 +412,18 @@ class StreamingEngine:
             for r0, r1 in self._pass_order(hits):
                 n = r1 - r0
                 if r1 <= hits:
-                    fn(self.x_cache[r0:r1], r0, r1)
+                    x = self.x_cache[r0:r1]
+                    if stash_to is not None:
+                        x = stash_to[r0:r1, :width]
+                        x.copy_(self.x_cache[r0:r1])
+                    if fn is not None:
+                        fn(x, r0, r1)
                     continue
                 to_cache = cached and r1 <= self.cache_rows
                 if to_cache:                    # first pass fills the HBM cache
                     dst, ready, free = self.x_cache[r0:r1], self._cache_ready, None
+                elif stash_to is not None:      # rows kept in the layer buffer
+                    dst, ready, free = stash_to[r0:r1, :width], torch.cuda.Event(), None
                 else:
                     b = nb & 1
                     nb += 1
@@ -417,7 +439,11 @@ class StreamingEngine:
                     done.record(cs)
                 src.release(token, done)
                 cur.wait_event(ready)
-                fn(dst, r0, r1)
+                if to_cache and stash_to is not None:
+                    stash_to[r0:r1, :width].copy_(dst)
+                    dst = stash_to[r0:r1, :width]
+                if fn is not None:
+                    fn(dst, r0, r1)
                 if free is not None:
                     free.record(cur)
                 self.h2d_bytes += n * width * 4
@@ -451,6 +477,7 @@ class StreamingEngine:
         src.configure(self.cache_rows)
         self.x_src = src
         self.x_cache_valid = False
+        self._xbuf = None
 
     def _to_host(self, src: torch.Tensor, host: torch.Tensor) -> None:
         """D2H of a whole layer in row chunks on the copy stream."""
@@ -475,6 +502,11 @@ class StreamingEngine:
         for dw in dW:
             dw.zero_()
         B = list(self.buf)                  # B[1] holds the current layer input
+        xb, self._xbuf = self._xbuf, None
+        if xb is not None:
+            # the last epoch's backward left every feature row in layer
+            # buffer xb: P_0 goes to the other buffer, A_1 over the rows
+            B = [self.buf[1] if xb is self.buf[0] else self.buf[0], xb]
         # ---- forward of the hidden (transform-first) layers ----
         for l in range(L - 1):
             c = cfg[l]
@@ -482,7 +514,8 @@ class StreamingEngine:
             P = B[0][:, : c.ld_out]
             if l == 0:
                 self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
-                    x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)))
+                    x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)),
+                    stash_from=xb)
             else:
                 ops.gemm(B[1][:, : c.ld_in], W[l], P, V, c.d_out, c.d_in, row_scale=s)
             sg.exchange(P, c.d_out)                               # halo rows of P
@@ -498,13 +531,32 @@ class StreamingEngine:
             s = self._scale(c)
             D = B[1][:, : c.ld_out]
             if l == 0:
-                self._backward_first(D, s)
+                self._backward_first(D, s, B[0])
                 break
             H = B[0][:, : c.ld_out]
             sg.exchange(D, c.d_out)
             ops.agg_sum(sg.bwd, D, H, c.d_out, post_scale=s)            # H = A_hat^T D
             ref_scale = self._pre_scale(l - 1)
-            if l == 1:
+            if l == 1 and self._x_fits(B[1]):
+                # regather A_1 = act((A_hat X) W_0) chunk by chunk from the
+                # feature rows themselves, streamed into the consumed buffer
+                # of D (one host pass; the rows stay there for the layer-0
+                # backward and the next epoch's forward)
+                c0 = cfg[0]
+                s0 = self._scale(c0)
+                X = B[1][:, : c0.ld_in]
+                self._stream(self.x_src, None, stash_to=B[1])
+                sg.exchange(X, c0.d_in)
+                for (r0, r1), spec in zip(sg.chunks, sg.fwd_chunks):
+                    n = r1 - r0
+                    N = self.nc[:n, : c0.ld_in]
+                    ops.agg_sum(spec, X, N, c0.d_in, src_scale=s0, post_div_deg=not c0.sym,
+                                post_scale=_rows(s0, r0, r1))
+                    a = self.ac[:n, : c.ld_in]
+                    ops.gemm(N, W[0], a, n, c0.d_out, c0.d_in, relu_out=True)
+                    self._hidden_grad(l, a, H, B[0], r0, r1, ref_scale)
+                self._xbuf = B[1]
+            elif l == 1:
                 # regather A_1 = act(A_hat (X W_0)) chunk by chunk from P_0
                 c0 = cfg[0]
                 s0 = self._scale(c0)
@@ -546,9 +598,25 @@ class StreamingEngine:
         # dA_l rows replace the (consumed) H rows: row copy kernel (K1, identity rows)
         ops.gather_rows(d, self.sg.self_ids[:n], out[r0:r1], c.ld_in)
 
-    def _backward_first(self, D: torch.Tensor, s) -> None:
-        """Layer 0: dW_0 = X^T (A_hat^T D), chunk by chunk with X streamed."""
+    def _x_fits(self, buf: torch.Tensor) -> bool:
+        """Whether the feature rows can live in layer buffer ``buf`` (same
+        row width, so every chunk is one contiguous block)."""
+        return (self.stash_on and buf.shape[1] == self.x_src.width and buf.shape[0] >= self.V
+                and buf.is_contiguous())
+
+    def _backward_first(self, D: torch.Tensor, s, free: torch.Tensor) -> None:
+        """Layer 0: dW_0 = X^T (A_hat^T D), chunk by chunk with X streamed.
+
+        ``free`` is the other layer buffer, unused until the next epoch: the
+        streamed feature rows are copied into its rows instead of the chunk
+        buffers, so the next epoch's layer-0 transform reads them from HBM
+        instead of over the host link again (GRD_STREAM_STASH=0: off)."""
         c = self.cfg[0]
+        stash_from = stash_to = None
+        if self._xbuf is free:          # the hidden layer-1 regather left X here
+            stash_from = free
+        elif self._x_fits(free):
+            stash_to = free
         specs = self.sg.bwd_chunks
 
         spec_of = {r0: sp for (r0, _), sp in zip(self.sg.chunks, specs)}
@@ -559,7 +627,8 @@ class StreamingEngine:
             h = self.nc[:n, : c.ld_out]
             ops.agg_sum(spec_of[r0], D, h, c.d_out, post_scale=_rows(s, r0, r1))
             ops.wgrad_sgd(x, h, self.wts.dw[0], c.d_in, c.d_out, n, accumulate=True)
-        self._stream(self.x_src, step)
+        self._stream(self.x_src, step, stash_to=stash_to, stash_from=stash_from)
+        self._xbuf = free if (stash_to is not None or stash_from is not None) else None
 
     def _last_layer(self, B: list) -> None:
         """Forward, loss and backward of the last layer in one chunked pass;
