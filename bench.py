@@ -123,7 +123,11 @@ def build_workload(spec):
     ds = g2.make_random_dataset(g, feature_dim=spec["F"], num_classes=spec["C"], seed=SEED + 1,
                                 feature_dtype=np.dtype(spec.get("feature_dtype", "float64")))
     t1 = time.perf_counter()
-    part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2))
+    # GPU partitioner when the GPU generator ran: bit-identical labels, trace
+    # and iteration count (tests/test_gpu_partition.py, reference digests in
+    # tests/test_gpu_golden_scale.py)
+    part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2),
+                                        device="cuda" if gpu_gen else None)
     t_part = time.perf_counter() - t1
     t2 = time.perf_counter()
     # bit-identical to the host plan (tests/test_gpu_plan.py)
@@ -136,7 +140,7 @@ def build_workload(spec):
                             seed=SEED + 3, aggregation_mode=spec["mode"],
                             heads=spec.get("heads", 4))
     prep = {"generate_s": round(t_gen, 3), "generator": "gpu" if gpu_gen else "host", "partition_s": round(t_part, 3),
-            "plan_s": round(t_plan, 3), "partitioner_iterations": part.iterations}
+            "partitioner": "gpu" if gpu_gen else "host", "plan_s": round(t_plan, 3), "partitioner_iterations": part.iterations}
     return g, ds, plan, model, prep
 
 
@@ -557,7 +561,8 @@ def run_sharded_stream(args, spec, rank, world, dev, backend):
     lab = torch.empty(n, dtype=torch.int32, device=dev if backend == "nccl" else "cpu")
     t1 = time.perf_counter()
     if rank == 0:
-        part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2))
+        part = g2.switching_aware_partition(g, spec["P"], g2.PartitionerParams(seed=SEED + 2),
+                                            device=dev)
         lab.copy_(torch.from_numpy(part.labels.astype(np.int32)))
     dist.broadcast(lab, 0)
     labels = lab.cpu().numpy()

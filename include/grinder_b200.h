@@ -98,6 +98,27 @@ int grd_sa_partition(int64_t num_vertices, const int64_t* src_ptr,
                      double* initial_objective, int32_t* iterations,
                      int32_t* converged, int32_t num_threads);
 
+/* Device analysis pass of the switching-aware partitioner (partition.py:
+ * 140-200 _analyze_kernel; GPU variant of the analysis inside
+ * grd_sa_partition): for every vertex v of the device CSR, with `labels`
+ * and the partition `sizes` (int64[p]) of the current iteration, writes its
+ * f64 objective term terms[v] = (1 + share_own) - sizes[own] / denom and its
+ * preference slots prefs[s * n + v] (s < group_depth; the top partitions of
+ * its out-neighbours by (count desc, id asc), all slots = p when the top one
+ * is its own partition or it has no neighbours), and adds the number of
+ * candidates (top partition != own) to *num_candidates (device u64).  The
+ * caller sums `terms` sequentially in vertex order (grd_sum_sequential) and
+ * relocates (partition.switching_aware_partition(..., device="cuda")).
+ * 2 <= num_partitions <= 1024.  All pointers are device memory. */
+int grd_sa_analyze(int64_t num_vertices, const int64_t* src_ptr, const int32_t* dst_idx,
+                   const int32_t* labels, const int64_t* sizes, int32_t num_partitions,
+                   int32_t group_depth, double denom, double* terms, int32_t* prefs,
+                   unsigned long long* num_candidates, void* stream);
+
+/* Left-to-right f64 sum of x[0..n) (the reference's sequential objective
+ * loop, partition.py:190-199), host memory. */
+int grd_sum_sequential(const double* x, int64_t n, double* out);
+
 /* Partition plan, bit-exact with plan.py:75-136 build_partition_plan.
  * Layout (concatenated over partitions in ascending id):
  *   part_ptr[P+1]        offsets of each partition's targets in perm

@@ -151,6 +151,9 @@ SIGNATURES = {
     "grd_kronecker_keys": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "grd_sa_partition": (c_i32, [c_i64, c_vp, c_vp, c_i32, ctypes.POINTER(GrdPartitionerParams),
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "grd_sa_analyze": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_vp, c_vp, c_vp,
+                               c_vp]),
+    "grd_sum_sequential": (c_i32, [c_vp, c_i64, c_vp]),
     "grd_plan_create": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "grd_plan_sizes": (c_i32, [c_vp, c_vp, c_vp]),
     "grd_plan_export": (c_i32, [c_vp] + [c_vp] * 9),

@@ -419,6 +419,15 @@ extern "C" int grd_sa_partition(int64_t num_vertices, const int64_t* src_ptr,
     return 0;
 }
 
+extern "C" int grd_sum_sequential(const double* x, int64_t n, double* out) {
+    clear_error();
+    if (!out || (n > 0 && !x)) return fail(kErrArg, "sum_sequential: null argument");
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += x[i];
+    *out = acc;
+    return 0;
+}
+
 // --------------------------------------------------------------------------
 // Partition plan (plan.py:75-136).  The (owner, id) order of every gather
 // map is the global "perm" order (targets of partition 0 ascending, then 1,

@@ -140,8 +140,10 @@ def partition_objective(graph: CsrGraph, labels: np.ndarray, num_partitions: int
 
 def switching_aware_partition(graph: CsrGraph, num_partitions: int,
                               params: PartitionerParams | None = None,
-                              num_threads: int | None = None) -> PartitionResult:
-    """Iterative grouped relocation under a hard capacity (partition.py:254-321)."""
+                              num_threads: int | None = None, device=None) -> PartitionResult:
+    """Iterative grouped relocation under a hard capacity (partition.py:254-321).
+    ``device="cuda"`` runs the iterations on the GPU (same labels, trace and
+    iteration count, bit for bit: :func:`_sa_partition_gpu`)."""
     params = params or PartitionerParams()
     n, p = graph.num_vertices, num_partitions
     if p < 1:
@@ -151,6 +153,8 @@ def switching_aware_partition(graph: CsrGraph, num_partitions: int,
         return PartitionResult(labels, 1, [], partition_objective(graph, labels, 1, params.alpha_balance),
                                True, 0, [n])
     labels = random_partition(n, p, params.seed)
+    if device is not None and str(device).startswith("cuda") and _gpu_fits(n, p, params.group_depth):
+        return _sa_partition_gpu(graph, p, params, labels, device)
     src_ptr = np.ascontiguousarray(graph.src_ptr, dtype=np.int64)
     dst_idx = np.ascontiguousarray(graph.dst_idx, dtype=np.int32)
     trace = np.zeros(params.max_iters, dtype=np.float64)
@@ -170,6 +174,130 @@ def switching_aware_partition(graph: CsrGraph, num_partitions: int,
                            objective_trace=[float(x) for x in trace[:k]],
                            initial_objective=float(init[0]), converged=bool(conv[0]),
                            iterations=k, max_size_per_iteration=[int(x) for x in sizes[:k + 1]])
+
+
+def _gpu_fits(n: int, p: int, depth: int) -> bool:
+    """The device path packs (preference slots, vertex id) into one int64
+    sort key and keeps a per-warp histogram of p counters."""
+    return p <= 1024 and (p + 1) ** depth * max(n, 1) < (1 << 62)
+
+
+def _relocate_sorted(prefs, lab, sizes, p: int, cap_limit: int) -> None:
+    """_relocate_kernel (partition.py:203-251) on torch tensors (any device):
+    ``prefs`` [depth, n] int32 preference slots, ``lab`` [n] int32 labels
+    (updated in place), ``sizes`` [p] int64 pre-iteration sizes.  Candidates
+    (slot 0 != p) are ordered by one sort of (slot_0, .., slot_{d-1}, id)
+    packed base p+1; equal (target, tail) keys are the reference's runs,
+    and per target block the first longest run moves its first
+    min(len, capacity) vertices."""
+    import torch
+    dev = lab.device
+    depth, n = prefs.shape
+    base = p + 1
+    ids = torch.nonzero(prefs[0] != p).squeeze(1)
+    key = prefs[0][ids].long()
+    for s_ in range(1, depth):
+        key = key * base + prefs[s_][ids].long()
+    order = torch.sort(key * n + ids).values
+    del key, ids
+    gval, gcount = torch.unique_consecutive(order // n, return_counts=True)
+    if gval.numel() == 0:
+        return
+    tgt = gval // base ** (depth - 1)
+    gstart = torch.cumsum(gcount, 0) - gcount
+    best = torch.zeros(p, dtype=torch.int64, device=dev).scatter_reduce(
+        0, tgt, gcount, "amax", include_self=False)
+    G = gval.numel()
+    first = torch.full((p,), G, dtype=torch.int64, device=dev)
+    win = gcount == best[tgt]
+    first.scatter_reduce_(0, tgt[win], torch.arange(G, device=dev)[win], "amin")
+    ts = torch.nonzero(first < G).squeeze(1)
+    g = first[ts]
+    take = torch.minimum(gcount[g], (cap_limit - sizes[ts]).clamp_min(0))
+    for t, a, k in zip(ts.tolist(), gstart[g].tolist(), take.tolist()):
+        if k:
+            lab[order[a:a + k] % n] = t
+
+
+def _sa_partition_gpu(graph: CsrGraph, p: int, params: PartitionerParams, labels: np.ndarray,
+                      device) -> PartitionResult:
+    """switching_aware_partition's iterations on the GPU (partition.py:279-321).
+
+    Per iteration: the analysis pass is the sm_100a kernel grd_sa_analyze
+    (terms, preference slots, candidate count; neighbour labels read through
+    dst_idx, so the reference's dst_part refresh is fused away); the f64
+    objective is the sequential sum of the terms in vertex order on the host
+    (grd_sum_sequential: the reference's loop order, hence its bits); the
+    candidate order — np.lexsort(prefs[::-1]) restricted to candidates — is
+    one device sort of (slot_0, .., slot_{d-1}, vertex id) packed base p+1
+    into an int64 key; the relocation (partition.py:203-251) is segment
+    arithmetic on the sorted keys: equal (target, tail) keys are the
+    reference's runs, the first longest run of every target block wins and
+    its first min(len, capacity) vertices (ascending id) move."""
+    import torch
+    dev = torch.device(device)
+    n = graph.num_vertices
+    depth = params.group_depth
+    denom = params.alpha_balance * n / p
+    cap_limit = math.floor(params.beta * n / p + 1e-9)
+    L = _lib.lib()
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        src_ptr = torch.from_numpy(np.ascontiguousarray(graph.src_ptr, dtype=np.int64)).to(dev)
+        dst_idx = torch.from_numpy(np.ascontiguousarray(graph.dst_idx, dtype=np.int32)).to(dev)
+        if dst_idx.numel() == 0:        # edgeless graph: a valid (never read) pointer
+            dst_idx = torch.zeros(1, dtype=torch.int32, device=dev)
+        lab = torch.from_numpy(labels).to(dev)
+        terms = torch.empty(n, dtype=torch.float64, device=dev)
+        prefs = torch.empty((depth, n), dtype=torch.int32, device=dev)
+        cand = torch.zeros(1, dtype=torch.int64, device=dev)
+        terms_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        out = np.zeros(1, dtype=np.float64)
+
+        def analyze():
+            sizes = torch.bincount(lab, minlength=p)
+            cand.zero_()
+            _lib.check(L.grd_sa_analyze(n, src_ptr.data_ptr(), dst_idx.data_ptr(), lab.data_ptr(),
+                                        sizes.data_ptr(), p, depth, denom, terms.data_ptr(),
+                                        prefs.data_ptr(), cand.data_ptr(), stream), "sa_analyze")
+            terms_host.copy_(terms)
+            _lib.check(L.grd_sum_sequential(terms_host.data_ptr(), n, _lib.ptr(out)), "sum_sequential")
+            return float(out[0]), int(cand.item()), sizes
+
+        obj_prev, num_candidates, sizes = analyze()
+        initial_objective = obj_prev
+        trace: list[float] = []
+        max_sizes = [int(sizes.max().item())]
+        converged, iterations, streak = False, 0, 0
+        for _ in range(params.max_iters):
+            if num_candidates == 0:
+                converged = True
+                break
+            _relocate_sorted(prefs, lab, sizes, p, cap_limit)
+            iterations += 1
+            obj_cur, num_candidates, sizes = analyze()
+            trace.append(obj_cur)
+            max_sizes.append(int(sizes.max().item()))
+            if obj_prev != 0.0:
+                rel = (obj_cur - obj_prev) / abs(obj_prev)
+            else:
+                rel = 0.0 if obj_cur == 0.0 else math.inf
+            if rel < params.epsilon:
+                streak += 1
+                if streak >= params.patience:
+                    converged = True
+                    break
+            else:
+                streak = 0
+            obj_prev = obj_cur
+        else:
+            converged = num_candidates == 0
+        out_labels = lab.cpu().numpy().astype(np.int32)
+        del src_ptr, dst_idx, lab, terms, prefs
+    torch.cuda.empty_cache()
+    return PartitionResult(labels=out_labels, num_partitions=p, objective_trace=trace,
+                           initial_objective=initial_objective, converged=converged,
+                           iterations=iterations, max_size_per_iteration=max_sizes)
 
 
 def expansion_ratio(graph: CsrGraph, labels: np.ndarray, num_partitions: int,

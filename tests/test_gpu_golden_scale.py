@@ -1,6 +1,6 @@
 """GPU parity at the papers / products shapes against the reference itself.
 
-* The GPU Kronecker generator and the GPU plan builder reproduce the
+* The GPU Kronecker generator, the GPU partitioner and the GPU plan builder reproduce the
   reference's graph and plan digests at configs[1]'s graph
   (generate_kronecker(21, 30, 0), P = 8) and at the papers-shaped
   generate_kronecker(22, 12, 0) with P = 16 — against reference-produced
@@ -38,7 +38,9 @@ def papers():
     gold = load("papers_s22.npz")
     scale, deg, F, C, L, H, P = [int(x) for x in gold["spec"]]
     g = g2.generate_kronecker(scale, deg, seed=0, device="cuda")
-    labels = g2.switching_aware_partition(g, P, g2.PartitionerParams(seed=2)).labels
+    # the GPU partitioner (bench.py's): its labels are checked against the
+    # reference's digest below
+    labels = g2.switching_aware_partition(g, P, g2.PartitionerParams(seed=2), device="cuda").labels
     plan = g2.build_partition_plan(g, labels, P, device="cuda")
     ds = g2.make_random_dataset(g, feature_dim=F, num_classes=C, seed=1,
                                 feature_dtype=np.float32)
@@ -62,6 +64,8 @@ def test_gpu_generator_and_plan_match_reference_products():
     assert digest(g.src_ptr, g.dst_idx) == str(gold["graph_digest"])
     labels = g2.switching_aware_partition(g, 8, g2.PartitionerParams(seed=2)).labels
     assert digest(labels) == str(gold["sa_labels_digest"])
+    dev = g2.switching_aware_partition(g, 8, g2.PartitionerParams(seed=2), device="cuda").labels
+    assert digest(dev) == str(gold["sa_labels_digest"])
     plan = g2.build_partition_plan(g, labels, 8, device="cuda")
     for q in range(8):
         assert plan_digest(plan.topology(q)) == str(gold[f"plan_digest_{q}"]), f"partition {q}"
