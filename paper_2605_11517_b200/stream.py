@@ -592,11 +592,27 @@ class StreamingEngine:
         n = r1 - r0
         Hc = H[r0:r1]
         ops.wgrad_sgd(a, Hc, self.wts.dw[l], c.d_in, c.d_out, n, accumulate=True)
+        if out.data_ptr() == H.data_ptr() and self._gemm_rowwise(c):
+            # dA_l rows written straight over the H rows they are computed
+            # from: one N tile and no K split, so every CTA has loaded its
+            # rows' whole K extent before its epilogue stores them
+            ops.gemm(Hc, self.wts.w[l], out[r0:r1, : c.ld_in], n, c.d_in, c.d_out, trans_b=True,
+                     row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
+            return
         d = self.dc[:n, : c.ld_in]
         ops.gemm(Hc, self.wts.w[l], d, n, c.d_in, c.d_out, trans_b=True,
                  row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
         # dA_l rows replace the (consumed) H rows: row copy kernel (K1, identity rows)
         ops.gather_rows(d, self.sg.self_ids[:n], out[r0:r1], c.ld_in)
+
+    @staticmethod
+    def _gemm_rowwise(c) -> bool:
+        """Whether the input-gradient GEMM ``H W^T`` (n = d_in, k = d_out)
+        runs as one N tile without a K split (ops.gemm / grd_gemm_tc.cu
+        pick_bn), so it may overwrite its own A rows."""
+        bn_max = int(os.environ.get("GRD_GEMM_BN_MAX", "256"))
+        return (os.environ.get("GRD_STREAM_INPLACE", "1") != "0" and c.ld_in <= min(bn_max, 128)
+                and not ops._KSPLIT_TB)
 
     def _x_fits(self, buf: torch.Tensor) -> bool:
         """Whether the feature rows can live in layer buffer ``buf`` (same
