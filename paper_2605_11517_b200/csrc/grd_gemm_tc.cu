@@ -84,6 +84,8 @@ struct Params {
     int kch;                        // K blocks per TMEM accumulation (0: the whole K)
     int hi_raw;                     // 1: the raw fp32 tile is the hi operand (the MMA reads
                                     // only its tf32 bits), the converter writes lo alone
+    int lo_slots;                   // > 0: lo tiles live in their own ring of this many slots
+                                    // (a stage then carries raw operands only: deeper ring)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -558,13 +560,26 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // B-resident mode (small packed weight, one N tile, no split-K): stages
     // carry A only, and this CTA's B hi|lo tiles of every K block sit after
     // the ring for the whole launch — loaded once instead of once per M tile.
+    // lo ring (p.lo_slots > 0): a stage carries the raw operands only
+    // (A raw | B raw, or B's packed hi|lo) and the converters write the lo
+    // tiles into a separate ring of lo_slots slots, released by the MMAs that
+    // read them; a lo tile lives only between its stage's conversion and
+    // MMAs, so the same shared memory holds a raw ring twice as deep — the
+    // loads in flight per SM are what bounds these HBM-streaming shapes.
     const bool bres = p.b_resident != 0;
+    const bool lring = p.lo_slots > 0;
+    const int SL = lring ? p.lo_slots : 0;
+    const bool b_conv = p.b_mode != kPacked;                // B split by the converters
     const int64_t nkb_b = (p.k + kBK - 1) / kBK;
-    const uint32_t stage_bytes = bres ? 2u * a_bytes : 2u * (a_bytes + b_bytes);
-    uint8_t* bres_smem = smem + S * stage_bytes;
+    const uint32_t stage_bytes = lring ? a_bytes + (bres ? 0u : (b_conv ? b_bytes : 2u * b_bytes))
+                                       : (bres ? 2u * a_bytes : 2u * (a_bytes + b_bytes));
+    const uint32_t lo_bytes = a_bytes + (b_conv ? b_bytes : 0u);
+    uint8_t* lo_ring = smem + S * stage_bytes;
+    const uint32_t b_off = lring ? a_bytes : 2u * a_bytes;  // B's offset inside a stage
+    uint8_t* bres_smem = lo_ring + SL * lo_bytes;
     const uint32_t bres_bytes = bres ? static_cast<uint32_t>(nkb_b) * 2u * b_bytes : 0u;
     // TMA-store staging: 4 KB per epilogue warp, 1024-byte aligned (swizzle atoms)
-    uint8_t* epi_stage = smem + ((S * stage_bytes + bres_bytes + 1023u) & ~1023u);
+    uint8_t* epi_stage = smem + ((static_cast<uint32_t>(bres_smem - smem) + bres_bytes + 1023u) & ~1023u);
     const uint32_t epi_bytes = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u : 0u;
     uint64_t* bars = reinterpret_cast<uint64_t*>(p.tma_store ? epi_stage + epi_bytes : bres_smem + bres_bytes);
     uint64_t* full = bars;             // [S]
@@ -573,7 +588,8 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     uint64_t* tfull = bars + 3 * S;    // [2]
     uint64_t* tempty = bars + 3 * S + 2;   // [2]
     uint64_t* bready = bars + 3 * S + 4;   // [1] resident B landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
+    uint64_t* lofree = bars + 3 * S + 5;   // [SL] lo slot consumed by its MMAs
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5 + SL);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -617,6 +633,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mbar_init(tempty + a, kEpiThreads * nc);
         }
         mbar_init(bready, 1);
+        for (int l = 0; l < SL; ++l) mbar_init(lofree + l, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
         if (p.b_mode != kPacked) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
@@ -668,7 +685,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                    static_cast<int32_t>(k0), full + s);
                     }
                     if (bres) continue;
-                    uint8_t* bdst = st + 2 * a_bytes;
+                    uint8_t* bdst = st + b_off;
                     if (pair) {
                         // this CTA's half of the B tile: rows [crank * bnl, +bnl)
                         const int64_t nb0 = n0 + crank * bnl;
@@ -765,9 +782,12 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     mbar_wait(conv + s, static_cast<uint32_t>((g / S) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     uint8_t* st = smem + s * stage_bytes;
-                    const uint32_t ah = smem_u32(st), al = smem_u32(st + a_bytes);
-                    const uint8_t* bst = bres ? bres_smem + kb * 2 * b_bytes : st + 2 * a_bytes;
-                    const uint32_t bh = smem_u32(bst), bl = smem_u32(bst + b_bytes);
+                    const int slot = lring ? static_cast<int>(g % SL) : 0;
+                    uint8_t* lo = lring ? lo_ring + slot * lo_bytes : st + a_bytes;
+                    const uint32_t ah = smem_u32(st), al = smem_u32(lo);
+                    const uint8_t* bst = bres ? bres_smem + kb * 2 * b_bytes : st + b_off;
+                    const uint32_t bh = smem_u32(bst);
+                    const uint32_t bl = smem_u32((lring && b_conv) ? lo + a_bytes : bst + b_bytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 8; ++kk) {
                         const uint64_t dah = make_desc(ah + kk * a_step, a_lbo, a_sbo, a_lay);
@@ -788,6 +808,10 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     if constexpr (kPair) mma_commit_pair(empty + s);   // both CTAs' stage s
                     else if (C == 1) mma_commit(empty + s);
                     else mma_commit_mc(empty + s, cmask);   // release the stage in every CTA
+                    if (lring) {                            // and the lo slot (each CTA its own)
+                        if constexpr (kPair) mma_commit_pair(lofree + slot);
+                        else mma_commit(lofree + slot);
+                    }
                     if constexpr (kFresh) {
                         if constexpr (kPair) mma_commit_pair(tfull + acc);
                         else mma_commit(tfull + acc);
@@ -812,9 +836,16 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int s = static_cast<int>(g % S);
                 mbar_wait(full + s, static_cast<uint32_t>((g / S) & 1));
                 uint8_t* st = smem + s * stage_bytes;
-                split_tile(st, st + a_bytes, a_bytes, ctid, kConvThreads, !p.hi_raw);
-                uint8_t* bh = st + 2 * a_bytes;
-                if (p.b_mode != kPacked) split_tile(bh, bh + b_bytes, b_bytes, ctid, kConvThreads, !p.hi_raw);
+                uint8_t* lo = st + a_bytes;
+                if (lring) {
+                    const int slot = static_cast<int>(g % SL);
+                    if (g >= static_cast<uint64_t>(SL))
+                        mbar_wait(lofree + slot, static_cast<uint32_t>((g / SL - 1) & 1));
+                    lo = lo_ring + slot * lo_bytes;
+                }
+                split_tile(st, lo, a_bytes, ctid, kConvThreads, !p.hi_raw);
+                uint8_t* bh = st + b_off;
+                if (b_conv) split_tile(bh, lring ? lo + a_bytes : bh + b_bytes, b_bytes, ctid, kConvThreads, !p.hi_raw);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (pair) mbar_arrive_cluster(conv + s, 0);     // the issuing CTA's barrier
                 else mbar_arrive(conv + s);
@@ -1227,6 +1258,22 @@ inline int hi_raw_pref() {
     return v;
 }
 
+// lo tiles in a ring of their own (GRD_GEMM_LORING = slots, 0: inside every
+// stage).  Default: a 2-slot ring for the weight gradients (both operands
+// raw and MN-major: -8..-11 % at the papers shapes, flat at products) and
+// lo tiles inside the stages for the forward / input-gradient GEMMs, where
+// the deeper raw ring measured 0-60 % slower (profiles/r02_ncu_gemm_papers.md)
+inline int loring_pref(bool weight_grad) {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("GRD_GEMM_LORING");
+        v = e ? atoi(e) : -1;
+        if (v > 4) v = -1;
+    }
+    if (v >= 0) return v;
+    return weight_grad ? 2 : 0;
+}
+
 // packed weight operand resident in shared memory when it fits (GRD_GEMM_BRES = 1 / 0)
 inline int bres_pref() {
     static int v = -1;
@@ -1420,19 +1467,36 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         make_map(&map_c, g.c, g.m, (g.n + 3) / 4 * 4, g.ldc, 32, 32))
         p.tma_store = 1;
     const uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;
-    if (bres_pref() && p.b_mode == kPacked && p.splits == 1 && g.n <= p.bn && (p.pair || cluster_pref() == 1)) {
-        const uint32_t res = static_cast<uint32_t>((g.k + kBK - 1) / kBK) * 2u * bnl_bytes;
-        const uint32_t st_a = 2u * kBM * 128u;
-        if (res + 3u * st_a + epi <= 220u * 1024u) {
-            resident = res;
-            stage = st_a;
+    const bool bres_ok = bres_pref() && p.b_mode == kPacked && p.splits == 1 && g.n <= p.bn &&
+                         (p.pair || cluster_pref() == 1);
+    const uint32_t res_b = static_cast<uint32_t>((g.k + kBK - 1) / kBK) * 2u * bnl_bytes;
+    const uint32_t a_raw = kBM * 128u;
+    uint32_t lo_total = 0;
+    p.lo_slots = loring_pref(p.a_mode == kMNMajorTma);
+    if (p.lo_slots > 0) {
+        // raw-only stages + a ring of lo slots (see the kernel's layout note)
+        const bool b_conv = p.b_mode != kPacked;
+        const uint32_t lo = a_raw + (b_conv ? bnl_bytes : 0u);
+        lo_total = static_cast<uint32_t>(p.lo_slots) * lo;
+        stage = a_raw + (b_conv ? bnl_bytes : 2u * bnl_bytes);
+        if (bres_ok && res_b + 3u * a_raw + lo_total + epi <= 220u * 1024u) {
+            resident = res_b;
+            stage = a_raw;
             p.b_resident = 1;
         }
+        p.stages = static_cast<int>((220u * 1024u - resident - epi - lo_total) / stage);
+        if (p.stages > 8) p.stages = 8;
+    } else {
+        if (bres_ok && res_b + 3u * 2u * a_raw + epi <= 220u * 1024u) {
+            resident = res_b;
+            stage = 2u * a_raw;
+            p.b_resident = 1;
+        }
+        p.stages = static_cast<int>((220u * 1024u - resident - epi) / stage);
+        if (p.stages > (p.b_resident ? 6 : 4)) p.stages = p.b_resident ? 6 : 4;
     }
-    p.stages = static_cast<int>((220u * 1024u - resident - epi) / stage);
-    if (p.stages > (p.b_resident ? 6 : 4)) p.stages = p.b_resident ? 6 : 4;
     if (p.stages < 2) p.stages = 2;
-    const size_t smem = static_cast<size_t>(p.stages) * stage + resident + epi + 1024 + 256;
+    const size_t smem = static_cast<size_t>(p.stages) * stage + lo_total + resident + epi + 1024 + 512;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;
     if (!attr) {

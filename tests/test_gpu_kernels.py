@@ -460,3 +460,45 @@ print('ok')
     env = dict(os.environ, GRD_GEMM_TMA_STORE=tma)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("loring", ["0", "1", "2", "3"])
+def test_gemm_lo_ring_depths(loring):
+    """The lo-tile ring (GRD_GEMM_LORING slots; 0 = lo tiles inside every
+    stage) on every operand mode: K-major A with the packed weight resident
+    or staged, trans_b, CTA pairs (256-wide tiles), MN-major weight
+    gradients with split-K and CTA pairs; with and without TMA-store
+    epilogues.  Read once per process, so each setting runs in a child."""
+    import subprocess
+    import sys
+    code = f"""
+import sys; sys.path.insert(0, {str(Path(__file__).resolve().parents[1])!r})
+import numpy as np, torch
+from paper_2605_11517_b200 import ops
+rng = np.random.default_rng(7)
+def dev(x): 
+    t = ops.zeros_rows(x.shape[0], x.shape[1], 'cuda'); t[:, :x.shape[1]] = torch.from_numpy(x.astype(np.float32)).cuda(); return t
+for m, n, k, tb in [(70000, 128, 128, 0), (5000, 172, 128, 0), (5000, 128, 172, 1), (9000, 256, 256, 0),
+                    (3000, 47, 300, 0), (40000, 512, 100, 0), (1300, 256, 70, 1)]:
+    a = rng.normal(size=(m, k)); b = rng.normal(size=(n, k) if tb else (k, n))
+    rs = rng.uniform(0.5, 1.5, size=m).astype(np.float32)
+    c = ops.zeros_rows(m, n, 'cuda')
+    ops.gemm(dev(a), dev(b), c, m, n, k, trans_b=bool(tb), row_scale=torch.from_numpy(rs).cuda())
+    want = (a @ (b.T if tb else b)) * rs[:, None]
+    got = c[:, :n].double().cpu().numpy()
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 5e-6, (m, n, k, tb, err)
+for m, n, k in [(128, 128, 200000), (128, 172, 50000), (256, 256, 70000), (100, 47, 3000), (384, 128, 30000)]:
+    a = rng.normal(size=(k, m)).astype(np.float32); b = rng.normal(size=(k, n)).astype(np.float32)
+    dw = ops.zeros_rows(m, n, 'cuda')
+    ops.wgrad_sgd(dev(a), dev(b), dw, m, n, k)
+    want = a.astype(np.float64).T @ b.astype(np.float64)
+    got = dw[:, :n].double().cpu().numpy()
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 5e-6, (m, n, k, err)
+print('ok')
+"""
+    for tma in ("1", "0"):
+        env = dict(os.environ, GRD_GEMM_LORING=loring, GRD_GEMM_TMA_STORE=tma)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, (tma, r.stdout + r.stderr)
