@@ -15,6 +15,8 @@ if [ -z "$SKIP_NCU" ]; then
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/dram_$W.csv python tools/profile_epoch.py $W > gpurun_out/ncu_dram_$W.log 2>&1
   echo "ncu rc=$?"
+  # merge into the committed table (other workloads' entries stay)
+  [ -f gpurun_out/traffic.json ] || cp profiles/traffic.json gpurun_out/traffic.json
   python tools/dram_traffic.py gpurun_out/dram_$W.csv $W gpurun_out/traffic.json
 fi
 if [ -z "$SKIP_REF" ]; then
