@@ -217,6 +217,16 @@ class StreamGraph:
     def exchange(self, buf: torch.Tensor, width: int) -> None:
         """One device holds every row: nothing to exchange."""
 
+    def gat_pull(self):
+        """(pull spec, its edges' positions in the forward CSR) of GAT's
+        transposed pull: the in-CSR's transpose."""
+        if getattr(self, "_gat_pull", None) is None:
+            self._gat_pull = (self.bwd, _pull_perm(self))
+        return self._gat_pull
+
+    def reverse_add(self, buf: torch.Tensor, width: int) -> None:
+        """One device: no halo partial sums to return."""
+
     def scale(self, name: str | None) -> torch.Tensor | None:
         if name is None:
             return None
@@ -258,6 +268,15 @@ class ShardStreamGraph:
     def exchange(self, buf: torch.Tensor, width: int) -> None:
         self.dg.exchange(buf, width)
 
+    def gat_pull(self):
+        """GAT's transposed pull over the local in-CSR's transpose (every
+        local source row, owned targets only; engine.ShardDeviceGraph)."""
+        return self.dg.gat_pull()
+
+    def reverse_add(self, buf: torch.Tensor, width: int) -> None:
+        """Halo rows' partial sums back to their owners (engine.ShardDeviceGraph)."""
+        self.dg.reverse_add(buf, width)
+
     def scale(self, name: str | None) -> torch.Tensor | None:
         return self.dg.scale(name)
 
@@ -282,9 +301,8 @@ class StreamingEngine:
         self.V = sg.n_rows          # rows this engine computes (owned rows when sharded)
         self.NL = sg.n_local        # rows of the layer buffers (owned + halo when sharded)
         self.comm = sg.comm
-        if self.comm is not None and (model.kind not in ("gcn", "sage") or self.L > 3):
-            raise NotImplementedError("the sharded streaming engine trains GCN and GraphSAGE "
-                                      "models of <= 3 layers")
+        if self.comm is not None and self.L > 3:
+            raise NotImplementedError("the sharded streaming engine trains models of <= 3 layers")
         self.mode = model.aggregation_mode
         self.cfg = [_LayerCfg(l, self.dims, self.mode, False, l == self.L - 1, model.heads)
                     for l in range(self.L)]
@@ -829,7 +847,7 @@ class StreamingEngine:
         self.delta_self = torch.zeros_like(self.alpha_self)
         self.cdot = torch.zeros_like(self.alpha_self)
         self.st = ops.zeros_rows(self.NL, 2 * H, dev)
-        self.edge_perm = _pull_perm(sg)
+        self.pull, self.edge_perm = sg.gat_pull()
 
     def _gat_transform(self, l: int, src, P: torch.Tensor) -> None:
         """[P | s | t] = A_l W_ext -> P (src: a device matrix, or the streamed
@@ -842,6 +860,7 @@ class StreamingEngine:
         else:
             self._stream(src, lambda x, r0, r1: ops.gemm(x, wt.wext[l], P[r0:r1], r1 - r0, c.n_ext,
                                                          c.d_in))
+        self.sg.exchange(P, c.n_ext)                      # halo rows of [P | s | t]
         ops.gat_pack_scores(P, self.NL, c.heads, c.dhp, self.st)
         ops.gat_softmax(self.sg.fwd, P, c.heads, c.dhp, self.alpha, self.alpha_self, st=self.st)
 
@@ -854,9 +873,15 @@ class StreamingEngine:
         """dL/d[P | s | t] of layer l into G (engine.LayerwiseEngine's fused
         pull backward; c = gO . O is in self.cdot)."""
         c = self.cfg[l]
-        ops.gat_pull_bwd(self.sg.bwd, P, c.heads, c.dhp, self.edge_perm, self.alpha,
+        if self.NL > self.V:
+            # sharded: halo rows carry no gradient of their own (no self term);
+            # their rows of G collect partial sums for their owners
+            gO[self.V:].zero_()
+            self.cdot[self.V * c.heads:].zero_()
+        ops.gat_pull_bwd(self.pull, P, c.heads, c.dhp, self.edge_perm, self.alpha,
                          self.alpha_self, gO, self.cdot, self.delta, self.delta_self, G, st=self.st)
         ops.gat_dst_grad(self.sg.fwd, c.heads, c.dhp, self.delta, self.delta_self, G)
+        self.sg.reverse_add(G, c.hdp + c.heads)
 
     def _gat_input_grad(self, l: int, G: torch.Tensor, A: torch.Tensor, out: torch.Tensor) -> None:
         """Per chunk: gO_{l-1} = relu'(A_l) (G W_ext^T) and c_{l-1} = gO . A_l
@@ -940,6 +965,10 @@ class StreamingEngine:
             else:
                 ops.wgrad_sgd(A, G, wt.dwext[l], c.d_in, c.n_ext, V)
                 self._gat_input_grad(l, G, A, B1)
+        if self.comm is not None:      # every layer's dW_ext in one all-reduce
+            self.comm.all_reduce_sum(wt.grad_bucket)
+            self.stats.copy_(self.stats_all.sum(dim=0))
+            self.comm.all_reduce_sum(self.stats)
         # ---- SGD: dW, datt from dW_ext ----
         for l in range(L):
             c = cfg[l]

@@ -412,7 +412,7 @@ def _use_streaming(dataset: LabeledDataset, model: ModelState, comm=None) -> boo
         if forced == "stream" and streaming_supported(model) is not None:
             raise NotImplementedError(streaming_supported(model))
         return forced == "stream"
-    if streaming_supported(model) is not None or (comm is not None and model.kind == "gat"):
+    if streaming_supported(model) is not None or (comm is not None and model.num_layers > 3):
         return False
     free, _ = torch.cuda.mem_get_info()
     avail = free + torch.cuda.memory_reserved() - torch.cuda.memory_allocated()

@@ -181,17 +181,23 @@ def _setup_stream(mode="mean_self_loop"):
     plan = g2.build_partition_plan(g, part.labels, 6)
     # configs[3]'s structure: transform-first hidden layers, aggregate-first
     # last layer (GraphSAGE, configs[4]'s model: every layer transform-first)
-    model = g2.create_model(16, 7, num_layers=3, hidden_dim=8, seed=7, aggregation_mode=mode)
+    # GAT: 4 heads; "gat_l2" a two-layer model (layer 0's backward is the last's)
+    L = 2 if mode == "gat_l2" else 3
+    mode = "gat" if mode.startswith("gat") else mode
+    model = g2.create_model(16, 7, num_layers=L, hidden_dim=16 if mode == "gat" else 8, seed=7,
+                            aggregation_mode=mode)
     return ds, plan, model
 
 
-@pytest.mark.parametrize("mode", ["mean_self_loop", "sage_mean"])
+@pytest.mark.parametrize("mode", ["mean_self_loop", "sage_mean", "gat", "gat_l2"])
 def test_sharded_streaming_engine_matches_one_device(tmp_path, mode):
     """The layer-streaming engine over a rank's shard (owned rows streamed,
     halo rows of every aggregation's input exchanged, one bucketed weight-
-    gradient all-reduce, loss sums all-reduced): two ranks on one GPU equal
-    the single-device streaming engine within 1e-5 and keep replicated
-    weights bitwise equal."""
+    gradient all-reduce, loss sums all-reduced; GAT: halo rows of
+    [P | s | t], the transposed pull over the local in-CSR and the reverse
+    exchange of its halo partial sums): two ranks on one GPU equal the
+    single-device streaming engine within 1e-5 and keep replicated weights
+    bitwise equal."""
     import torch.multiprocessing as mp
     from paper_2605_11517_b200.stream import StreamSession
     with socket.socket() as s:
