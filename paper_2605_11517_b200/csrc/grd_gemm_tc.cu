@@ -86,6 +86,7 @@ struct Params {
                                     // only its tf32 bits), the converter writes lo alone
     int lo_slots;                   // > 0: lo tiles live in their own ring of this many slots
                                     // (a stage then carries raw operands only: deeper ring)
+    int epi_bufs;                   // TMA-store staging tiles per epilogue warp (1 or 2)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -354,6 +355,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void tma_store_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -409,6 +413,10 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
                                               int64_t ntiles, TileFn tile_of,
                                               const CUtensorMap* map_c = nullptr, uint8_t* stage = nullptr) {
     const bool tma = !kSplit && p.tma_store && stage != nullptr;
+    // two staging tiles per warp: a chunk is staged while the previous
+    // chunk's bulk store still reads the other tile
+    const int ebufs = p.epi_bufs > 1 ? 2 : 1;
+    int eb = 0;
     const int q = warp & 3;                               // TMEM lane quarter
     const int half = (warp - kEpiWarp0) >> 2;             // which interleaved column chunks
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
@@ -452,13 +460,19 @@ __device__ __forceinline__ void epilogue_loop(const Params& p, uint32_t tmem, ui
                     continue;
                 }
                 if (tma && chunks == 1) {
-                    if (lane == 0) tma_store_wait_read();     // the staging tile's last store has read it
+                    uint8_t* sb = stage + eb * 4096;
+                    // the staging tile's last store (ebufs chunks ago) has read it
+                    if (lane == 0) {
+                        if (ebufs > 1) tma_store_wait_read1();
+                        else tma_store_wait_read();
+                    }
                     __syncwarp();
-                    epi_stage_tma(p, v, row0 + lane, n0 + c0, in, stage, lane);
+                    epi_stage_tma(p, v, row0 + lane, n0 + c0, in, sb, lane);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0)
-                        tma_store_2d(map_c, stage, static_cast<int32_t>(n0 + c0), static_cast<int32_t>(row0));
+                        tma_store_2d(map_c, sb, static_cast<int32_t>(n0 + c0), static_cast<int32_t>(row0));
+                    eb = (eb + 1) % ebufs;
                     continue;
                 }
                 epi_store_direct<kSplit>(p, v, row0 + lane, n0 + c0, z, in);
@@ -580,7 +594,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t bres_bytes = bres ? static_cast<uint32_t>(nkb_b) * 2u * b_bytes : 0u;
     // TMA-store staging: 4 KB per epilogue warp, 1024-byte aligned (swizzle atoms)
     uint8_t* epi_stage = smem + ((static_cast<uint32_t>(bres_smem - smem) + bres_bytes + 1023u) & ~1023u);
-    const uint32_t epi_bytes = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u : 0u;
+    const uint32_t epi_bytes = p.tma_store ? static_cast<uint32_t>(kEpiWarps * p.epi_bufs) * 4096u : 0u;
     uint64_t* bars = reinterpret_cast<uint64_t*>(p.tma_store ? epi_stage + epi_bytes : bres_smem + bres_bytes);
     uint64_t* full = bars;             // [S]
     uint64_t* conv = bars + S;         // [S]
@@ -864,7 +878,7 @@ gemm_tf32x3_ws(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             epilogue_fresh<kPair>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of, kblocks_of);
         else
             epilogue_loop<kPair, kSplit>(p, tmem, tfull, tempty, warp, lane, cid, ncl, ntiles, tile_of, &map_c,
-                                         epi_stage + (warp - kEpiWarp0) * 4096);
+                                         epi_stage + (warp - kEpiWarp0) * 4096 * p.epi_bufs);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -1274,6 +1288,21 @@ inline int loring_pref(bool weight_grad) {
     return weight_grad ? 2 : 0;
 }
 
+// TMA-store staging tiles per epilogue warp (GRD_GEMM_EPI_BUFS = 1, 2 = two
+// when the stage ring keeps its depth, 3 = two up to the 227 KB limit).
+// Measured (tools/gemm_epibufs.sh): no gain at the papers shapes, products
+// 2 M x 256 x 256 +8 % slower — the staging wait is not the epilogue's limit,
+// so one tile stays the default.
+inline int epi_bufs_pref() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GRD_GEMM_EPI_BUFS");
+        v = e ? atoi(e) : 1;
+        if (v < 1 || v > 3) v = 1;
+    }
+    return v;
+}
+
 // packed weight operand resident in shared memory when it fits (GRD_GEMM_BRES = 1 / 0)
 inline int bres_pref() {
     static int v = -1;
@@ -1466,7 +1495,8 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         (g.ldc % 4) == 0 &&
         make_map(&map_c, g.c, g.m, (g.n + 3) / 4 * 4, g.ldc, 32, 32))
         p.tma_store = 1;
-    const uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;
+    p.epi_bufs = 1;
+    uint32_t epi = p.tma_store ? static_cast<uint32_t>(kEpiWarps) * 4096u + 1024u : 0u;
     const bool bres_ok = bres_pref() && p.b_mode == kPacked && p.splits == 1 && g.n <= p.bn &&
                          (p.pair || cluster_pref() == 1);
     const uint32_t res_b = static_cast<uint32_t>((g.k + kBK - 1) / kBK) * 2u * bnl_bytes;
@@ -1496,6 +1526,18 @@ cudaError_t grd_tc_gemm(const GrdTcGemm& g, cudaStream_t st) {
         if (p.stages > (p.b_resident ? 6 : 4)) p.stages = p.b_resident ? 6 : 4;
     }
     if (p.stages < 2) p.stages = 2;
+    // a second staging tile per epilogue warp when the ring keeps its depth
+    // (GRD_GEMM_EPI_BUFS = 1 / 2; default: 2 when free)
+    if (p.tma_store && epi_bufs_pref() > 1) {
+        const uint32_t epi2 = epi + static_cast<uint32_t>(kEpiWarps) * 4096u;
+        const uint32_t used = static_cast<uint32_t>(p.stages) * stage + lo_total + resident;
+        if (used + epi2 <= 220u * 1024u || epi_bufs_pref() == 3) {
+            if (used + epi2 + 1024 + 512 <= 227u * 1024u) {
+                epi = epi2;
+                p.epi_bufs = 2;
+            }
+        }
+    }
     const size_t smem = static_cast<size_t>(p.stages) * stage + lo_total + resident + epi + 1024 + 512;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static bool attr = false;

@@ -465,7 +465,8 @@ print('ok')
 @pytest.mark.parametrize("loring", ["0", "1", "2", "3"])
 def test_gemm_lo_ring_depths(loring):
     """The lo-tile ring (GRD_GEMM_LORING slots; 0 = lo tiles inside every
-    stage) on every operand mode: K-major A with the packed weight resident
+    stage) and the epilogue's staging tiles per warp (GRD_GEMM_EPI_BUFS) on
+    every operand mode: K-major A with the packed weight resident
     or staged, trans_b, CTA pairs (256-wide tiles), MN-major weight
     gradients with split-K and CTA pairs; with and without TMA-store
     epilogues.  Read once per process, so each setting runs in a child."""
@@ -498,7 +499,8 @@ for m, n, k in [(128, 128, 200000), (128, 172, 50000), (256, 256, 70000), (100, 
     assert err < 5e-6, (m, n, k, err)
 print('ok')
 """
-    for tma in ("1", "0"):
-        env = dict(os.environ, GRD_GEMM_LORING=loring, GRD_GEMM_TMA_STORE=tma)
+    # TMA-store epilogue with two / one staging tiles per warp, and per-row stores
+    for tma, ebufs in (("1", "2"), ("1", "1"), ("0", "2")):
+        env = dict(os.environ, GRD_GEMM_LORING=loring, GRD_GEMM_TMA_STORE=tma, GRD_GEMM_EPI_BUFS=ebufs)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0 and "ok" in r.stdout, (tma, r.stdout + r.stderr)
+        assert r.returncode == 0 and "ok" in r.stdout, (tma, ebufs, r.stdout + r.stderr)
