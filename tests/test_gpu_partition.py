@@ -28,7 +28,7 @@ def _same(a, b):
 
 @pytest.mark.parametrize("scale,deg,P,depth", [
     (7, 6, 3, 2), (8, 8, 4, 2), (8, 8, 4, 3), (9, 4, 6, 2), (12, 12, 16, 2), (13, 8, 33, 2),
-    (11, 16, 2, 4), (12, 6, 40, 3),
+    (11, 16, 2, 4), (12, 6, 40, 3), (11, 8, 300, 2),   # p > 256: int32 labels in the kernel
 ])
 def test_gpu_partitioner_matches_host(scale, deg, P, depth):
     g = g2.generate_kronecker(scale, deg, seed=scale)
