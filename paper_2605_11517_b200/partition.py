@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import math
 import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -248,52 +249,100 @@ def _sa_partition_gpu(graph: CsrGraph, p: int, params: PartitionerParams, labels
         if dst_idx.numel() == 0:        # edgeless graph: a valid (never read) pointer
             dst_idx = torch.zeros(1, dtype=torch.int32, device=dev)
         lab = torch.from_numpy(labels).to(dev)
-        terms = torch.empty(n, dtype=torch.float64, device=dev)
+        lab_prev = torch.empty_like(lab)
         prefs = torch.empty((depth, n), dtype=torch.int32, device=dev)
-        cand = torch.zeros(1, dtype=torch.int64, device=dev)
-        terms_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        out = np.zeros(1, dtype=np.float64)
+        # two analysis slots: while the host sums one pass's terms (the
+        # sequential f64 objective that fixes the convergence bits), the GPU
+        # already runs the next relocation + analysis speculatively; a stop
+        # decision restores the labels from before that relocation
+        terms = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+        terms_host = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        cand = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
+        copy_stream = torch.cuda.Stream(dev)
+        pool = ThreadPoolExecutor(max_workers=1)
+        slot = [0]
 
         def analyze():
+            """Launch one analysis pass: (future of its objective, candidates,
+            sizes, max size); the terms' D2H and host sum run beside the GPU."""
+            b = slot[0]
+            slot[0] ^= 1
             sizes = torch.bincount(lab, minlength=p)
-            cand.zero_()
+            cand[b].zero_()
             _lib.check(L.grd_sa_analyze(n, src_ptr.data_ptr(), dst_idx.data_ptr(), lab.data_ptr(),
-                                        sizes.data_ptr(), p, depth, denom, terms.data_ptr(),
-                                        prefs.data_ptr(), cand.data_ptr(), stream), "sa_analyze")
-            terms_host.copy_(terms)
-            _lib.check(L.grd_sum_sequential(terms_host.data_ptr(), n, _lib.ptr(out)), "sum_sequential")
-            return float(out[0]), int(cand.item()), sizes
+                                        sizes.data_ptr(), p, depth, denom, terms[b].data_ptr(),
+                                        prefs.data_ptr(), cand[b].data_ptr(), stream), "sa_analyze")
+            done = torch.cuda.Event()
+            done.record()
+            copy_stream.wait_event(done)
+            with torch.cuda.stream(copy_stream):
+                terms_host[b].copy_(terms[b], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(copy_stream)
+            res = np.zeros(1, dtype=np.float64)
 
-        obj_prev, num_candidates, sizes = analyze()
-        initial_objective = obj_prev
-        trace: list[float] = []
-        max_sizes = [int(sizes.max().item())]
-        converged, iterations, streak = False, 0, 0
-        for _ in range(params.max_iters):
-            if num_candidates == 0:
-                converged = True
-                break
-            _relocate_sorted(prefs, lab, sizes, p, cap_limit)
-            iterations += 1
-            obj_cur, num_candidates, sizes = analyze()
-            trace.append(obj_cur)
-            max_sizes.append(int(sizes.max().item()))
-            if obj_prev != 0.0:
-                rel = (obj_cur - obj_prev) / abs(obj_prev)
-            else:
-                rel = 0.0 if obj_cur == 0.0 else math.inf
-            if rel < params.epsilon:
-                streak += 1
-                if streak >= params.patience:
+            def total() -> float:
+                copied.synchronize()
+                _lib.check(L.grd_sum_sequential(terms_host[b].data_ptr(), n, _lib.ptr(res)),
+                           "sum_sequential")
+                return float(res[0])
+            fut = pool.submit(total)
+            return fut, int(cand[b].item()), sizes, int(sizes.max().item())
+
+        try:
+            fut, num_candidates, sizes, smax = analyze()
+            obj_prev = fut.result()
+            initial_objective = obj_prev
+            trace: list[float] = []
+            max_sizes = [smax]
+            converged, iterations, streak = False, 0, 0
+            pending = None
+            while True:
+                # reference loop (partition.py:292-321): max_iters relocations,
+                # stop early on no candidates or on the patience rule
+                if iterations >= params.max_iters:
+                    converged = num_candidates == 0
+                    break
+                if num_candidates == 0:
                     converged = True
                     break
-            else:
-                streak = 0
-            obj_prev = obj_cur
-        else:
-            converged = num_candidates == 0
+                if pending is None:
+                    _relocate_sorted(prefs, lab, sizes, p, cap_limit)
+                    pending = analyze()
+                fut, nc_cur, sizes_cur, smax = pending
+                pending = None
+                iterations += 1
+                speculate = iterations < params.max_iters and nc_cur != 0
+                if speculate:                   # the next iteration, before this one's decision
+                    lab_prev.copy_(lab)
+                    _relocate_sorted(prefs, lab, sizes_cur, p, cap_limit)
+                    pending = analyze()
+                obj_cur = fut.result()
+                trace.append(obj_cur)
+                max_sizes.append(smax)
+                if obj_prev != 0.0:
+                    rel = (obj_cur - obj_prev) / abs(obj_prev)
+                else:
+                    rel = 0.0 if obj_cur == 0.0 else math.inf
+                if rel < params.epsilon:
+                    streak += 1
+                    if streak >= params.patience:
+                        converged = True
+                        if pending is not None:     # undo the speculative relocation
+                            lab.copy_(lab_prev)
+                            pending[0].result()
+                            pending = None
+                        break
+                else:
+                    streak = 0
+                obj_prev = obj_cur
+                num_candidates, sizes = nc_cur, sizes_cur
+        finally:
+            if pending is not None:
+                pending[0].result()
+            pool.shutdown(wait=True)
         out_labels = lab.cpu().numpy().astype(np.int32)
-        del src_ptr, dst_idx, lab, terms, prefs
+        del src_ptr, dst_idx, lab, lab_prev, terms, prefs
     torch.cuda.empty_cache()
     return PartitionResult(labels=out_labels, num_partitions=p, objective_trace=trace,
                            initial_objective=initial_objective, converged=converged,
