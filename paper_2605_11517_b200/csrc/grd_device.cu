@@ -628,15 +628,16 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
                 // the general loop adds j = lane first, then j = lane + 32
                 for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
                 const float scale = gscale ? gscale[r] : 1.0f;
+                const float inv_sum = 1.0f / sum;   // one division per row, not per class
                 if (lane < c) {
-                    float pr = e0 / sum;
+                    float pr = e0 * inv_sum;
                     if (lane == y) pr -= 1.0f;
                     const float gv = pr * inv_count * scale;
                     grow[lane] = gv;
                     if (grow2) grow2[lane] = gv * s2;     // the pull's source scale, pre-applied
                 }
                 if (lane + kWarp < c) {
-                    float pr = e1 / sum;
+                    float pr = e1 * inv_sum;
                     if (lane + kWarp == y) pr -= 1.0f;
                     const float gv = pr * inv_count * scale;
                     grow[lane + kWarp] = gv;
@@ -710,12 +711,13 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
                 }
                 for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
                 const float scale = gscale ? gscale[r] : 1.0f;
+                const float inv_sum = 1.0f / sum;   // one division per row, not per class
                 float ey = 0.f;
 #pragma unroll
                 for (int k = 0; k < NV; ++k) {
                     const int j = lane + k * kWarp;
                     if (j < c) {
-                        float pr = e[k] / sum;
+                        float pr = e[k] * inv_sum;
                         if (j == y) { pr -= 1.0f; ey = e[k]; }
                         const float gv = pr * inv_count * scale;
                         grow[j] = gv;
@@ -770,8 +772,9 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ log
         for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
         const int y = labels[r];
         const float scale = gscale ? gscale[r] : 1.0f;
+        const float inv_sum = 1.0f / sum;
         for (int j = lane; j < c; j += kWarp) {
-            float p = expf(row[j] - mx) / sum;
+            float p = expf(row[j] - mx) * inv_sum;
             if (j == y) p -= 1.0f;
             const float gv = p * inv_count * scale;
             grow[j] = gv;
