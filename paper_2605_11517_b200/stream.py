@@ -343,12 +343,25 @@ class StreamingEngine:
         maxw = max(ld_of(d) for d in self.dims)
         # streamed host rows (features, or a deeper hidden layer kept on the host)
         xw = max([ld_of(F)] + [t.shape[1] for t in self.host_acts.values()])
-        self.xc = [torch.zeros(cr * xw, dtype=torch.float32, device=dev) for _ in range(2)]
+        # GCN whose feature rows fit a layer buffer row: every feature pass
+        # lands in a layer buffer (epoch()), so the two chunk buffers of
+        # streamed rows are never used — their HBM goes to the feature cache
+        self.stash_on = (os.environ.get("GRD_STREAM_STASH", "1") != "0"
+                         and all(ld_of(d) == d for d in self.dims[1:]))
+        self.x_in_buf = (self.stash_on and not (self.sage or self.gat) and not self.host_acts
+                         and self.buf[0].shape[1] == ld_of(F) == self.buf[1].shape[1])
+        self._xc_elems = cr * xw
+        self.xc = None if self.x_in_buf else \
+            [torch.zeros(cr * xw, dtype=torch.float32, device=dev) for _ in range(2)]
         self.ac = ops.zeros_rows(cr, maxw, dev)                       # regathered hidden rows
         self.nc = ops.zeros_rows(cr, maxw, dev)                       # aggregate / pull rows
         self.lc = ops.zeros_rows(cr, last.d_out, dev)                 # logits
         self.gc = ops.zeros_rows(cr, last.d_out, dev)                 # logit gradient
-        self.dc = ops.zeros_rows(cr, maxw, dev)                       # input-gradient rows
+        # input-gradient rows: not needed when every GCN input gradient is
+        # written in place over its H rows (_gemm_rowwise)
+        need_dc = self.sage or self.gat or not all(self._gemm_rowwise(self.cfg[l])
+                                                  for l in range(1, self.L))
+        self.dc = ops.zeros_rows(cr, maxw, dev) if need_dc else None
         self.copy_stream = torch.cuda.Stream(dev)
         self._ready = [torch.cuda.Event() for _ in range(2)]
         self._free = [torch.cuda.Event() for _ in range(2)]
@@ -374,9 +387,6 @@ class StreamingEngine:
         rows = min(self.V, int(x_cache_bytes) // row_bytes)
         rows = max([r1 for _, r1 in sg.chunks if r1 <= rows], default=0)
         self.cache_rows = rows
-        # stash needs the layers to leave no pad columns that must stay zero
-        self.stash_on = (os.environ.get("GRD_STREAM_STASH", "1") != "0"
-                         and all(ld_of(d) == d for d in self.dims[1:]))
         self.x_cache = torch.empty((rows, ld_of(F)), dtype=torch.float32, device=dev) if rows else None
         self.set_features(features)
 
@@ -443,6 +453,9 @@ class StreamingEngine:
                 elif stash_to is not None:      # rows kept in the layer buffer
                     dst, ready, free = stash_to[r0:r1, :width], torch.cuda.Event(), None
                 else:
+                    if self.xc is None:         # first use outside a layer buffer
+                        self.xc = [torch.zeros(self._xc_elems, dtype=torch.float32, device=self.device)
+                                   for _ in range(2)]
                     b = nb & 1
                     nb += 1
                     dst = self.xc[b][: n * width].view(n, width)
@@ -533,7 +546,9 @@ class StreamingEngine:
             if l == 0:
                 self._stream(self.x_src, lambda x, r0, r1: ops.gemm(
                     x, W[0], P[r0:r1], r1 - r0, c.d_out, c.d_in, row_scale=_rows(s, r0, r1)),
-                    stash_from=xb)
+                    stash_from=xb,
+                    # first epoch: the streamed rows land in B[1], which A_1 then overwrites
+                    stash_to=B[1] if (xb is None and self.x_in_buf and self._x_fits(B[1])) else None)
             else:
                 ops.gemm(B[1][:, : c.ld_in], W[l], P, V, c.d_out, c.d_in, row_scale=s)
             sg.exchange(P, c.d_out)                               # halo rows of P
@@ -617,6 +632,8 @@ class StreamingEngine:
             ops.gemm(Hc, self.wts.w[l], out[r0:r1, : c.ld_in], n, c.d_in, c.d_out, trans_b=True,
                      row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
             return
+        if self.dc is None:
+            self.dc = ops.zeros_rows(self.chunk_rows, max(ld_of(d) for d in self.dims), self.device)
         d = self.dc[:n, : c.ld_in]
         ops.gemm(Hc, self.wts.w[l], d, n, c.d_in, c.d_out, trans_b=True,
                  row_scale=_rows(ref_scale, r0, r1), relu_ref=a)
